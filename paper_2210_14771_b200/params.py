@@ -1,0 +1,155 @@
+"""Pipeline tunables with the paper's defaults.
+
+Same field names, defaults and validation as the reference's ``EcaConfig``
+(/root/reference/pkg/src/eca/config.py:14-78).  :meth:`EcaConfig.device_params`
+packs it into the POD ``EcaParams`` struct of ``include/eca_b200.h`` that every
+kernel receives by value.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+from dataclasses import dataclass
+from pathlib import Path
+
+_POSITIVE = ("gradient_threshold", "angle_threshold_deg", "intensity_threshold",
+             "min_point_score", "inlier_distance_px", "min_circle_score",
+             "min_radius_frac", "max_radius_frac", "max_center_offset_frac")
+
+
+@dataclass(frozen=True, slots=True)
+class EcaConfig:
+    strip_count: int = 16
+    strip_weighting: float = 8.0
+    gradient_threshold: float = 20.0
+    angle_threshold_deg: float = 30.0
+    intensity_threshold: float = 25.0
+    edge_margin_px: int = 3
+    min_point_score: float = 0.03
+    inlier_distance_px: float = 3.0
+    min_circle_score: float = 0.06
+    min_circle_score_absolute: bool = False
+    min_radius_frac: float = 0.1
+    max_radius_frac: float = 0.8
+    max_center_offset_frac: float = 0.2
+    ransac_attempts: int = 32
+    ransac_iterations: int = 3
+
+    def __post_init__(self) -> None:   # config.py:41-66
+        if self.strip_count < 4:
+            raise ValueError(f"strip_count must be >= 4, got {self.strip_count}")
+        if self.strip_weighting <= 0:
+            raise ValueError(f"strip_weighting must be positive, got {self.strip_weighting}")
+        for name in _POSITIVE:
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be positive, got {getattr(self, name)}")
+        if self.edge_margin_px < 0:
+            raise ValueError(f"edge_margin_px must be >= 0, got {self.edge_margin_px}")
+        if self.min_radius_frac >= self.max_radius_frac:
+            raise ValueError(f"min_radius_frac must be < max_radius_frac, got "
+                             f"{self.min_radius_frac} >= {self.max_radius_frac}")
+        if self.ransac_attempts < 1 or self.ransac_iterations < 1:
+            raise ValueError("ransac_attempts and ransac_iterations must be >= 1")
+
+    def circle_score_threshold(self) -> float:
+        """Absolute inlier-score sum a fit needs (config.py:69-73)."""
+        if self.min_circle_score_absolute:
+            return self.min_circle_score
+        return self.min_circle_score * self.strip_count
+
+    def device_params(self, width: int, height: int, center=None) -> "EcaParams":
+        """POD copy for the kernels; derived constants use the reference's
+        evaluation order so the GPU sees the same doubles numpy does."""
+        ang = 180.0 / (math.pi * self.angle_threshold_deg)          # handcrafted.py:178
+        cx, cy = ((width - 1) / 2.0, (height - 1) / 2.0) if center is None else center
+        return EcaParams(
+            width=width, height=height, strip_count=self.strip_count,
+            edge_margin_px=self.edge_margin_px, ransac_attempts=self.ransac_attempts,
+            ransac_iterations=self.ransac_iterations,
+            gradient_threshold=self.gradient_threshold,
+            intensity_threshold=self.intensity_threshold,
+            angle_scale=ang, zero_grad_angle=math.pi * ang,
+            min_point_score=self.min_point_score,
+            inlier_tol=self.inlier_distance_px / width,
+            circle_score_threshold=self.circle_score_threshold(),
+            min_radius_frac=self.min_radius_frac, max_radius_frac=self.max_radius_frac,
+            max_center_offset_frac=self.max_center_offset_frac,
+            center_x=cx, center_y=cy,
+        )
+
+
+class EcaParams(ctypes.Structure):
+    """ctypes mirror of ``struct EcaParams`` (include/eca_b200.h)."""
+
+    _fields_ = [
+        ("width", ctypes.c_int32), ("height", ctypes.c_int32),
+        ("strip_count", ctypes.c_int32), ("edge_margin_px", ctypes.c_int32),
+        ("ransac_attempts", ctypes.c_int32), ("ransac_iterations", ctypes.c_int32),
+        ("gradient_threshold", ctypes.c_double), ("intensity_threshold", ctypes.c_double),
+        ("angle_scale", ctypes.c_double), ("zero_grad_angle", ctypes.c_double),
+        ("min_point_score", ctypes.c_double), ("inlier_tol", ctypes.c_double),
+        ("circle_score_threshold", ctypes.c_double),
+        ("min_radius_frac", ctypes.c_double), ("max_radius_frac", ctypes.c_double),
+        ("max_center_offset_frac", ctypes.c_double),
+        ("center_x", ctypes.c_double), ("center_y", ctypes.c_double),
+    ]
+
+
+def config_default() -> EcaConfig:
+    return EcaConfig()
+
+
+_TYPES = {f.name: f.type for f in dataclasses.fields(EcaConfig)}
+
+
+def _parse(name: str, text: str):
+    if name not in _TYPES:
+        raise ValueError(f"unknown config field {name!r}")
+    text = text.strip()
+    kind = _TYPES[name]
+    if kind == "bool":
+        low = text.lower()
+        if low in ("true", "1", "yes"):
+            return True
+        if low in ("false", "0", "no"):
+            return False
+        raise ValueError(f"bad boolean for {name}: {text!r}")
+    return int(text) if kind == "int" else float(text)
+
+
+def apply_overrides(cfg: EcaConfig, overrides: list[str]) -> EcaConfig:
+    """``name=value`` overrides (config.py:137-146)."""
+    vals = {}
+    for item in overrides:
+        if "=" not in item:
+            raise ValueError(f"override must look like name=value, got {item!r}")
+        k, _, v = item.partition("=")
+        vals[k.strip()] = _parse(k.strip(), v)
+    return dataclasses.replace(cfg, **vals)
+
+
+def save_config(cfg: EcaConfig, path) -> None:
+    """Flat ``name = value`` file; floats via repr so they round-trip exactly."""
+    lines = ["# content-area estimation parameters"]
+    for f in dataclasses.fields(EcaConfig):
+        v = getattr(cfg, f.name)
+        lines.append(f"{f.name} = {('true' if v else 'false') if isinstance(v, bool) else repr(v)}")
+    Path(path).write_text("\n".join(lines) + "\n", encoding="utf-8")
+
+
+def load_config(path, base: EcaConfig | None = None) -> EcaConfig:
+    vals = {}
+    for no, raw in enumerate(Path(path).read_text(encoding="utf-8").splitlines(), 1):
+        line = raw.split("#", 1)[0].strip()
+        if not line:
+            continue
+        if "=" not in line:
+            raise ValueError(f"line {no}: expected 'name = value', got {raw!r}")
+        k, _, v = line.partition("=")
+        try:
+            vals[k.strip()] = _parse(k.strip(), v)
+        except ValueError as exc:
+            raise ValueError(f"line {no}: {exc}") from None
+    return dataclasses.replace(base or config_default(), **vals)
