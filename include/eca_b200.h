@@ -1,0 +1,173 @@
+/*
+ * eca_b200.h — C ABI of the B200-native content-area hot path (libeca_b200.so).
+ *
+ * The reference (/root/reference/pkg/src/eca) is pure Python/numpy and has no
+ * FFI of its own; these entry points are what its Python functions would bind
+ * through ctypes.  Each declaration names the reference
+ * function it replaces.
+ *
+ * Conventions
+ *   - Frames are HWC uint8 RGB in DEVICE memory: pixel (b, y, x, c) lives at
+ *     frames + b*frame_stride + y*row_stride + 3*x + c (bytes).  Any strides
+ *     are accepted; contiguous frames use frame_stride = H*W*3, row_stride = W*3.
+ *   - Every pointer except `params`, `strip_rows` and the host-helper outputs is
+ *     a device pointer owned by the caller.  Device calls are asynchronous on
+ *     `stream` (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *   - Return 0 on success or a negative ECA_ERR_* code; nothing throws and no
+ *     call allocates device memory.
+ *   - Candidate arrays are [batch][2*n_strips] in the reference's flatten
+ *     order (estimator.py:69): every strip's left winner, then every right one.
+ */
+#ifndef ECA_B200_H
+#define ECA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ECA_OK 0
+#define ECA_ERR_ARG (-1)         /* bad shape / size / pointer              */
+#define ECA_ERR_CUDA (-2)        /* a CUDA launch or runtime call failed    */
+#define ECA_ERR_UNSUPPORTED (-3) /* outside the supported envelope         */
+
+#define ECA_MAX_STRIPS 128       /* 2*128 candidates per frame              */
+#define ECA_MAX_WIDTH 4096
+#define ECA_MAX_ATTEMPTS 8192
+
+/* RejectionReason (fitting.py:18-36) plus acceptance, as stored in EcaFitRecord.status */
+enum EcaStatus {
+  ECA_ACCEPTED = 0,
+  ECA_NO_CANDIDATES = 1,
+  ECA_LOW_SCORE = 2,
+  ECA_GEOMETRY_GATE = 3
+};
+
+/* POD view of EcaConfig (config.py:14-73) with the derived doubles precomputed
+ * in the reference's evaluation order (params.py: EcaConfig.device_params). */
+typedef struct EcaParams {
+  int32_t width, height;
+  int32_t strip_count, edge_margin_px;
+  int32_t ransac_attempts, ransac_iterations;
+  double gradient_threshold;     /* t_g                                      */
+  double intensity_threshold;    /* t_i                                      */
+  double angle_scale;            /* 180 / (pi * t_theta)   handcrafted.py:178 */
+  double zero_grad_angle;        /* pi * angle_scale       handcrafted.py:182 */
+  double min_point_score;        /* fitting.py:51                           */
+  double inlier_tol;             /* inlier_distance_px / W fitting.py:189    */
+  double circle_score_threshold; /* config.py:69-73                         */
+  double min_radius_frac, max_radius_frac, max_center_offset_frac;
+  double center_x, center_y;     /* fit reference point (fitting.py:186)     */
+} EcaParams;
+
+/* One frame's fit result; 40 bytes; also the NCCL gather record. */
+typedef struct EcaFitRecord {
+  double cx, cy, r;   /* pixels; 0 unless status == ECA_ACCEPTED */
+  double score;       /* inlier score sum                         */
+  int32_t inliers;
+  int32_t status;     /* enum EcaStatus                           */
+} EcaFitRecord;
+
+/* ---------------------------------------------------------------- host ---- */
+
+/* strip_heights (strips.py:41-60).  Writes <= count rows; returns how many
+ * (after de-duplication) or ECA_ERR_ARG. */
+int eca_strip_rows(int height, int count, double weighting, int32_t* out_rows);
+
+/* _sample_triplets (fitting.py:147-156) for every n in [3, max_n]:
+ * out[((n-3)*attempts + a)*3 + j], the three smallest PCG64 keys of attempt a
+ * in ascending key order.  numpy default_rng(seed) stream, bit-exact. */
+int eca_triplet_table(uint64_t seed, int attempts, int max_n, int16_t* out);
+
+/* First `count` doubles of numpy.random.default_rng(seed).random() (test hook). */
+int eca_pcg64_doubles(uint64_t seed, int64_t count, double* out);
+
+/* FP32 prefilter tolerance the handcrafted kernels use for `params`; returns
+ * 0 and writes the relative bound, or 1 when the config needs the all-FP64
+ * path (FP32 range insufficient). */
+int eca_prefilter_bound(const EcaParams* params, double* out_rel_bound);
+
+/* -------------------------------------------------------------- device ---- */
+
+/* Every strip entry point takes `strip_rows` (the strip centre rows y, frame
+ * coordinates: geometry) and optional `band_rows`: the memory row, within each
+ * frame buffer, that holds row y-1 (handcrafted) / y-3 (learned).  NULL means
+ * full frames (band = y-1 / y-3).  Non-NULL lets the kernels read compact
+ * strip-row buffers produced by eca_h2d_bands. */
+
+/* Frame ingest: copy rows [first_rows[k], first_rows[k]+rows_per_band) of every
+ * HOST frame into dev as [batch][n_bands*rows_per_band][width][3] (packed),
+ * one strided cudaMemcpy2DAsync per band (pinned host memory for async). */
+int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_stride,
+                  int64_t host_row_stride, const int32_t* first_rows, int n_bands,
+                  int rows_per_band, int width, uint8_t* dev, void* stream);
+
+/* score_frame_strips + select_candidates_batch, handcrafted variant
+ * (estimator.py:35-52, handcrafted.py:148-205, 120-138). */
+int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
+                           int64_t row_stride, const int32_t* strip_rows,
+                           const int32_t* band_rows, int n_strips,
+                           const EcaParams* params, int32_t* out_x, int32_t* out_y,
+                           double* out_score, void* stream);
+
+/* Same, plus every column's FP64 score: out_scores[batch][n_strips][width]
+ * (StripScoreRow.scores, handcrafted.py:25-31). */
+int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
+                               int64_t row_stride, const int32_t* strip_rows,
+                               const int32_t* band_rows, int n_strips,
+                               const EcaParams* params, double* out_scores, int32_t* out_x,
+                               int32_t* out_y, double* out_score, void* stream);
+
+/* filter_candidates + ransac_fit (fitting.py:39-52, 159-230) per frame.
+ * triplets: device copy of eca_triplet_table(seed, attempts, n_cand) (ignored
+ * when exhaustive != 0, which enumerates all C(n,3) triplets in order). */
+int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const double* cand_score,
+            int batch, int n_cand, const EcaParams* params, const int16_t* triplets,
+            int exhaustive, EcaFitRecord* out, void* stream);
+
+/* estimate() for a batch in ONE launch (estimator.py:55-74): strip scoring,
+ * candidates, filter, RANSAC.  `counters` = batch int32 zeros (left zeroed on
+ * return).  The candidate outputs double as the fitter's input staging. */
+int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
+                             int64_t row_stride, const int32_t* strip_rows,
+                             const int32_t* band_rows, int n_strips,
+                             const EcaParams* params, const int16_t* triplets,
+                             int32_t* counters, int32_t* out_x, int32_t* out_y,
+                             double* out_score, EcaFitRecord* out, void* stream);
+
+/* ---- learned variant (edgenet.py:67-83, 100-116, 182-233, 347-370) ---- */
+
+/* Packed FP32 weights: k0[8*5*9] b0[8] k1[16*8*9] b1[16] k2[32*16*9] b2[32]
+  * k3[32] b3[1] (reference (out,in,kh,kw) order) = 6209 floats; norm = mean[3], std[3]. */
+#define ECA_NET_FLOATS 6209
+int eca_points_learned(const uint8_t* frames, int batch, int64_t frame_stride,
+                       int64_t row_stride, const int32_t* strip_rows,
+                       const int32_t* band_rows, int n_strips,
+                       int height, int width, const float* weights, const double* norm,
+                       float* out_probs /* [batch][n_strips][width-6] */,
+                       int32_t* out_x, int32_t* out_y, double* out_score, void* stream);
+
+/* -------------------------------------------------------- mask / crop ---- */
+
+/* Vectorised circle_contains (geometry.py:30-34): out[b][y][x] = 1 inside the
+ * closed disk of an ACCEPTED record, all ones otherwise (FullFrame). */
+int eca_draw_mask(const EcaFitRecord* fits, int batch, int height, int width,
+                  uint8_t* out, int64_t out_frame_stride, void* stream);
+
+/* crop_augment bounds (dataset.py:151-187): out_bounds[b] = {x0, y0, x1, y1}
+ * inclusive, or {-1,-1,-1,-1} when the reference returns None / the record is
+ * not ACCEPTED. */
+int eca_crop_bounds(const EcaFitRecord* fits, int batch, int height, int width,
+                    int32_t* out_bounds, void* stream);
+
+/* Copy each frame's rectangle (bounds from eca_crop_bounds) to
+ * out + out_offsets[b] as a packed HWC crop; max_rows >= the tallest crop. */
+int eca_crop_copy(const uint8_t* frames, int batch, int64_t frame_stride, int64_t row_stride,
+                  const int32_t* bounds, const int64_t* out_offsets, uint8_t* out,
+                  int max_rows, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECA_B200_H */

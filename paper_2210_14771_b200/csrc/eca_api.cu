@@ -1,0 +1,210 @@
+// C ABI entry points of libeca_b200.so (declared in include/eca_b200.h):
+// argument validation, launch geometry and kernel dispatch.  No entry point
+// allocates device memory or synchronises the stream.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "eca_fit.cuh"
+#include "eca_strip.cuh"
+
+using namespace eca;
+
+namespace {
+
+constexpr int kStages = 2;
+
+int sm_count() {
+  static int count[64];
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::call_once(once[dev], [dev] {
+    int c = 0;
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    count[dev] = c > 0 ? c : 148;
+  });
+  return count[dev];
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_launch() { return cudaGetLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA; }
+
+// Fill the geometry/precision part of a StripJob; returns ECA_OK or an error.
+int prepare_strip_job(StripJob& J, const uint8_t* frames, int batch, int64_t frame_stride,
+                      int64_t row_stride, const int32_t* strip_rows, const int32_t* band_rows,
+                      int n_strips, const EcaParams* params, bool force_exact) {
+  if (!frames || !strip_rows || !params || batch < 0) return ECA_ERR_ARG;
+  const int W = params->width, H = params->height;
+  if (W < 8 || H < 14) return ECA_ERR_ARG;
+  if (H > 32767 || W > ECA_MAX_WIDTH || n_strips < 1 || n_strips > ECA_MAX_STRIPS) return ECA_ERR_UNSUPPORTED;
+  if (row_stride < 3LL * W || frame_stride < 0) return ECA_ERR_ARG;
+  if (batch > 0 && int64_t(batch) * n_strips > (int64_t(1) << 30)) return ECA_ERR_UNSUPPORTED;
+  std::memset(&J, 0, sizeof(J));
+  J.frames = frames;
+  J.frame_stride = frame_stride;
+  J.row_stride = row_stride;
+  J.batch = batch;
+  J.n_strips = n_strips;
+  J.nthreads = ((W + kPx - 1) / kPx + 31) / 32 * 32;
+  J.rowcap = (24 * J.nthreads + 48 + 15) / 16 * 16;
+  J.sumcap = J.nthreads * kPx + 16;
+  J.contiguous = (row_stride == 3LL * W) ? 1 : 0;
+  J.p = *params;
+  for (int k = 0; k < n_strips; ++k) {
+    if (strip_rows[k] < 3 || strip_rows[k] > H - 4) return ECA_ERR_ARG;
+    J.rows[k] = int16_t(strip_rows[k]);
+    const int band = band_rows ? band_rows[k] : strip_rows[k] - 1;
+    if (band < 0 || band > 32767) return ECA_ERR_ARG;
+    J.band[k] = int16_t(band);
+  }
+  double bound = 0.0;
+  const int risky = eca_prefilter_bound(params, &bound);
+  const double log2e = 1.4426950408889634;
+  J.window = std::nextafter(float(1.0 - bound), 0.0f);
+  J.kT = float(-2.0 * log2e / (3.0 * params->gradient_threshold));
+  J.kA = float(2.0 * params->angle_scale * log2e);
+  J.tau = (risky || force_exact) ? INFINITY : float(1e-11 * 20.0 / params->gradient_threshold);
+  for (int s = 0; s < kDTab; ++s) {
+    const double pre = (s < 766 ? s : 765) / 3.0;
+    J.dtab[s] = float(2.0 / (1.0 + std::exp(2.0 * pre / params->intensity_threshold)));
+  }
+  return ECA_OK;
+}
+
+template <bool kRows, bool kFused>
+int launch_strips(const StripJob& J, cudaStream_t stream) {
+  if (J.batch == 0) return ECA_OK;
+  auto kern = strip_kernel<kStages, kRows, kFused>;
+  const size_t smem = strip_smem_bytes<kStages>(J.rowcap, J.sumcap, kFused);
+  static std::once_flag once;
+  std::call_once(once, [kern] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, J.nthreads, smem) !=
+          cudaSuccess ||
+      per_sm < 1)
+    return ECA_ERR_CUDA;
+  const int items = J.batch * J.n_strips;
+  const int grid = items < sm_count() * per_sm ? items : sm_count() * per_sm;
+  kern<<<grid, J.nthreads, smem, stream>>>(J);
+  return check_launch();
+}
+
+struct FitJob {
+  const int32_t* x;
+  const int32_t* y;
+  const double* s;
+  int n_cand, exhaustive;
+  EcaParams p;
+  const int16_t* trip;
+  EcaFitRecord* out;
+};
+
+__global__ void __launch_bounds__(512) fit_kernel(const __grid_constant__ FitJob J) {
+  __shared__ FitScratch fs;
+  const size_t o = size_t(blockIdx.x) * J.n_cand;
+  fit_frame(J.x + o, J.y + o, J.s + o, J.n_cand, false, J.p, J.trip, J.exhaustive, &fs,
+            J.out + blockIdx.x);
+}
+
+}  // namespace
+
+extern "C" int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
+                                      int64_t row_stride, const int32_t* strip_rows,
+                                      const int32_t* band_rows, int n_strips, const EcaParams* params, int32_t* out_x,
+                                      int32_t* out_y, double* out_score, void* stream) {
+  StripJob J;
+  int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
+                             n_strips, params, false);
+  if (rc) return rc;
+  if (!out_x || !out_y || !out_score) return ECA_ERR_ARG;
+  J.out_x = out_x;
+  J.out_y = out_y;
+  J.out_score = out_score;
+  return launch_strips<false, false>(J, as_stream(stream));
+}
+
+extern "C" int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
+                                          int64_t row_stride, const int32_t* strip_rows,
+                                          const int32_t* band_rows, int n_strips, const EcaParams* params,
+                                          double* out_scores, int32_t* out_x, int32_t* out_y,
+                                          double* out_score, void* stream) {
+  StripJob J;
+  int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
+                             n_strips, params, true);
+  if (rc) return rc;
+  if (!out_scores || !out_x || !out_y || !out_score) return ECA_ERR_ARG;
+  J.out_rows = out_scores;
+  J.out_x = out_x;
+  J.out_y = out_y;
+  J.out_score = out_score;
+  return launch_strips<true, false>(J, as_stream(stream));
+}
+
+extern "C" int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const double* cand_score,
+                       int batch, int n_cand, const EcaParams* params, const int16_t* triplets,
+                       int exhaustive, EcaFitRecord* out, void* stream) {
+  if (batch < 0 || n_cand < 0 || n_cand > 2 * ECA_MAX_STRIPS || !params) return ECA_ERR_ARG;
+  if (batch == 0) return ECA_OK;
+  if (!cand_x || !cand_y || !cand_score || !out || (!exhaustive && !triplets)) return ECA_ERR_ARG;
+  if (params->ransac_attempts < 1 || params->ransac_attempts > ECA_MAX_ATTEMPTS ||
+      params->ransac_iterations < 1)
+    return ECA_ERR_ARG;
+  if (batch > 0x7fffffff) return ECA_ERR_UNSUPPORTED;
+  FitJob J{cand_x, cand_y, cand_score, n_cand, exhaustive ? 1 : 0, *params, triplets, out};
+  fit_kernel<<<batch, 512, 0, as_stream(stream)>>>(J);
+  return check_launch();
+}
+
+extern "C" int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
+                                        int64_t row_stride, const int32_t* strip_rows,
+                                        const int32_t* band_rows, int n_strips, const EcaParams* params,
+                                        const int16_t* triplets, int32_t* counters,
+                                        int32_t* out_x, int32_t* out_y, double* out_score,
+                                        EcaFitRecord* out, void* stream) {
+  StripJob J;
+  int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
+                             n_strips, params, false);
+  if (rc) return rc;
+  if (!triplets || !counters || !out || !out_x || !out_y || !out_score) return ECA_ERR_ARG;
+  if (params->ransac_attempts < 1 || params->ransac_attempts > ECA_MAX_ATTEMPTS ||
+      params->ransac_iterations < 1)
+    return ECA_ERR_ARG;
+  J.out_x = out_x;
+  J.out_y = out_y;
+  J.out_score = out_score;
+  J.triplets = triplets;
+  J.counters = counters;
+  J.out_fit = out;
+  return launch_strips<false, true>(J, as_stream(stream));
+}
+
+extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_stride,
+                             int64_t host_row_stride, const int32_t* first_rows, int n_bands,
+                             int rows_per_band, int width, uint8_t* dev, void* stream) {
+  if (batch < 0 || n_bands < 0 || rows_per_band < 1 || width < 1) return ECA_ERR_ARG;
+  if (batch == 0 || n_bands == 0) return ECA_OK;
+  if (!host || !first_rows || !dev || host_row_stride < 3LL * width) return ECA_ERR_ARG;
+  const size_t row_bytes = size_t(3) * width;
+  const size_t band_bytes = row_bytes * rows_per_band;
+  const size_t dev_frame = band_bytes * n_bands;
+  auto st = as_stream(stream);
+  for (int k = 0; k < n_bands; ++k) {
+    for (int r = 0; r < rows_per_band; ++r) {
+      // one strided DMA per (band, row) across every frame of the batch; a whole
+      // band in one DMA when the host rows are packed
+      const bool packed = host_row_stride == int64_t(row_bytes);
+      if (packed && r > 0) break;
+      const uint8_t* src = host + int64_t(first_rows[k] + r) * host_row_stride;
+      uint8_t* dst = dev + k * band_bytes + r * row_bytes;
+      const size_t w = packed ? band_bytes : row_bytes;
+      if (cudaMemcpy2DAsync(dst, dev_frame, src, size_t(host_frame_stride), w, size_t(batch),
+                            cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return ECA_ERR_CUDA;
+    }
+  }
+  return ECA_OK;
+}

@@ -1,0 +1,167 @@
+"""Fixed-shape batched estimator: preallocated buffers, CUDA-graph replay and
+strip-rows-only host ingest.  This is the throughput / latency path the bench
+drives; the list-based API in ``api.py`` is built from the same calls.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib, api
+from .params import EcaConfig, config_default
+
+
+class ContentAreaEngine:
+    """estimate() for batches of ``batch`` frames of one (height, width).
+
+    ``run(frames)``      frames already on the GPU (B,H,W,3) uint8 -> (B,5) records
+    ``run_host(frames)`` pinned host frames: H2D of the strip rows only, one
+                         fused launch, D2H of the 40-byte records
+    ``capture(frames)``  record a CUDA graph of run(frames) for ``replay()``
+    Records are EcaFitRecord rows (cx, cy, r, score, inliers|status).
+    """
+
+    def __init__(self, height: int, width: int, batch: int, cfg: EcaConfig | None = None,
+                 seed: int = 0, variant: api.EstimatorVariant = api.HANDCRAFTED, device=None):
+        self.cfg = cfg or config_default()
+        self.height, self.width, self.batch = height, width, batch
+        self.device = api._device(device)
+        self.variant = variant
+        self.seed = seed
+        self.rows = api.strip_heights(height, self.cfg.strip_count, self.cfg.strip_weighting)
+        s = self.n_strips = len(self.rows)
+        self.half = api.HALF_WINDOW if isinstance(variant, api.Learned) else 1
+        self._rows = api._i32_array(self.rows)
+        self._first = api._i32_array([r - self.half for r in self.rows])
+        rpb = 2 * self.half + 1
+        self._band = api._i32_array([k * rpb for k in range(s)])
+        self.params = self.cfg.device_params(width, height)
+        d = self.device
+        self.trip = api._dev_triplets(seed, self.cfg.ransac_attempts, 2 * s, d)
+        self.counters = torch.zeros(batch, dtype=torch.int32, device=d)
+        self.xs = torch.empty((batch, 2 * s), dtype=torch.int32, device=d)
+        self.ys = torch.empty_like(self.xs)
+        self.sc = torch.empty((batch, 2 * s), dtype=torch.float64, device=d)
+        self.rec = torch.empty((batch, 5), dtype=torch.float64, device=d)
+        self.bands = torch.empty((batch, s * rpb, width, 3), dtype=torch.uint8, device=d)
+        self.rec_host = torch.empty((batch, 5), dtype=torch.float64, pin_memory=True)
+        if isinstance(variant, api.Learned):
+            self.probs = torch.empty((batch, s, width - 6), dtype=torch.float32, device=d)
+            self.w_dev, self.norm = api._dev_net(variant.net, d)
+        self.graph = None
+        self.launches_per_run = 2 if isinstance(variant, api.Learned) else 1
+        if isinstance(variant, api.Learned):
+            self.launches_per_run = 3
+
+    # ------------------------------------------------------------ launches
+    def _launch(self, ptr: int, fstride: int, rstride: int, band) -> None:
+        lib = _lib.load()
+        st = api._stream(self.device)
+        s = self.n_strips
+        if isinstance(self.variant, api.Learned):
+            rc = lib.eca_points_learned(ctypes.c_void_p(ptr), self.batch, fstride, rstride, self._rows,
+                                        band, s, self.height, self.width, api._ptr(self.w_dev),
+                                        self.norm, api._ptr(self.probs), api._ptr(self.xs),
+                                        api._ptr(self.ys), api._ptr(self.sc), st)
+            _lib.check(rc, "eca_points_learned")
+            rc = lib.eca_fit(api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), self.batch,
+                             2 * s, ctypes.byref(self.params), api._ptr(self.trip), 0,
+                             api._ptr(self.rec), st)
+            _lib.check(rc, "eca_fit")
+            return
+        rc = lib.eca_estimate_handcrafted(ctypes.c_void_p(ptr), self.batch, fstride, rstride,
+                                          self._rows, band, s, ctypes.byref(self.params),
+                                          api._ptr(self.trip), api._ptr(self.counters),
+                                          api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc),
+                                          api._ptr(self.rec), st)
+        _lib.check(rc, "eca_estimate_handcrafted")
+
+    def _check_frames(self, frames: torch.Tensor) -> torch.Tensor:
+        if frames.dim() == 3:
+            frames = frames.unsqueeze(0)
+        if tuple(frames.shape) != (self.batch, self.height, self.width, 3) or frames.dtype != torch.uint8:
+            raise ValueError(f"expected uint8 frames of shape {(self.batch, self.height, self.width, 3)}, "
+                             f"got {tuple(frames.shape)} {frames.dtype}")
+        if frames.stride(3) != 1 or frames.stride(2) != 3:
+            frames = frames.contiguous()
+        return frames
+
+    def run(self, frames: torch.Tensor) -> torch.Tensor:
+        """Frames on this GPU -> device records (asynchronous)."""
+        f = self._check_frames(frames)
+        if f.device != self.device:
+            raise ValueError(f"frames must live on {self.device}")
+        self._launch(f.data_ptr(), f.stride(0), f.stride(1), None)
+        return self.rec
+
+    def ingest(self, host_frames) -> None:
+        """Strip-row H2D copies of a pinned host batch into ``self.bands``."""
+        a = host_frames
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda:
+                raise ValueError("ingest() takes host frames")
+            ptr, fs, rs = a.data_ptr(), a.stride(0), a.stride(1)
+            ok = a.stride(3) == 1 and a.stride(2) == 3
+        else:
+            ptr, fs, rs = a.ctypes.data, a.strides[0], a.strides[1]
+            ok = a.strides[3] == 1 and a.strides[2] == 3
+        if tuple(a.shape) != (self.batch, self.height, self.width, 3) or not ok:
+            raise ValueError("host frames must be (B,H,W,3) uint8 with packed pixels")
+        rc = _lib.load().eca_h2d_bands(ctypes.c_void_p(ptr), self.batch, fs, rs, self._first,
+                                       self.n_strips, 2 * self.half + 1, self.width,
+                                       api._ptr(self.bands), api._stream(self.device))
+        _lib.check(rc, "eca_h2d_bands")
+
+    def run_bands(self) -> torch.Tensor:
+        self._launch(self.bands.data_ptr(), self.bands.stride(0), self.bands.stride(1), self._band)
+        return self.rec
+
+    def run_host(self, host_frames) -> torch.Tensor:
+        """Pinned host frames -> pinned host records (synchronises the stream)."""
+        self.ingest(host_frames)
+        self.run_bands()
+        self.rec_host.copy_(self.rec, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return self.rec_host
+
+    # --------------------------------------------------------------- graphs
+    def capture(self, frames: torch.Tensor) -> None:
+        """Capture run(frames) (fixed input pointer) into a CUDA graph."""
+        f = self._check_frames(frames)
+        self._graph_input = f
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self._launch(f.data_ptr(), f.stride(0), f.stride(1), None)   # warm-up, attributes
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._launch(f.data_ptr(), f.stride(0), f.stride(1), None)
+        self.graph = g
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.rec
+
+    # --------------------------------------------------------------- results
+    def results(self, rec: torch.Tensor | None = None):
+        return api._records_to_results(self.rec if rec is None else rec)
+
+    def fits(self, rec: torch.Tensor | None = None):
+        return api.records_to_fits(self.rec if rec is None else rec)
+
+    @staticmethod
+    def status(rec: torch.Tensor) -> torch.Tensor:
+        return rec.view(torch.int32).view(rec.shape[0], 10)[:, 9]
+
+
+def records_numpy(rec: torch.Tensor) -> np.ndarray:
+    """(B,5) float64 records -> structured numpy array (cx, cy, r, score, inliers, status)."""
+    r = rec.detach().cpu().numpy()
+    dt = np.dtype([("cx", "<f8"), ("cy", "<f8"), ("r", "<f8"), ("score", "<f8"),
+                   ("inliers", "<i4"), ("status", "<i4")])
+    return r.view(dt).reshape(len(r))

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path against the reference's golden fixtures and the
+CPU oracle on the same inputs.  Tolerances:
+  candidates (x, y, side) exact; |d score| <= max(8 ulp, 1e-12)
+  fit status + inlier count exact; cx, cy, r within 1e-3 px; score rel 1e-12
+  masks / crop bounds bit-exact; learned probabilities within 1e-5.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2210_14771_b200 as eb
+from oracle import eca_oracle as orc
+from paper_2210_14771_b200 import synth
+
+from ._fixtures import case_cfg, frame_cases, load_json, load_npz, make_frame, sha
+
+pytestmark = pytest.mark.gpu
+
+SCORE_ULPS = 8
+SCORE_ABS = 1e-12
+PX_TOL = 1e-3
+
+
+def close_scores(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    tol = np.maximum(SCORE_ULPS * np.spacing(np.abs(b)), SCORE_ABS)
+    return np.abs(a - b) <= tol
+
+
+def assert_fit_equal(got, want, ctx=""):
+    """got: FitResult; want: oracle tuple (status, cx, cy, r, score, inliers)."""
+    st = want[0]
+    if st == 0:
+        assert isinstance(got, eb.Accepted), (ctx, got, want)
+        assert abs(got.circle.cx - want[1]) <= PX_TOL, (ctx, got, want)
+        assert abs(got.circle.cy - want[2]) <= PX_TOL, (ctx, got, want)
+        assert abs(got.circle.r - want[3]) <= PX_TOL, (ctx, got, want)
+        assert got.score == pytest.approx(want[4], rel=1e-12), (ctx, got, want)
+        assert got.inlier_count == want[5], (ctx, got, want)
+    else:
+        code = {1: eb.RejectionReason.NO_CANDIDATES, 2: eb.RejectionReason.LOW_SCORE,
+                3: eb.RejectionReason.GEOMETRY_GATE}[st]
+        assert got == eb.Rejected(code), (ctx, got, want)
+
+
+def fit_tuple_of_area(area):
+    return area
+
+
+SMALL = frame_cases(max_pixels=1000 * 600)
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: c["name"])
+def test_candidates_match_reference(case):
+    frame = make_frame(case["recipe"])
+    assert sha(frame) == case["sha256"]
+    cfg = case_cfg(case)
+    pts = eb.get_points(frame, cfg=cfg)
+    s = len(case["rows"])
+    assert [p.x for p in pts] == case["cand_x"]
+    assert [p.y for p in pts] == case["cand_y"]
+    assert [p.side for p in pts] == [eb.Side.LEFT] * s + [eb.Side.RIGHT] * s
+    assert close_scores([p.score for p in pts], case["cand_score"]).all()
+
+
+@pytest.mark.parametrize("case", [c for c in SMALL if c["name"] in load_npz("scores.npz")],
+                         ids=lambda c: c["name"])
+def test_score_rows_match_reference(case):
+    frame = make_frame(case["recipe"])
+    rows, size = eb.score_frame_strips(frame, cfg=case_cfg(case))
+    got = np.stack([r.scores for r in rows])
+    want = load_npz("scores.npz")[case["name"]]
+    assert size == (frame.shape[1], frame.shape[0])
+    ok = close_scores(got, want)
+    assert ok.all(), (np.argwhere(~ok)[:5], got[~ok][:5], want[~ok][:5])
+    assert [r.left_best.x for r in rows] + [r.right_best.x for r in rows] == case["cand_x"]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: c["name"])
+def test_estimate_matches_reference(case):
+    frame = make_frame(case["recipe"])
+    cfg = case_cfg(case)
+    area = eb.estimate(frame, cfg=cfg, seed=case["seed"])
+    if case["estimate"] is None:
+        assert area == eb.FULL_FRAME
+    else:
+        assert isinstance(area, eb.CircularArea)
+        cx, cy, r, s = case["estimate"]
+        assert abs(area.circle.cx - cx) <= PX_TOL and abs(area.circle.cy - cy) <= PX_TOL
+        assert abs(area.circle.r - r) <= PX_TOL
+        assert area.score == pytest.approx(s, rel=1e-12)
+
+
+def test_fits_match_reference():
+    fails = []
+    for i, c in enumerate(load_json("fits.json")):
+        cfg = eb.EcaConfig(**c["cfg"])
+        cands = [eb.EdgeCandidate(x, y, s, eb.Side.LEFT) for x, y, s in zip(c["x"], c["y"], c["s"])]
+        center = tuple(c["center"]) if c["center"] is not None else None
+        got = eb.ransac_fit(cands, (c["w"], c["h"]), cfg, c["seed"], exhaustive=c["exhaustive"],
+                            center=center)
+        try:
+            assert_fit_equal(got, c["fit"], i)
+        except AssertionError as e:
+            fails.append(str(e)[:300])
+    assert not fails, fails[:5]
+
+
+@pytest.mark.parametrize("case", [c for c in frame_cases() if c not in SMALL], ids=lambda c: c["name"])
+def test_large_frames_match_reference(case):
+    """1080p (C1, C2 head) and 4K edge cases (C4) against the reference fixtures."""
+    frame = make_frame(case["recipe"])
+    assert sha(frame) == case["sha256"]
+    t = torch.from_numpy(frame).cuda()
+    pts = eb.get_points(t)
+    assert [p.x for p in pts] == case["cand_x"]
+    assert close_scores([p.score for p in pts], case["cand_score"]).all()
+    fit = eb.fit_area(pts, (frame.shape[1], frame.shape[0]), seed=case["seed"])
+    assert_fit_equal(fit, case["fit"], case["name"])
+
+
+def test_host_ingest_equals_device_frames():
+    """numpy frames ship strip rows only; results equal the device-resident path."""
+    specs = synth.bench_specs(6, 640, 480, seed=4)
+    frames = np.stack([synth.render(s, 50 + k) for k, (_, s) in enumerate(specs)])
+    a = eb.estimate_batch(list(frames))
+    b = eb.estimate_batch(torch.from_numpy(frames).cuda())
+    assert a == b
+    eng = eb.ContentAreaEngine(480, 640, len(frames))
+    host = torch.from_numpy(frames).pin_memory()
+    rec_h = eng.run_host(host).clone()
+    rec_d = eng.run(torch.from_numpy(frames).cuda()).cpu()
+    assert torch.equal(rec_h, rec_d)
+    assert eng.results(rec_d) == a
+
+
+def test_batch_mixed_sizes_and_errors():
+    f1 = synth.render(synth.bench_spec("clean", np.random.default_rng(1), 320, 240), 3)
+    f2 = synth.render(synth.bench_spec("dark", np.random.default_rng(2), 640, 480), 4)
+    bad = np.zeros((4, 4, 3), dtype=np.uint8)
+    out = eb.estimate_batch([f1, bad, f2, f1])
+    assert isinstance(out[1], eb.FrameError) and out[1].index == 1
+    assert out[0] == out[3]
+    cfg = eb.EcaConfig()
+    for f, o in [(f1, out[0]), (f2, out[2])]:
+        st, cx, cy, r, s, n = orc.estimate(f, cfg, 0)
+        if st == 0:
+            assert abs(o.circle.cx - cx) <= PX_TOL and abs(o.circle.r - r) <= PX_TOL
+        else:
+            assert o == eb.FULL_FRAME
+    assert eb.estimate_batch([]) == []
+
+
+def test_c2_batch_1080p_vs_oracle():
+    """The bench workload (C2): 1080p mix through one fused launch vs the oracle."""
+    specs = synth.bench_specs(24, 1920, 1080, seed=2024)
+    frames = np.stack([synth.render(s, 30000 + k) for k, (_, s) in enumerate(specs)])
+    eng = eb.ContentAreaEngine(1080, 1920, len(frames))
+    rec = eng.run(torch.from_numpy(frames).cuda())
+    got = eng.fits(rec)
+    xs = eng.xs.cpu().numpy()
+    cfg = eb.EcaConfig()
+    for k in range(len(frames)):
+        ox, oy, osc, rows, _ = orc.handcrafted_candidates(frames[k], cfg)
+        assert xs[k].tolist() == ox.tolist(), k
+        assert close_scores(eng.sc[k].cpu().numpy(), osc).all(), k
+        keep = orc.keep_mask(ox, oy, osc, 1920, 1080, cfg)
+        want = orc.ransac(ox[keep], oy[keep], osc[keep], 1920, 1080, cfg, 0)
+        assert_fit_equal(got[k], want, k)
+
+
+def test_graph_replay_matches_direct():
+    frame = synth.c1_frame()
+    t = torch.from_numpy(frame).cuda().unsqueeze(0)
+    eng = eb.ContentAreaEngine(1080, 1920, 1)
+    direct = eng.run(t).clone()
+    eng.capture(t)
+    for _ in range(3):
+        rep = eng.replay().clone()
+        assert torch.equal(rep, direct)
+    assert eng.fits(direct)[0] == eb.fit_area(eb.get_points(frame), (1920, 1080))
+
+
+def test_learned_matches_reference():
+    npz = load_npz("learned.npz")
+    net = eb.EdgeNet(eb.ChannelStats([100.0] * 3, [50.0] * 3), seed=0)
+    for i in range(4):
+        assert np.array_equal(net.layers[i].kernel, npz[f"w{i}"])
+    assert eb.save_weights(net) == npz["blob"].tobytes()
+    agree = total = 0
+    for c in load_json("learned.json"):
+        frame = make_frame(c["recipe"])
+        rows, _ = eb.score_frame_strips(frame, eb.Learned(net))
+        got = np.stack([r.scores for r in rows])
+        want = npz[c["name"]]
+        assert np.abs(got - want).max() <= 1e-5
+        xs = [r.left_best.x for r in rows] + [r.right_best.x for r in rows]
+        for k, (gx, wx) in enumerate(zip(xs, c["cand_x"])):
+            total += 1
+            if gx == wx:
+                agree += 1
+            else:   # a disagreement must be a near-tie in the reference's own scores
+                row = want[k % len(rows)]
+                assert abs(row[gx] - row[wx]) <= 2e-6 * max(row[wx], 1e-30), (c["name"], k)
+    assert agree / total >= 0.9
+
+
+def test_mask_bit_exact_vs_oracle():
+    rng = np.random.default_rng(0)
+    circles = [eb.Circle(319.5, 239.5, 200.0), eb.Circle(10.25, 400.75, 333.3),
+               eb.Circle(320.0, 240.0, 100.0), eb.Circle(-50.0, 240.0, 80.0),
+               eb.Circle(319.5, 239.5, 0.5), eb.Circle(0.0, 0.0, 1e-3)]
+    circles += [eb.Circle(float(rng.uniform(-100, 740)), float(rng.uniform(-100, 580)),
+                          float(rng.uniform(0.1, 600))) for _ in range(40)]
+    areas = [eb.CircularArea(c, 1.0) for c in circles] + [eb.FULL_FRAME]
+    masks = eb.draw_mask(areas, 480, 640).cpu().numpy()
+    for m, c in zip(masks, circles):
+        assert np.array_equal(m, orc.disk_mask(c.cx, c.cy, c.r, 480, 640)), c
+    assert masks[-1].all()
+    odd = eb.draw_mask(eb.CircularArea(eb.Circle(50.3, 20.7, 17.0), 1.0), 41, 101).cpu().numpy()
+    assert np.array_equal(odd, orc.disk_mask(50.3, 20.7, 17.0, 41, 101))
+
+
+def test_crop_bounds_match_reference():
+    fails = []
+    for c in load_json("crops.json"):
+        got = eb.crop_bounds([eb.Circle(*c["circle"])], c["h"], c["w"])[0]
+        want = tuple(c["bounds"]) if c["bounds"] is not None else None
+        if got != want:
+            fails.append((c, got))
+    assert not fails, fails[:3]
+
+
+def test_crop_area_copies_pixels():
+    frame = synth.c1_frame()
+    area = eb.estimate(frame)
+    crop = eb.crop_area(frame, area)
+    x0, y0, x1, y1 = orc.crop_bounds(area.circle.cx, area.circle.cy, area.circle.r, 1920, 1080)
+    assert np.array_equal(crop.cpu().numpy(), frame[y0:y1 + 1, x0:x1 + 1])
+    with pytest.raises(ValueError):
+        eb.crop_area(frame, eb.FULL_FRAME)

@@ -1,0 +1,117 @@
+"""CPU-only checks of libeca_b200.so: it loads, exports every symbol the
+header declares, and its host helpers (strip rows, PCG64 triplet tables,
+prefilter bound) match the reference fixtures.  No device calls."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2210_14771_b200 import EcaConfig, _lib, api
+
+from ._fixtures import load_json, load_npz
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "eca_b200.h"
+
+
+def header_functions():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return re.findall(r"^\s*int\s+(eca_\w+)\s*\(", text, flags=re.M)
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    names = header_functions()
+    assert len(names) >= 12
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_lib.SIGNATURES), "ctypes table out of sync with the header"
+
+
+def test_strip_rows_match_reference():
+    for c in load_json("strip_rows.json"):
+        assert api.strip_heights(c["H"], c["S"], c["alpha"]) == c["rows"], c
+
+
+@pytest.mark.parametrize("h,s,a", [(13, 16, 8.0), (100, 1, 8.0), (100, 16, 0.0)])
+def test_strip_rows_reject_bad_arguments(h, s, a):
+    with pytest.raises(ValueError):
+        api.strip_heights(h, s, a)
+
+
+def test_pcg64_stream_matches_numpy():
+    lib = _lib.load()
+    for seed in [0, 1, 7, 12345, 2**32 + 5, 2**63 - 1]:
+        out = np.empty(257)
+        lib.eca_pcg64_doubles(seed, len(out), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        assert np.array_equal(out, np.random.default_rng(seed).random(len(out))), seed
+
+
+def test_triplet_tables_match_reference():
+    for key, ref in load_npz("triplets.npz").items():
+        seed, att, n = (int(p[1:]) for p in key.split("_"))
+        mine = api.triplet_table(seed, att, n)[n - 3]
+        # same 3-subsets always; same order on this host (numpy argpartition
+        # returns the 3 smallest keys ascending here)
+        assert [sorted(r) for r in mine.tolist()] == [sorted(r) for r in ref.tolist()], key
+        assert np.array_equal(mine, ref), key
+
+
+def test_triplet_order_is_ascending_key():
+    for seed in [0, 3, 99]:
+        for n in [3, 4, 9, 32, 64]:
+            keys = np.random.default_rng(seed).random((32, n))
+            want = np.argsort(keys, axis=1, kind="stable")[:, :3]
+            assert np.array_equal(api.triplet_table(seed, 32, n)[n - 3], want)
+
+
+def test_prefilter_bound_default_and_risky():
+    lib = _lib.load()
+    b = ctypes.c_double()
+    p = EcaConfig().device_params(1920, 1080)
+    assert lib.eca_prefilter_bound(ctypes.byref(p), ctypes.byref(b)) == 0
+    assert 1e-6 < b.value < 1e-3
+    risky = EcaConfig(intensity_threshold=0.5).device_params(1920, 1080)
+    assert lib.eca_prefilter_bound(ctypes.byref(risky), ctypes.byref(b)) == 1
+
+
+def test_device_params_derived_constants():
+    import math
+    p = EcaConfig().device_params(640, 480)
+    assert p.angle_scale == 180.0 / (math.pi * 30.0)
+    assert p.zero_grad_angle == math.pi * p.angle_scale
+    assert p.inlier_tol == 3.0 / 640
+    assert p.circle_score_threshold == 0.06 * 16
+    assert (p.center_x, p.center_y) == (319.5, 239.5)
+    assert ctypes.sizeof(p) == 6 * 4 + 12 * 8
+
+
+def test_config_validation_mirrors_reference():
+    with pytest.raises(ValueError):
+        EcaConfig(strip_count=3)
+    with pytest.raises(ValueError):
+        EcaConfig(min_radius_frac=0.9)
+    with pytest.raises(ValueError):
+        EcaConfig(ransac_iterations=0)
+    assert EcaConfig(min_circle_score=2.0, min_circle_score_absolute=True).circle_score_threshold() == 2.0
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    frame = np.zeros((480, 640, 3), dtype=np.uint8)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        api.estimate(frame)
+
+
+def test_validate_frame_messages():
+    with pytest.raises(ValueError, match="expected an RGB frame"):
+        api.validate_frame(np.zeros((10, 10), dtype=np.uint8))
+    with pytest.raises(ValueError, match="uint8"):
+        api.validate_frame(np.zeros((20, 20, 3), dtype=np.float32))
+    with pytest.raises(ValueError, match="too small"):
+        api.validate_frame(np.zeros((10, 10, 3), dtype=np.uint8))
+    assert api.validate_frame(np.zeros((14, 8, 3), dtype=np.uint8)) == (8, 14)
