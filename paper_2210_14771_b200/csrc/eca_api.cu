@@ -2,6 +2,8 @@
 // argument validation, launch geometry and kernel dispatch.  No entry point
 // allocates device memory or synchronises the stream.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -73,24 +75,40 @@ int prepare_strip_job(StripJob& J, const uint8_t* frames, int batch, int64_t fra
   return ECA_OK;
 }
 
+bool tracing() {
+  static const bool on = std::getenv("ECA_TRACE") != nullptr;
+  return on;
+}
+#define ECA_TRACE(...)                    \
+  do {                                    \
+    if (tracing()) {                      \
+      std::fprintf(stderr, "[eca] " __VA_ARGS__); \
+      std::fflush(stderr);                \
+    }                                     \
+  } while (0)
+
 template <bool kRows, bool kFused>
 int launch_strips(const StripJob& J, cudaStream_t stream) {
   if (J.batch == 0) return ECA_OK;
   auto kern = strip_kernel<kStages, kRows, kFused>;
   const size_t smem = strip_smem_bytes<kStages>(J.rowcap, J.sumcap, kFused);
+  ECA_TRACE("launch_strips: job %zu B, smem %zu, threads %d\n", sizeof(StripJob), smem, J.nthreads);
   static std::once_flag once;
   std::call_once(once, [kern] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    ECA_TRACE("set attr: %s\n", cudaGetErrorString(e));
   });
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, J.nthreads, smem) !=
-          cudaSuccess ||
-      per_sm < 1)
-    return ECA_ERR_CUDA;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, J.nthreads, smem);
+  ECA_TRACE("occupancy: %s per_sm=%d\n", cudaGetErrorString(e), per_sm);
+  if (e != cudaSuccess || per_sm < 1) return ECA_ERR_CUDA;
   const int items = J.batch * J.n_strips;
   const int grid = items < sm_count() * per_sm ? items : sm_count() * per_sm;
+  ECA_TRACE("grid %d\n", grid);
   kern<<<grid, J.nthreads, smem, stream>>>(J);
-  return check_launch();
+  e = cudaGetLastError();
+  ECA_TRACE("launched: %s\n", cudaGetErrorString(e));
+  return e == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
 }
 
 struct FitJob {

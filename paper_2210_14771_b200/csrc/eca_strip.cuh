@@ -204,7 +204,7 @@ ECA_DEV void issue_item(const StripJob& J, int item, uint8_t* stage, uint64_t* b
 }
 
 template <int NSTAGE>
-ECA_DEV size_t strip_smem_bytes(int rowcap, int sumcap, bool fused) {
+__host__ __device__ inline size_t strip_smem_bytes(int rowcap, int sumcap, bool fused) {
   size_t b = 128 + size_t(NSTAGE) * 3 * rowcap + size_t(3) * sumcap * 2 + kDTab * 4 +
              sizeof(StripRed);
   if (fused) b += sizeof(FitScratch) + 16;
