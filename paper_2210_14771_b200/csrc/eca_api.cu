@@ -14,7 +14,7 @@ using namespace eca;
 
 namespace {
 
-constexpr int kStages = 2;
+constexpr int kStages = 3;
 
 int sm_count() {
   static int count[64];
@@ -33,14 +33,27 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int check_launch() { return cudaGetLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA; }
 
-// Fill the geometry/precision part of a StripJob; returns ECA_OK or an error.
+bool tracing() {
+  static const bool on = std::getenv("ECA_TRACE") != nullptr;
+  return on;
+}
+#define ECA_TRACE(...)                              \
+  do {                                              \
+    if (tracing()) {                                \
+      std::fprintf(stderr, "[eca] " __VA_ARGS__);   \
+      std::fflush(stderr);                          \
+    }                                               \
+  } while (0)
+
+// Fill a StripJob; returns ECA_OK or an error code.
 int prepare_strip_job(StripJob& J, const uint8_t* frames, int batch, int64_t frame_stride,
                       int64_t row_stride, const int32_t* strip_rows, const int32_t* band_rows,
-                      int n_strips, const EcaParams* params, bool force_exact) {
+                      int n_strips, const EcaParams* params) {
   if (!frames || !strip_rows || !params || batch < 0) return ECA_ERR_ARG;
   const int W = params->width, H = params->height;
   if (W < 8 || H < 14) return ECA_ERR_ARG;
-  if (H > 32767 || W > ECA_MAX_WIDTH || n_strips < 1 || n_strips > ECA_MAX_STRIPS) return ECA_ERR_UNSUPPORTED;
+  if (H > 32767 || W > ECA_MAX_WIDTH || n_strips < 1 || n_strips > ECA_MAX_STRIPS)
+    return ECA_ERR_UNSUPPORTED;
   if (row_stride < 3LL * W || frame_stride < 0) return ECA_ERR_ARG;
   if (batch > 0 && int64_t(batch) * n_strips > (int64_t(1) << 30)) return ECA_ERR_UNSUPPORTED;
   std::memset(&J, 0, sizeof(J));
@@ -51,7 +64,6 @@ int prepare_strip_job(StripJob& J, const uint8_t* frames, int batch, int64_t fra
   J.n_strips = n_strips;
   J.nthreads = ((W + kPx - 1) / kPx + 31) / 32 * 32;
   J.rowcap = (24 * J.nthreads + 48 + 15) / 16 * 16;
-  J.sumcap = J.nthreads * kPx + 16;
   J.contiguous = (row_stride == 3LL * W) ? 1 : 0;
   J.p = *params;
   for (int k = 0; k < n_strips; ++k) {
@@ -63,52 +75,39 @@ int prepare_strip_job(StripJob& J, const uint8_t* frames, int batch, int64_t fra
   }
   double bound = 0.0;
   const int risky = eca_prefilter_bound(params, &bound);
-  const double log2e = 1.4426950408889634;
-  J.window = std::nextafter(float(1.0 - bound), 0.0f);
-  J.kT = float(-2.0 * log2e / (3.0 * params->gradient_threshold));
-  J.kA = float(2.0 * params->angle_scale * log2e);
-  J.tau = (risky || force_exact) ? INFINITY : float(1e-11 * 20.0 / params->gradient_threshold);
-  for (int s = 0; s < kDTab; ++s) {
-    const double pre = (s < 766 ? s : 765) / 3.0;
-    J.dtab[s] = float(2.0 / (1.0 + std::exp(2.0 * pre / params->intensity_threshold)));
-  }
+  // residue scores of flat-but-not-identical neighbourhoods stay below
+  // ~5e-14 * 20 / t_g; halves whose best lower bound is under tau are scored
+  // exhaustively in FP64.  Risky configs (FP32 range) always are.
+  J.tau = risky ? INFINITY : float(1e-11 * 20.0 / params->gradient_threshold);
   return ECA_OK;
 }
 
-bool tracing() {
-  static const bool on = std::getenv("ECA_TRACE") != nullptr;
-  return on;
+template <int MAXT, int MINB, bool kRows, bool kFused>
+int launch_strips_t(const StripJob& J, cudaStream_t stream) {
+  auto kern = strip_kernel<kStages, MAXT, MINB, kRows, kFused>;
+  const StripLayout L = strip_layout(kStages, J.rowcap, J.nthreads);
+  ECA_TRACE("launch_strips: job %zu B, smem %zu, threads %d\n", sizeof(StripJob), L.total,
+            J.nthreads);
+  static std::once_flag once;
+  std::call_once(once, [kern] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  const int block = J.nthreads + 32 * kFpWarps;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, L.total);
+  if (e != cudaSuccess || per_sm < 1) return ECA_ERR_CUDA;
+  const int items = J.batch * J.n_strips;
+  const int grid = items < sm_count() * per_sm ? items : sm_count() * per_sm;
+  ECA_TRACE("per_sm %d grid %d\n", per_sm, grid);
+  kern<<<grid, block, L.total, stream>>>(J);
+  return check_launch();
 }
-#define ECA_TRACE(...)                    \
-  do {                                    \
-    if (tracing()) {                      \
-      std::fprintf(stderr, "[eca] " __VA_ARGS__); \
-      std::fflush(stderr);                \
-    }                                     \
-  } while (0)
 
 template <bool kRows, bool kFused>
 int launch_strips(const StripJob& J, cudaStream_t stream) {
   if (J.batch == 0) return ECA_OK;
-  auto kern = strip_kernel<kStages, kRows, kFused>;
-  const size_t smem = strip_smem_bytes<kStages>(J.rowcap, J.sumcap, kFused);
-  ECA_TRACE("launch_strips: job %zu B, smem %zu, threads %d\n", sizeof(StripJob), smem, J.nthreads);
-  static std::once_flag once;
-  std::call_once(once, [kern] {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    ECA_TRACE("set attr: %s\n", cudaGetErrorString(e));
-  });
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, J.nthreads, smem);
-  ECA_TRACE("occupancy: %s per_sm=%d\n", cudaGetErrorString(e), per_sm);
-  if (e != cudaSuccess || per_sm < 1) return ECA_ERR_CUDA;
-  const int items = J.batch * J.n_strips;
-  const int grid = items < sm_count() * per_sm ? items : sm_count() * per_sm;
-  ECA_TRACE("grid %d\n", grid);
-  kern<<<grid, J.nthreads, smem, stream>>>(J);
-  e = cudaGetLastError();
-  ECA_TRACE("launched: %s\n", cudaGetErrorString(e));
-  return e == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
+  if (J.nthreads <= 256) return launch_strips_t<256 + 32 * kFpWarps, 2, kRows, kFused>(J, stream);
+  return launch_strips_t<512 + 32 * kFpWarps, 1, kRows, kFused>(J, stream);
 }
 
 struct FitJob {
@@ -121,22 +120,36 @@ struct FitJob {
   EcaFitRecord* out;
 };
 
-__global__ void __launch_bounds__(512) fit_kernel(const __grid_constant__ FitJob J) {
-  __shared__ FitScratch fs;
-  const size_t o = size_t(blockIdx.x) * J.n_cand;
-  fit_frame(J.x + o, J.y + o, J.s + o, J.n_cand, false, J.p, J.trip, J.exhaustive, &fs,
-            J.out + blockIdx.x);
+// one warp per frame (same arithmetic order as the fused path's fit_warp)
+constexpr int kFitFramesPerCta = 4;
+
+__global__ void __launch_bounds__(32 * kFitFramesPerCta) fit_kernel(const __grid_constant__ FitJob J,
+                                                                   int batch) {
+  __shared__ FitScratchW fs[kFitFramesPerCta];
+  const int w = threadIdx.x >> 5;
+  const int b = blockIdx.x * kFitFramesPerCta + w;
+  if (b >= batch) return;
+  const size_t o = size_t(b) * J.n_cand;
+  fit_warp(J.x + o, J.y + o, J.s + o, J.n_cand, J.p, J.trip, J.exhaustive, &fs[w], J.out + b);
+}
+
+int check_fit_params(const EcaParams* params) {
+  if (params->ransac_attempts < 1 || params->ransac_attempts > ECA_MAX_ATTEMPTS ||
+      params->ransac_iterations < 1)
+    return ECA_ERR_ARG;
+  return ECA_OK;
 }
 
 }  // namespace
 
 extern "C" int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                                       int64_t row_stride, const int32_t* strip_rows,
-                                      const int32_t* band_rows, int n_strips, const EcaParams* params, int32_t* out_x,
-                                      int32_t* out_y, double* out_score, void* stream) {
+                                      const int32_t* band_rows, int n_strips,
+                                      const EcaParams* params, int32_t* out_x, int32_t* out_y,
+                                      double* out_score, void* stream) {
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
-                             n_strips, params, false);
+                             n_strips, params);
   if (rc) return rc;
   if (!out_x || !out_y || !out_score) return ECA_ERR_ARG;
   J.out_x = out_x;
@@ -147,12 +160,13 @@ extern "C" int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t 
 
 extern "C" int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                                           int64_t row_stride, const int32_t* strip_rows,
-                                          const int32_t* band_rows, int n_strips, const EcaParams* params,
-                                          double* out_scores, int32_t* out_x, int32_t* out_y,
-                                          double* out_score, void* stream) {
+                                          const int32_t* band_rows, int n_strips,
+                                          const EcaParams* params, double* out_scores,
+                                          int32_t* out_x, int32_t* out_y, double* out_score,
+                                          void* stream) {
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
-                             n_strips, params, true);
+                             n_strips, params);
   if (rc) return rc;
   if (!out_scores || !out_x || !out_y || !out_score) return ECA_ERR_ARG;
   J.out_rows = out_scores;
@@ -168,29 +182,25 @@ extern "C" int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const doubl
   if (batch < 0 || n_cand < 0 || n_cand > 2 * ECA_MAX_STRIPS || !params) return ECA_ERR_ARG;
   if (batch == 0) return ECA_OK;
   if (!cand_x || !cand_y || !cand_score || !out || (!exhaustive && !triplets)) return ECA_ERR_ARG;
-  if (params->ransac_attempts < 1 || params->ransac_attempts > ECA_MAX_ATTEMPTS ||
-      params->ransac_iterations < 1)
-    return ECA_ERR_ARG;
-  if (batch > 0x7fffffff) return ECA_ERR_UNSUPPORTED;
+  if (check_fit_params(params)) return ECA_ERR_ARG;
   FitJob J{cand_x, cand_y, cand_score, n_cand, exhaustive ? 1 : 0, *params, triplets, out};
-  fit_kernel<<<batch, 512, 0, as_stream(stream)>>>(J);
+  fit_kernel<<<(batch + kFitFramesPerCta - 1) / kFitFramesPerCta, 32 * kFitFramesPerCta, 0,
+               as_stream(stream)>>>(J, batch);
   return check_launch();
 }
 
 extern "C" int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                                         int64_t row_stride, const int32_t* strip_rows,
-                                        const int32_t* band_rows, int n_strips, const EcaParams* params,
-                                        const int16_t* triplets, int32_t* counters,
-                                        int32_t* out_x, int32_t* out_y, double* out_score,
-                                        EcaFitRecord* out, void* stream) {
+                                        const int32_t* band_rows, int n_strips,
+                                        const EcaParams* params, const int16_t* triplets,
+                                        int32_t* counters, int32_t* out_x, int32_t* out_y,
+                                        double* out_score, EcaFitRecord* out, void* stream) {
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
-                             n_strips, params, false);
+                             n_strips, params);
   if (rc) return rc;
   if (!triplets || !counters || !out || !out_x || !out_y || !out_score) return ECA_ERR_ARG;
-  if (params->ransac_attempts < 1 || params->ransac_attempts > ECA_MAX_ATTEMPTS ||
-      params->ransac_iterations < 1)
-    return ECA_ERR_ARG;
+  if (check_fit_params(params)) return ECA_ERR_ARG;
   J.out_x = out_x;
   J.out_y = out_y;
   J.out_score = out_score;
@@ -209,13 +219,11 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
   const size_t row_bytes = size_t(3) * width;
   const size_t band_bytes = row_bytes * rows_per_band;
   const size_t dev_frame = band_bytes * n_bands;
+  const bool packed = host_row_stride == int64_t(row_bytes);
   auto st = as_stream(stream);
   for (int k = 0; k < n_bands; ++k) {
-    for (int r = 0; r < rows_per_band; ++r) {
-      // one strided DMA per (band, row) across every frame of the batch; a whole
-      // band in one DMA when the host rows are packed
-      const bool packed = host_row_stride == int64_t(row_bytes);
-      if (packed && r > 0) break;
+    // one strided DMA per band (packed host rows) or per band row, across all frames
+    for (int r = 0; r < (packed ? 1 : rows_per_band); ++r) {
       const uint8_t* src = host + int64_t(first_rows[k] + r) * host_row_stride;
       uint8_t* dst = dev + k * band_bytes + r * row_bytes;
       const size_t w = packed ? band_bytes : row_bytes;

@@ -1,23 +1,31 @@
-// K2: candidate filter + seeded RANSAC with iterated FP64 least squares, one
-// CTA per frame, one WARP per hypothesis (lanes = candidates).
+// K2: candidate filter + seeded RANSAC with iterated FP64 least squares.
 //
 // Restates fitting.py:39-230 in the reference's evaluation order: every FP64
 // expression is written with explicit round-to-nearest intrinsics (no FMA
 // contraction) so circumcircles, gates and LSQ systems see numpy's doubles.
 // Only the moment sums (numpy: OpenBLAS dgemm) and the 3x3 solve (LAPACK
 // gesv) reassociate; the survey measured that headroom at <=2.3e-13 px.
+//
+// Mapping (one CTA per frame): LANE = hypothesis (32 attempts per chunk), so a
+// hypothesis' circle, inlier test and 3x3 solve live in one thread and need
+// no shuffles; the candidate list is split across up to kFitWarps WARPS, each
+// accumulating partial moments of its contiguous candidate range; partials
+// meet in shared memory and every warp finishes the (identical) solve.  Ties
+// between hypotheses resolve to the lowest attempt index (fitting.py:222).
 #pragma once
 
 #include "eca_common.cuh"
 
 namespace eca {
 
+constexpr int kFitWarps = 8;
+constexpr int kMom = 10;   // sx sy sz sxx sxy syy sxz syz count score
+
 struct FitScratch {
   double px[2 * ECA_MAX_STRIPS];
   double py[2 * ECA_MAX_STRIPS];
   double ps[2 * ECA_MAX_STRIPS];
-  double wb_s[32], wb_cx[32], wb_cy[32], wb_r[32];
-  int wb_a[32], wb_inl[32], wb_flags[32];
+  double part[kFitWarps][kMom][32];
   int n;
 };
 
@@ -48,9 +56,9 @@ ECA_DEV Circ circumcircle(double ax, double ay, double bx, double by, double qx,
 }
 
 // fitting.py:89-124 given the masked moments; returns ok and the new circle.
-ECA_DEV bool lsq_solve(double sx, double sy, double sz, double sxx, double sxy, double syy,
-                       double sxz, double syz, int cnt, double& a_out, double& b_out,
-                       double& r_out) {
+ECA_DEV bool lsq_solve(const double* mo, int cnt, double& a_out, double& b_out, double& r_out) {
+  const double sx = mo[0], sy = mo[1], sz = mo[2], sxx = mo[3], sxy = mo[4], syy = mo[5];
+  const double sxz = mo[6], syz = mo[7];
   const double n = double(cnt);
   double m[3][3] = {{mul_rn(4.0, sxx), mul_rn(4.0, sxy), mul_rn(2.0, sx)},
                     {mul_rn(4.0, sxy), mul_rn(4.0, syy), mul_rn(2.0, sy)},
@@ -61,7 +69,8 @@ ECA_DEV bool lsq_solve(double sx, double sy, double sz, double sxx, double sxy, 
   const double t3 = sub_rn(mul_rn(m[0][1], m[1][2]), mul_rn(m[1][1], m[0][2]));
   const double det = add_rn(sub_rn(mul_rn(m[0][0], t1), mul_rn(m[0][1], t2)), mul_rn(m[0][2], t3));
   const double nn = n > 1.0 ? n : 1.0;
-  bool ok = (cnt >= 3) && isfinite(det) && (fabs(det) > mul_rn(1e-12, mul_rn(mul_rn(nn, nn), nn)));
+  const bool ok = (cnt >= 3) && isfinite(det) &&
+                  (fabs(det) > mul_rn(1e-12, mul_rn(mul_rn(nn, nn), nn)));
   if (!ok) return false;
   // LU with partial pivoting (dgetrf2/dgetrs order: reciprocal-scaled
   // multipliers, forward then backward substitution)
@@ -127,50 +136,16 @@ ECA_DEV void unrank3(int a, int n, int& i, int& j, int& k) {
   k = j + 1 + a;
 }
 
-// Warp-parallel inlier pass: members of circle (cx,cy,r) among n points.
-// Returns the count; accumulates moments when `mom` is set, score sum otherwise.
-template <bool kMoments>
-ECA_DEV int inlier_pass(const FitScratch* fs, int n, double tol, double cx, double cy, double r,
-                        double* mom /* [8] */, double& score_sum) {
-  const int lane = threadIdx.x & 31;
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  double ssum = 0.0;
-  int cnt = 0;
-  for (int k = lane; k < n; k += 32) {
-    const double x = fs->px[k], y = fs->py[k];
-    const double d = fabs(sub_rn(hypot(sub_rn(x, cx), sub_rn(y, cy)), r));
-    if (d <= tol) {
-      ++cnt;
-      if (kMoments) {
-        const double z = add_rn(mul_rn(x, x), mul_rn(y, y));
-        acc[0] += x;
-        acc[1] += y;
-        acc[2] += z;
-        acc[3] += mul_rn(x, x);
-        acc[4] += mul_rn(x, y);
-        acc[5] += mul_rn(y, y);
-        acc[6] += mul_rn(x, z);
-        acc[7] += mul_rn(y, z);
-      } else {
-        ssum += fs->ps[k];
-      }
-    }
-  }
-  cnt = warp_sum(cnt);
-  if (kMoments) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) mom[q] = warp_sum(acc[q]);
-  } else {
-    score_sum = warp_sum(ssum);
-  }
-  return cnt;
+// Inlier test of fitting.py:199/206 for one candidate.
+ECA_DEV bool is_inlier(double x, double y, const Circ& c, double tol) {
+  return fabs(sub_rn(hypot(sub_rn(x, c.cx), sub_rn(y, c.cy)), c.r)) <= tol;
 }
 
-// One frame, whole CTA.  cand_* hold n_cand candidates in estimator.py:69
-// order; `volatile_loads` reads them through L2 (written by other CTAs).
+// One frame on the whole CTA.  cand_* hold n_cand candidates in estimator.py:69
+// order; `l2_loads` reads them through L2 (written by other CTAs this launch).
 ECA_DEV void fit_frame(const int32_t* cand_x, const int32_t* cand_y, const double* cand_s,
-                       int n_cand, bool volatile_loads, const EcaParams& p,
-                       const int16_t* trip, int exhaustive, FitScratch* fs, EcaFitRecord* out) {
+                       int n_cand, bool l2_loads, const EcaParams& p, const int16_t* trip,
+                       int exhaustive, FitScratch* fs, EcaFitRecord* out) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int n_warps = blockDim.x >> 5;
@@ -184,7 +159,7 @@ ECA_DEV void fit_frame(const int32_t* cand_x, const int32_t* cand_y, const doubl
       int x = 0, y = 0;
       double s = 0.0;
       if (i < n_cand) {
-        if (volatile_loads) {
+        if (l2_loads) {
           x = __ldcg(cand_x + i);
           y = __ldcg(cand_y + i);
           s = __ldcg(cand_s + i);
@@ -215,28 +190,217 @@ ECA_DEV void fit_frame(const int32_t* cand_x, const int32_t* cand_y, const doubl
     __syncthreads();
     return;
   }
+  const int G = n_warps < kFitWarps ? n_warps : kFitWarps;
+  const bool worker = warp < G;
+  const int kb = worker ? (n * warp) / G : 0, ke = worker ? (n * (warp + 1)) / G : 0;
+  const int attempts = exhaustive ? n * (n - 1) * (n - 2) / 6 : p.ransac_attempts;
+  const double tol = p.inlier_tol;
+
+  double best_s = -1.0, bcx = 0.0, bcy = 0.0, br = 0.0;
+  int best_a = -1, best_inl = 0, any_live = 0, any_gated = 0;
+  for (int c0 = 0; c0 < attempts; c0 += 32) {
+    const int a = c0 + lane;
+    Circ c{0.0, 0.0, 1.0, false};
+    if (a < attempts) {
+      int i0, i1, i2;
+      if (exhaustive) {
+        unrank3(a, n, i0, i1, i2);
+      } else {
+        const int16_t* t = trip + (size_t(n - 3) * p.ransac_attempts + a) * 3;
+        i0 = t[0];
+        i1 = t[1];
+        i2 = t[2];
+      }
+      c = circumcircle(fs->px[i0], fs->py[i0], fs->px[i1], fs->py[i1], fs->px[i2], fs->py[i2]);
+    }
+    // ---- iterated least squares (fitting.py:198-205)
+    for (int it = 0; it < p.ransac_iterations; ++it) {
+      if (!__syncthreads_or(c.alive ? 1 : 0)) break;   // identical in every warp
+      if (worker) {
+        double acc[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (c.alive) {
+          for (int k = kb; k < ke; ++k) {
+            const double x = fs->px[k], y = fs->py[k];
+            if (is_inlier(x, y, c, tol)) {
+              const double z = add_rn(mul_rn(x, x), mul_rn(y, y));
+              acc[0] = add_rn(acc[0], x);
+              acc[1] = add_rn(acc[1], y);
+              acc[2] = add_rn(acc[2], z);
+              acc[3] = add_rn(acc[3], mul_rn(x, x));
+              acc[4] = add_rn(acc[4], mul_rn(x, y));
+              acc[5] = add_rn(acc[5], mul_rn(y, y));
+              acc[6] = add_rn(acc[6], mul_rn(x, z));
+              acc[7] = add_rn(acc[7], mul_rn(y, z));
+              acc[8] += 1.0;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kMom - 1; ++q) fs->part[warp][q][lane] = acc[q];
+      }
+      __syncthreads();
+      double mo[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int q = 0; q < kMom - 1; ++q) mo[q] = add_rn(mo[q], fs->part[g][q][lane]);
+      __syncthreads();   // partials may be overwritten after this
+      if (c.alive) {
+        double na, nb, nr;
+        if (lsq_solve(mo, int(mo[8]), na, nb, nr)) {
+          c.cx = na;
+          c.cy = nb;
+          c.r = nr;
+        } else {
+          c.alive = false;
+        }
+      }
+    }
+    // ---- final membership + score (fitting.py:206-208)
+    if (worker) {
+      double s = 0.0, cnt = 0.0;
+      if (c.alive)
+        for (int k = kb; k < ke; ++k)
+          if (is_inlier(fs->px[k], fs->py[k], c, tol)) {
+            s = add_rn(s, fs->ps[k]);
+            cnt += 1.0;
+          }
+      fs->part[warp][0][lane] = s;
+      fs->part[warp][1][lane] = cnt;
+    }
+    __syncthreads();
+    double score = 0.0, inl = 0.0;
+    for (int g = 0; g < G; ++g) {
+      score = add_rn(score, fs->part[g][0][lane]);
+      inl += fs->part[g][1][lane];
+    }
+    __syncthreads();
+    // ---- gates (normalised units, fitting.py:210-216) + first-index argmax
+    const bool gated = (c.r < p.min_radius_frac) || (c.r > p.max_radius_frac) ||
+                       (hypot(c.cx, c.cy) > p.max_center_offset_frac);
+    const bool surv = c.alive && !gated;
+    any_live |= __any_sync(kFull, surv);
+    any_gated |= __any_sync(kFull, c.alive && gated);
+    double s_l = surv ? score : -1.0;
+    int a_l = surv ? a : 0x7fffffff;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      const double os = __shfl_xor_sync(kFull, s_l, d);
+      const int oa = __shfl_xor_sync(kFull, a_l, d);
+      if (os > s_l || (os == s_l && oa < a_l)) {
+        s_l = os;
+        a_l = oa;
+      }
+    }
+    if (a_l != 0x7fffffff && s_l > best_s) {   // chunks ascend: strict keeps the first
+      const int src = a_l - c0;
+      best_s = s_l;
+      best_a = a_l;
+      bcx = __shfl_sync(kFull, c.cx, src);
+      bcy = __shfl_sync(kFull, c.cy, src);
+      br = __shfl_sync(kFull, c.r, src);
+      best_inl = int(__shfl_sync(kFull, inl, src));
+    }
+  }
+  if (threadIdx.x == 0) {
+    EcaFitRecord rec{0.0, 0.0, 0.0, 0.0, 0, ECA_LOW_SCORE};
+    if (!any_live) {
+      rec.status = any_gated ? ECA_GEOMETRY_GATE : ECA_LOW_SCORE;
+    } else if (!(best_s < p.circle_score_threshold)) {
+      rec.status = ECA_ACCEPTED;
+      rec.cx = add_rn(p.center_x, mul_rn(bcx, double(W)));
+      rec.cy = add_rn(p.center_y, mul_rn(bcy, double(W)));
+      rec.r = mul_rn(br, double(W));
+      rec.score = best_s;
+      rec.inliers = best_inl;
+    }
+    (void)best_a;
+    *out = rec;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Single-warp variant (no CTA barriers): lane = hypothesis, each lane walks the
+// whole candidate list.  Used by the fused strip kernel, where the warp that
+// completes a frame fits it while the CTA's other warps keep scoring strips.
+struct FitScratchW {
+  double px[2 * ECA_MAX_STRIPS];
+  double py[2 * ECA_MAX_STRIPS];
+  double ps[2 * ECA_MAX_STRIPS];
+};
+
+ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double* cand_s,
+                      int n_cand, const EcaParams& p, const int16_t* trip, int exhaustive,
+                      FitScratchW* fs, EcaFitRecord* out) {
+  const int lane = threadIdx.x & 31;
+  const int W = p.width, H = p.height;
+  int n = 0;
+  for (int base = 0; base < n_cand; base += 32) {   // filter_candidates, order-preserving
+    const int i = base + lane;
+    bool keep = false;
+    int x = 0, y = 0;
+    double s = 0.0;
+    if (i < n_cand) {
+      x = __ldcg(cand_x + i);
+      y = __ldcg(cand_y + i);
+      s = __ldcg(cand_s + i);
+      const int edge = min(min(x, W - 1 - x), min(y, H - 1 - y));
+      keep = edge >= p.edge_margin_px && s >= p.min_point_score;
+    }
+    const unsigned bal = __ballot_sync(kFull, keep);
+    if (keep) {
+      const int pos = n + __popc(bal & ((1u << lane) - 1u));
+      fs->px[pos] = div_rn(sub_rn(double(x), p.center_x), double(W));
+      fs->py[pos] = div_rn(sub_rn(double(y), p.center_y), double(W));
+      fs->ps[pos] = s;
+    }
+    n += __popc(bal);
+  }
+  __syncwarp();
+  if (n < 3) {
+    if (lane == 0) *out = EcaFitRecord{0.0, 0.0, 0.0, 0.0, 0, ECA_NO_CANDIDATES};
+    __syncwarp();
+    return;
+  }
   const int attempts = exhaustive ? n * (n - 1) * (n - 2) / 6 : p.ransac_attempts;
   const double tol = p.inlier_tol;
   double best_s = -1.0, bcx = 0.0, bcy = 0.0, br = 0.0;
-  int best_a = -1, best_inl = 0, flags = 0;  // bit0: any survivor, bit1: any live gated
-  for (int a = warp; a < attempts; a += n_warps) {
-    int i0, i1, i2;
-    if (exhaustive) {
-      unrank3(a, n, i0, i1, i2);
-    } else {
-      const int16_t* t = trip + (size_t(n - 3) * p.ransac_attempts + a) * 3;
-      i0 = t[0];
-      i1 = t[1];
-      i2 = t[2];
+  int best_inl = 0, any_live = 0, any_gated = 0;
+  for (int c0 = 0; c0 < attempts; c0 += 32) {
+    const int a = c0 + lane;
+    Circ c{0.0, 0.0, 1.0, false};
+    if (a < attempts) {
+      int i0, i1, i2;
+      if (exhaustive) {
+        unrank3(a, n, i0, i1, i2);
+      } else {
+        const int16_t* t = trip + (size_t(n - 3) * p.ransac_attempts + a) * 3;
+        i0 = t[0];
+        i1 = t[1];
+        i2 = t[2];
+      }
+      c = circumcircle(fs->px[i0], fs->py[i0], fs->px[i1], fs->py[i1], fs->px[i2], fs->py[i2]);
     }
-    Circ c = circumcircle(fs->px[i0], fs->py[i0], fs->px[i1], fs->py[i1], fs->px[i2], fs->py[i2]);
-    for (int it = 0; it < p.ransac_iterations && c.alive; ++it) {
-      double mom[8];
-      double unused;
-      const int cnt = inlier_pass<true>(fs, n, tol, c.cx, c.cy, c.r, mom, unused);
+    for (int it = 0; it < p.ransac_iterations && __any_sync(kFull, c.alive); ++it) {
+      if (!c.alive) continue;
+      double mo[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int k = 0; k < n; ++k) {
+        const double x = fs->px[k], y = fs->py[k];
+        if (is_inlier(x, y, c, tol)) {
+          const double z = add_rn(mul_rn(x, x), mul_rn(y, y));
+          mo[0] = add_rn(mo[0], x);
+          mo[1] = add_rn(mo[1], y);
+          mo[2] = add_rn(mo[2], z);
+          mo[3] = add_rn(mo[3], mul_rn(x, x));
+          mo[4] = add_rn(mo[4], mul_rn(x, y));
+          mo[5] = add_rn(mo[5], mul_rn(y, y));
+          mo[6] = add_rn(mo[6], mul_rn(x, z));
+          mo[7] = add_rn(mo[7], mul_rn(y, z));
+          mo[8] += 1.0;
+        }
+      }
       double na, nb, nr;
-      if (lsq_solve(mom[0], mom[1], mom[2], mom[3], mom[4], mom[5], mom[6], mom[7], cnt, na, nb,
-                    nr)) {
+      if (lsq_solve(mo, int(mo[8]), na, nb, nr)) {
         c.cx = na;
         c.cy = nb;
         c.r = nr;
@@ -244,58 +408,54 @@ ECA_DEV void fit_frame(const int32_t* cand_x, const int32_t* cand_y, const doubl
         c.alive = false;
       }
     }
-    if (!c.alive) continue;   // no members, neither survivor nor gated
-    double score;
-    const int inl = inlier_pass<false>(fs, n, tol, c.cx, c.cy, c.r, nullptr, score);
+    double score = 0.0;
+    int inl = 0;
+    if (c.alive)
+      for (int k = 0; k < n; ++k)
+        if (is_inlier(fs->px[k], fs->py[k], c, tol)) {
+          score = add_rn(score, fs->ps[k]);
+          ++inl;
+        }
     const bool gated = (c.r < p.min_radius_frac) || (c.r > p.max_radius_frac) ||
                        (hypot(c.cx, c.cy) > p.max_center_offset_frac);
-    if (gated) {
-      flags |= 2;
-    } else {
-      flags |= 1;
-      if (score > best_s) {   // strict: first (lowest) attempt wins ties
-        best_s = score;
-        best_a = a;
-        bcx = c.cx;
-        bcy = c.cy;
-        br = c.r;
-        best_inl = inl;
+    const bool surv = c.alive && !gated;
+    any_live |= __any_sync(kFull, surv);
+    any_gated |= __any_sync(kFull, c.alive && gated);
+    double s_l = surv ? score : -1.0;
+    int a_l = surv ? a : 0x7fffffff;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      const double os = __shfl_xor_sync(kFull, s_l, d);
+      const int oa = __shfl_xor_sync(kFull, a_l, d);
+      if (os > s_l || (os == s_l && oa < a_l)) {
+        s_l = os;
+        a_l = oa;
       }
+    }
+    if (a_l != 0x7fffffff && s_l > best_s) {
+      const int src = a_l - c0;
+      best_s = s_l;
+      bcx = __shfl_sync(kFull, c.cx, src);
+      bcy = __shfl_sync(kFull, c.cy, src);
+      br = __shfl_sync(kFull, c.r, src);
+      best_inl = __shfl_sync(kFull, inl, src);
     }
   }
   if (lane == 0) {
-    fs->wb_s[warp] = best_s;
-    fs->wb_a[warp] = best_a;
-    fs->wb_cx[warp] = bcx;
-    fs->wb_cy[warp] = bcy;
-    fs->wb_r[warp] = br;
-    fs->wb_inl[warp] = best_inl;
-    fs->wb_flags[warp] = flags;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int all = 0, bw = -1;
-    for (int w = 0; w < n_warps; ++w) {
-      all |= fs->wb_flags[w];
-      if (fs->wb_a[w] < 0) continue;
-      if (bw < 0 || fs->wb_s[w] > fs->wb_s[bw] ||
-          (fs->wb_s[w] == fs->wb_s[bw] && fs->wb_a[w] < fs->wb_a[bw]))
-        bw = w;
-    }
     EcaFitRecord rec{0.0, 0.0, 0.0, 0.0, 0, ECA_LOW_SCORE};
-    if (!(all & 1)) {
-      rec.status = (all & 2) ? ECA_GEOMETRY_GATE : ECA_LOW_SCORE;
-    } else if (!(fs->wb_s[bw] < p.circle_score_threshold)) {
+    if (!any_live) {
+      rec.status = any_gated ? ECA_GEOMETRY_GATE : ECA_LOW_SCORE;
+    } else if (!(best_s < p.circle_score_threshold)) {
       rec.status = ECA_ACCEPTED;
-      rec.cx = add_rn(p.center_x, mul_rn(fs->wb_cx[bw], double(W)));
-      rec.cy = add_rn(p.center_y, mul_rn(fs->wb_cy[bw], double(W)));
-      rec.r = mul_rn(fs->wb_r[bw], double(W));
-      rec.score = fs->wb_s[bw];
-      rec.inliers = fs->wb_inl[bw];
+      rec.cx = add_rn(p.center_x, mul_rn(bcx, double(W)));
+      rec.cy = add_rn(p.center_y, mul_rn(bcy, double(W)));
+      rec.r = mul_rn(br, double(W));
+      rec.score = best_s;
+      rec.inliers = best_inl;
     }
     *out = rec;
   }
-  __syncthreads();
+  __syncwarp();
 }
 
 }  // namespace eca

@@ -1,0 +1,34 @@
+"""Time the pieces of the step separately (points-only, fit-only, fused)."""
+import sys, ctypes, numpy as np, torch
+sys.path.insert(0, '.')
+import paper_2210_14771_b200 as eb
+from paper_2210_14771_b200 import _lib, api, synth
+import bench
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+dev = torch.device('cuda', 0)
+base = bench.base_frames(40)
+pool = torch.empty((2048, 1080, 1920, 3), dtype=torch.uint8, device=dev)
+bd = torch.from_numpy(base).to(dev)
+for i in range(2048): pool[i].copy_(bd[i % 40])
+eng = eb.ContentAreaEngine(1080, 1920, B, device=dev)
+lib = _lib.load(); st = api._stream(dev)
+rows = eng._rows; S = eng.n_strips
+def points(i):
+    f = pool[(i % (2048 // B)) * B:][:B]
+    _lib.check(lib.eca_points_handcrafted(api._ptr(f), B, f.stride(0), f.stride(1), rows, None, S, ctypes.byref(eng.params), api._ptr(eng.xs), api._ptr(eng.ys), api._ptr(eng.sc), st), "pts")
+def fit(i):
+    _lib.check(lib.eca_fit(api._ptr(eng.xs), api._ptr(eng.ys), api._ptr(eng.sc), B, 2 * S, ctypes.byref(eng.params), api._ptr(eng.trip), 0, api._ptr(eng.rec), st), "fit")
+def fused(i):
+    f = pool[(i % (2048 // B)) * B:][:B]
+    eng.run(f)
+def timeit(fn, n=50):
+    for i in range(5): fn(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(n): fn(i)
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) / n
+for name, fn in [("points", points), ("fit", fit), ("fused", fused)]:
+    ms = timeit(fn)
+    print(f"{name:8s} B={B} {ms*1e3:9.1f} us  {ms*1e3/B:7.3f} us/frame  {70778880*B/256/(ms/1e3)/1e9:8.1f} GB/s(strip bytes)", flush=True)
