@@ -234,3 +234,15 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
   }
   return ECA_OK;
 }
+
+#ifdef ECA_STATS
+extern "C" int eca_debug_strip_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_strip_stats, sizeof(unsigned long long) * 16) != cudaSuccess)
+    return ECA_ERR_CUDA;
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_strip_stats, z, sizeof(z));
+  }
+  return ECA_OK;
+}
+#endif
