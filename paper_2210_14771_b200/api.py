@@ -300,11 +300,21 @@ def _handcrafted_batch(df: _DevFrames, width: int, height: int, rows, cfg: EcaCo
     rec = torch.empty((b, 5), dtype=torch.float64, device=device)
     params = cfg.device_params(width, height, center)
     trip = _dev_triplets(seed, cfg.ransac_attempts, 2 * s, device)
-    cnt = _dev_counters(b, device)
-    rc = lib.eca_estimate_handcrafted(df.ptr, b, df.fstride, df.rstride, _i32_array(rows), df.band,
-                                      s, ctypes.byref(params), _ptr(trip), _ptr(cnt), _ptr(xs),
-                                      _ptr(ys), _ptr(sc), _ptr(rec), _stream(device))
-    _lib.check(rc, "eca_estimate_handcrafted")
+    if b <= 16:   # latency: one fused launch
+        cnt = _dev_counters(b, device)
+        rc = lib.eca_estimate_handcrafted(df.ptr, b, df.fstride, df.rstride, _i32_array(rows),
+                                          df.band, s, ctypes.byref(params), _ptr(trip), _ptr(cnt),
+                                          _ptr(xs), _ptr(ys), _ptr(sc), _ptr(rec), _stream(device))
+        _lib.check(rc, "eca_estimate_handcrafted")
+        return xs, ys, sc, rec
+    # throughput: strip kernel, then the fit kernel (one warp per frame)
+    rc = lib.eca_points_handcrafted(df.ptr, b, df.fstride, df.rstride, _i32_array(rows), df.band, s,
+                                    ctypes.byref(params), _ptr(xs), _ptr(ys), _ptr(sc),
+                                    _stream(device))
+    _lib.check(rc, "eca_points_handcrafted")
+    rc = lib.eca_fit(_ptr(xs), _ptr(ys), _ptr(sc), b, 2 * s, ctypes.byref(params), _ptr(trip), 0,
+                     _ptr(rec), _stream(device))
+    _lib.check(rc, "eca_fit")
     return xs, ys, sc, rec
 
 

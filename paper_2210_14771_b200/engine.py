@@ -52,9 +52,17 @@ class ContentAreaEngine:
             self.probs = torch.empty((batch, s, width - 6), dtype=torch.float32, device=d)
             self.w_dev, self.norm = api._dev_net(variant.net, d)
         self.graph = None
-        self.launches_per_run = 2 if isinstance(variant, api.Learned) else 1
+        # Small batches (latency): one fused launch whose last strip CTA per
+        # frame runs the fit.  Large batches (throughput): strip kernel then a
+        # fit kernel (one warp per frame), which keeps the fits off the strip
+        # kernel's critical path.
+        self.fused = batch <= self.FUSED_MAX_BATCH
         if isinstance(variant, api.Learned):
             self.launches_per_run = 3
+        else:
+            self.launches_per_run = 1 if self.fused else 2
+
+    FUSED_MAX_BATCH = 16
 
     # ------------------------------------------------------------ launches
     def _launch(self, ptr: int, fstride: int, rstride: int, band) -> None:
@@ -72,12 +80,21 @@ class ContentAreaEngine:
                              api._ptr(self.rec), st)
             _lib.check(rc, "eca_fit")
             return
-        rc = lib.eca_estimate_handcrafted(ctypes.c_void_p(ptr), self.batch, fstride, rstride,
-                                          self._rows, band, s, ctypes.byref(self.params),
-                                          api._ptr(self.trip), api._ptr(self.counters),
-                                          api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc),
-                                          api._ptr(self.rec), st)
-        _lib.check(rc, "eca_estimate_handcrafted")
+        if self.fused:
+            rc = lib.eca_estimate_handcrafted(ctypes.c_void_p(ptr), self.batch, fstride, rstride,
+                                              self._rows, band, s, ctypes.byref(self.params),
+                                              api._ptr(self.trip), api._ptr(self.counters),
+                                              api._ptr(self.xs), api._ptr(self.ys),
+                                              api._ptr(self.sc), api._ptr(self.rec), st)
+            _lib.check(rc, "eca_estimate_handcrafted")
+            return
+        rc = lib.eca_points_handcrafted(ctypes.c_void_p(ptr), self.batch, fstride, rstride,
+                                        self._rows, band, s, ctypes.byref(self.params),
+                                        api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), st)
+        _lib.check(rc, "eca_points_handcrafted")
+        rc = lib.eca_fit(api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), self.batch, 2 * s,
+                         ctypes.byref(self.params), api._ptr(self.trip), 0, api._ptr(self.rec), st)
+        _lib.check(rc, "eca_fit")
 
     def _check_frames(self, frames: torch.Tensor) -> torch.Tensor:
         if frames.dim() == 3:
@@ -88,6 +105,16 @@ class ContentAreaEngine:
         if frames.stride(3) != 1 or frames.stride(2) != 3:
             frames = frames.contiguous()
         return frames
+
+    def points(self, frames: torch.Tensor) -> None:
+        """Only the strip-scoring kernel (candidates into self.xs/ys/sc); the
+        bench times it alone for the roofline of the dominant kernel."""
+        f = self._check_frames(frames)
+        rc = _lib.load().eca_points_handcrafted(
+            ctypes.c_void_p(f.data_ptr()), self.batch, f.stride(0), f.stride(1), self._rows, None,
+            self.n_strips, ctypes.byref(self.params), api._ptr(self.xs), api._ptr(self.ys),
+            api._ptr(self.sc), api._stream(self.device))
+        _lib.check(rc, "eca_points_handcrafted")
 
     def run(self, frames: torch.Tensor) -> torch.Tensor:
         """Frames on this GPU -> device records (asynchronous)."""
