@@ -103,13 +103,18 @@ int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_stride,
                   int64_t host_row_stride, const int32_t* first_rows, int n_bands,
                   int rows_per_band, int width, uint8_t* dev, void* stream);
 
+/* Bytes of device workspace eca_points_handcrafted needs for (batch, n_strips). */
+int eca_points_workspace_bytes(int batch, int n_strips, int64_t* out_bytes);
+
 /* score_frame_strips + select_candidates_batch, handcrafted variant
- * (estimator.py:35-52, handcrafted.py:148-205, 120-138). */
+ * (estimator.py:35-52, handcrafted.py:148-205, 120-138).  With a workspace of
+ * eca_points_workspace_bytes: bound-and-prune kernel + dense FP64 rescoring
+ * kernel (fast); workspace == NULL: the single-kernel path. */
 int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                            int64_t row_stride, const int32_t* strip_rows,
                            const int32_t* band_rows, int n_strips,
                            const EcaParams* params, int32_t* out_x, int32_t* out_y,
-                           double* out_score, void* stream);
+                           double* out_score, void* workspace, void* stream);
 
 /* Same, plus every column's FP64 score: out_scores[batch][n_strips][width]
  * (StripScoreRow.scores, handcrafted.py:25-31). */

@@ -248,6 +248,21 @@ def _dev_triplets(seed: int, attempts: int, max_n: int, device) -> torch.Tensor:
     return t
 
 
+_WORKSPACES: dict = {}
+
+
+def points_workspace(batch: int, n_strips: int, device) -> torch.Tensor:
+    """Device scratch for eca_points_handcrafted (survivor slots), cached per device."""
+    n = ctypes.c_int64()
+    _lib.check(_lib.load().eca_points_workspace_bytes(batch, n_strips, ctypes.byref(n)),
+               "eca_points_workspace_bytes")
+    t = _WORKSPACES.get(str(device))
+    if t is None or t.numel() < n.value:
+        t = torch.empty(max(n.value, 1 << 20), dtype=torch.uint8, device=device)
+        _WORKSPACES[str(device)] = t
+    return t
+
+
 _COUNTERS: dict = {}
 
 
@@ -308,8 +323,9 @@ def _handcrafted_batch(df: _DevFrames, width: int, height: int, rows, cfg: EcaCo
         _lib.check(rc, "eca_estimate_handcrafted")
         return xs, ys, sc, rec
     # throughput: strip kernel, then the fit kernel (one warp per frame)
+    ws = points_workspace(b, s, device)
     rc = lib.eca_points_handcrafted(df.ptr, b, df.fstride, df.rstride, _i32_array(rows), df.band, s,
-                                    ctypes.byref(params), _ptr(xs), _ptr(ys), _ptr(sc),
+                                    ctypes.byref(params), _ptr(xs), _ptr(ys), _ptr(sc), _ptr(ws),
                                     _stream(device))
     _lib.check(rc, "eca_points_handcrafted")
     rc = lib.eca_fit(_ptr(xs), _ptr(ys), _ptr(sc), b, 2 * s, ctypes.byref(params), _ptr(trip), 0,
@@ -427,9 +443,10 @@ def get_points_batch(frames, variant: EstimatorVariant = HANDCRAFTED, cfg: EcaCo
         xs = torch.empty((df.batch, 2 * s), dtype=torch.int32, device=dev)
         ys = torch.empty_like(xs)
         sc = torch.empty((df.batch, 2 * s), dtype=torch.float64, device=dev)
+        ws = points_workspace(df.batch, s, dev)
         rc = lib.eca_points_handcrafted(df.ptr, df.batch, df.fstride, df.rstride, _i32_array(rows),
                                         df.band, s, ctypes.byref(cfg.device_params(width, height)),
-                                        _ptr(xs), _ptr(ys), _ptr(sc), _stream(dev))
+                                        _ptr(xs), _ptr(ys), _ptr(sc), _ptr(ws), _stream(dev))
         _lib.check(rc, "eca_points_handcrafted")
     xs, ys, sc = xs.cpu().numpy(), ys.cpu().numpy(), sc.cpu().numpy()
     return [_candidates(xs[i], ys[i], sc[i], s) for i in range(len(xs))]

@@ -9,6 +9,7 @@
 
 #include "eca_fit.cuh"
 #include "eca_strip.cuh"
+#include "eca_points.cuh"
 
 using namespace eca;
 
@@ -103,6 +104,60 @@ int launch_strips_t(const StripJob& J, cudaStream_t stream) {
   return check_launch();
 }
 
+// ---- v6 points pipeline: bounds_kernel (warp per half row) + rescore_kernel
+int64_t points_workspace(int batch, int n_strips) {
+  const int64_t n_hr = int64_t(batch) * n_strips * 2;
+  return ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)) + n_hr * 4;
+}
+
+template <int NS>
+int launch_points_t(PointsJob PJ, cudaStream_t stream) {
+  auto kern = bounds_kernel<NS>;
+  StripJob& J = PJ.J;
+  const int W = J.p.width;
+  const int split = (W + 1) / 2;
+  const int half_w = split > W - split ? split : W - split;
+  const int nch = (half_w + kWChunk - 1) / kWChunk;
+  J.rowcap = (3 * (nch * kWChunk + 8) + 16 + 15) / 16 * 16;
+  static std::once_flag once;
+  std::call_once(once, [kern] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  int warps = 8;   // largest CTA whose smem fits twice per SM
+  while (warps > 1 && warp_layout(NS, J.rowcap, warps).total > 113 * 1024) warps /= 2;
+  const size_t smem = warp_layout(NS, J.rowcap, warps).total;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem) != cudaSuccess ||
+      per_sm < 1)
+    return ECA_ERR_CUDA;
+  const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
+  const int64_t need = (n_hr + warps - 1) / warps;
+  const int grid = int(need < int64_t(sm_count()) * per_sm ? need : int64_t(sm_count()) * per_sm);
+  ECA_TRACE("bounds kernel: NS %d warps %d smem %zu per_sm %d grid %d\n", NS, warps, smem, per_sm,
+            grid);
+  kern<<<grid, 32 * warps, smem, stream>>>(PJ);
+  if (cudaGetLastError() != cudaSuccess) return ECA_ERR_CUDA;
+  const int64_t blocks = (n_hr + 15) / 16;   // 4 warps x 4 half rows
+  rescore_kernel<<<unsigned(blocks), 128, 0, stream>>>(PJ);
+  return check_launch();
+}
+
+int launch_points(const StripJob& J, void* workspace, cudaStream_t stream) {
+  if (J.batch == 0) return ECA_OK;
+  const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
+  PointsJob PJ;
+  PJ.J = J;
+  PJ.slots = reinterpret_cast<SurvSlot*>(workspace);
+  PJ.counts = reinterpret_cast<int32_t*>(
+      reinterpret_cast<uint8_t*>(workspace) +
+      ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)));
+  static const int ns = [] {
+    const char* v = std::getenv("ECA_WSTAGES");
+    return v ? std::atoi(v) : 1;
+  }();
+  return ns == 2 ? launch_points_t<2>(PJ, stream) : launch_points_t<1>(PJ, stream);
+}
+
 template <bool kRows, bool kFused>
 int launch_strips(const StripJob& J, cudaStream_t stream) {
   if (J.batch == 0) return ECA_OK;
@@ -142,11 +197,17 @@ int check_fit_params(const EcaParams* params) {
 
 }  // namespace
 
+extern "C" int eca_points_workspace_bytes(int batch, int n_strips, int64_t* out_bytes) {
+  if (batch < 0 || n_strips < 1 || n_strips > ECA_MAX_STRIPS || !out_bytes) return ECA_ERR_ARG;
+  *out_bytes = points_workspace(batch, n_strips);
+  return ECA_OK;
+}
+
 extern "C" int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                                       int64_t row_stride, const int32_t* strip_rows,
                                       const int32_t* band_rows, int n_strips,
                                       const EcaParams* params, int32_t* out_x, int32_t* out_y,
-                                      double* out_score, void* stream) {
+                                      double* out_score, void* workspace, void* stream) {
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
                              n_strips, params);
@@ -155,7 +216,8 @@ extern "C" int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t 
   J.out_x = out_x;
   J.out_y = out_y;
   J.out_score = out_score;
-  return launch_strips<false, false>(J, as_stream(stream));
+  if (!workspace) return launch_strips<false, false>(J, as_stream(stream));  // single-kernel path
+  return launch_points(J, workspace, as_stream(stream));
 }
 
 extern "C" int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
@@ -237,11 +299,11 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
 
 #ifdef ECA_STATS
 extern "C" int eca_debug_strip_stats(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, g_strip_stats, sizeof(unsigned long long) * 16) != cudaSuccess)
+  if (cudaMemcpyFromSymbol(out, g_warp_stats, sizeof(unsigned long long) * 8) != cudaSuccess)
     return ECA_ERR_CUDA;
   if (reset) {
-    unsigned long long z[16] = {};
-    cudaMemcpyToSymbol(g_strip_stats, z, sizeof(z));
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_warp_stats, z, sizeof(z));
   }
   return ECA_OK;
 }

@@ -47,6 +47,10 @@ class ContentAreaEngine:
         self.sc = torch.empty((batch, 2 * s), dtype=torch.float64, device=d)
         self.rec = torch.empty((batch, 5), dtype=torch.float64, device=d)
         self.bands = torch.empty((batch, s * rpb, width, 3), dtype=torch.uint8, device=d)
+        nws = ctypes.c_int64()
+        _lib.check(_lib.load().eca_points_workspace_bytes(batch, s, ctypes.byref(nws)),
+                   "eca_points_workspace_bytes")
+        self.workspace = torch.empty(max(nws.value, 256), dtype=torch.uint8, device=d)
         self.rec_host = torch.empty((batch, 5), dtype=torch.float64, pin_memory=True)
         if isinstance(variant, api.Learned):
             self.probs = torch.empty((batch, s, width - 6), dtype=torch.float32, device=d)
@@ -90,7 +94,8 @@ class ContentAreaEngine:
             return
         rc = lib.eca_points_handcrafted(ctypes.c_void_p(ptr), self.batch, fstride, rstride,
                                         self._rows, band, s, ctypes.byref(self.params),
-                                        api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), st)
+                                        api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc),
+                                        api._ptr(self.workspace), st)
         _lib.check(rc, "eca_points_handcrafted")
         rc = lib.eca_fit(api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), self.batch, 2 * s,
                          ctypes.byref(self.params), api._ptr(self.trip), 0, api._ptr(self.rec), st)
@@ -113,7 +118,7 @@ class ContentAreaEngine:
         rc = _lib.load().eca_points_handcrafted(
             ctypes.c_void_p(f.data_ptr()), self.batch, f.stride(0), f.stride(1), self._rows, None,
             self.n_strips, ctypes.byref(self.params), api._ptr(self.xs), api._ptr(self.ys),
-            api._ptr(self.sc), api._stream(self.device))
+            api._ptr(self.sc), api._ptr(self.workspace), api._stream(self.device))
         _lib.check(rc, "eca_points_handcrafted")
 
     def run(self, frames: torch.Tensor) -> torch.Tensor:
