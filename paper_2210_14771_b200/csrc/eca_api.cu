@@ -176,7 +176,7 @@ struct FitJob {
 };
 
 // one warp per frame (same arithmetic order as the fused path's fit_warp)
-constexpr int kFitFramesPerCta = 4;
+constexpr int kFitFramesPerCta = 1;   // spread the frames over every SM
 
 __global__ void __launch_bounds__(32 * kFitFramesPerCta) fit_kernel(const __grid_constant__ FitJob J,
                                                                    int batch) {

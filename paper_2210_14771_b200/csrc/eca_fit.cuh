@@ -141,6 +141,41 @@ ECA_DEV bool is_inlier(double x, double y, const Circ& c, double tol) {
   return fabs(sub_rn(hypot(sub_rn(x, c.cx), sub_rn(y, c.cy)), c.r)) <= tol;
 }
 
+// The same decision with a cheap squared-distance screen: points whose d^2 is
+// outside a 1e-8 relative band around (r -/+ tol)^2 are decided without the
+// hypot (rounding of d^2 and of hypot are ~1e-16 relative, so the screen can
+// never disagree with is_inlier); only points in the band take the exact test.
+struct Ring {
+  double in_lo, in_hi, out_lo, out_hi;
+};
+
+ECA_DEV Ring ring_of(const Circ& c, double tol) {
+  const double e = 1e-8;
+  const double ro = c.r + tol, ri = c.r - tol;
+  Ring g;
+  g.in_hi = ro * ro * (1.0 - e);
+  g.out_hi = ro * ro * (1.0 + e);
+  if (ri > 1e-6 * c.r) {          // annulus: both edges screened
+    g.in_lo = ri * ri * (1.0 + e);
+    g.out_lo = ri * ri * (1.0 - e);
+  } else if (ri < -1e-6 * c.r) {  // disk: no inner edge
+    g.in_lo = -1.0;
+    g.out_lo = -1.0;
+  } else {                        // r ~ tol: inner edge ambiguous, test exactly
+    g.in_lo = __longlong_as_double(0x7ff0000000000000LL);
+    g.out_lo = -1.0;
+  }
+  return g;
+}
+
+ECA_DEV bool is_inlier_fast(double x, double y, const Circ& c, const Ring& g, double tol) {
+  const double dx = x - c.cx, dy = y - c.cy;
+  const double d2 = fma(dx, dx, dy * dy);
+  if (d2 <= g.in_hi && d2 >= g.in_lo) return true;
+  if (d2 > g.out_hi || d2 < g.out_lo) return false;
+  return is_inlier(x, y, c, tol);
+}
+
 // One frame on the whole CTA.  cand_* hold n_cand candidates in estimator.py:69
 // order; `l2_loads` reads them through L2 (written by other CTAs this launch).
 ECA_DEV void fit_frame(const int32_t* cand_x, const int32_t* cand_y, const double* cand_s,
@@ -323,11 +358,34 @@ ECA_DEV void fit_frame(const int32_t* cand_x, const int32_t* cand_y, const doubl
 // Single-warp variant (no CTA barriers): lane = hypothesis, each lane walks the
 // whole candidate list.  Used by the fused strip kernel, where the warp that
 // completes a frame fits it while the CTA's other warps keep scoring strips.
+// Per-candidate moment terms (identical for every hypothesis, so computed
+// once per frame in fitting.py's per-point order): x, y, z = x^2+y^2 and the
+// products the masked least squares sums.
+struct FitPt {
+  double x, y, z, xx, xy, yy, xz, yz;
+};
+
 struct FitScratchW {
-  double px[2 * ECA_MAX_STRIPS];
-  double py[2 * ECA_MAX_STRIPS];
+  FitPt pt[2 * ECA_MAX_STRIPS];
   double ps[2 * ECA_MAX_STRIPS];
 };
+
+// Inlier mask of candidate k against lane's circle, warp-uniform control flow:
+// the d^2 screen decides almost every point; the exact hypot test runs only
+// when some lane of the warp has a point inside the screen's band.
+ECA_DEV bool inlier_w(const FitPt& P, const Circ& c, const Ring& g, double tol) {
+  const double dx = P.x - c.cx, dy = P.y - c.cy;
+  const double d2 = fma(dx, dx, dy * dy);
+  bool in = d2 <= g.in_hi && d2 >= g.in_lo;
+  const bool amb = !in && !(d2 > g.out_hi || d2 < g.out_lo);
+  if (__any_sync(kFull, amb))
+    if (amb) in = is_inlier(P.x, P.y, c, tol);
+  return in;
+}
+
+ECA_DEV Ring ring_dead() {   // matches no point (hypothesis no longer alive)
+  return Ring{1.0, -1.0, -1.0, -1.0};
+}
 
 ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double* cand_s,
                       int n_cand, const EcaParams& p, const int16_t* trip, int exhaustive,
@@ -350,8 +408,16 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
     const unsigned bal = __ballot_sync(kFull, keep);
     if (keep) {
       const int pos = n + __popc(bal & ((1u << lane) - 1u));
-      fs->px[pos] = div_rn(sub_rn(double(x), p.center_x), double(W));
-      fs->py[pos] = div_rn(sub_rn(double(y), p.center_y), double(W));
+      FitPt q;
+      q.x = div_rn(sub_rn(double(x), p.center_x), double(W));
+      q.y = div_rn(sub_rn(double(y), p.center_y), double(W));
+      q.z = add_rn(mul_rn(q.x, q.x), mul_rn(q.y, q.y));
+      q.xx = mul_rn(q.x, q.x);
+      q.xy = mul_rn(q.x, q.y);
+      q.yy = mul_rn(q.y, q.y);
+      q.xz = mul_rn(q.x, q.z);
+      q.yz = mul_rn(q.y, q.z);
+      fs->pt[pos] = q;
       fs->ps[pos] = s;
     }
     n += __popc(bal);
@@ -379,43 +445,51 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
         i1 = t[1];
         i2 = t[2];
       }
-      c = circumcircle(fs->px[i0], fs->py[i0], fs->px[i1], fs->py[i1], fs->px[i2], fs->py[i2]);
+      c = circumcircle(fs->pt[i0].x, fs->pt[i0].y, fs->pt[i1].x, fs->pt[i1].y, fs->pt[i2].x,
+                       fs->pt[i2].y);
     }
+    // iterated masked least squares (fitting.py:193-203); every lane runs the
+    // loop, dead hypotheses with an empty ring (adding +0.0 for an outlier
+    // leaves a sum that started at +0.0 bit-identical)
     for (int it = 0; it < p.ransac_iterations && __any_sync(kFull, c.alive); ++it) {
-      if (!c.alive) continue;
+      const Ring g = c.alive ? ring_of(c, tol) : ring_dead();
       double mo[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
       for (int k = 0; k < n; ++k) {
-        const double x = fs->px[k], y = fs->py[k];
-        if (is_inlier(x, y, c, tol)) {
-          const double z = add_rn(mul_rn(x, x), mul_rn(y, y));
-          mo[0] = add_rn(mo[0], x);
-          mo[1] = add_rn(mo[1], y);
-          mo[2] = add_rn(mo[2], z);
-          mo[3] = add_rn(mo[3], mul_rn(x, x));
-          mo[4] = add_rn(mo[4], mul_rn(x, y));
-          mo[5] = add_rn(mo[5], mul_rn(y, y));
-          mo[6] = add_rn(mo[6], mul_rn(x, z));
-          mo[7] = add_rn(mo[7], mul_rn(y, z));
-          mo[8] += 1.0;
-        }
+        const FitPt P = fs->pt[k];
+        const bool in = inlier_w(P, c, g, tol);
+        mo[0] = add_rn(mo[0], in ? P.x : 0.0);
+        mo[1] = add_rn(mo[1], in ? P.y : 0.0);
+        mo[2] = add_rn(mo[2], in ? P.z : 0.0);
+        mo[3] = add_rn(mo[3], in ? P.xx : 0.0);
+        mo[4] = add_rn(mo[4], in ? P.xy : 0.0);
+        mo[5] = add_rn(mo[5], in ? P.yy : 0.0);
+        mo[6] = add_rn(mo[6], in ? P.xz : 0.0);
+        mo[7] = add_rn(mo[7], in ? P.yz : 0.0);
+        mo[8] += in ? 1.0 : 0.0;
       }
       double na, nb, nr;
-      if (lsq_solve(mo, int(mo[8]), na, nb, nr)) {
-        c.cx = na;
-        c.cy = nb;
-        c.r = nr;
-      } else {
-        c.alive = false;
+      if (c.alive) {
+        if (lsq_solve(mo, int(mo[8]), na, nb, nr)) {
+          c.cx = na;
+          c.cy = nb;
+          c.r = nr;
+        } else {
+          c.alive = false;
+        }
       }
     }
     double score = 0.0;
     int inl = 0;
-    if (c.alive)
-      for (int k = 0; k < n; ++k)
-        if (is_inlier(fs->px[k], fs->py[k], c, tol)) {
-          score = add_rn(score, fs->ps[k]);
-          ++inl;
-        }
+    {
+      const Ring g = c.alive ? ring_of(c, tol) : ring_dead();
+#pragma unroll 4
+      for (int k = 0; k < n; ++k) {
+        const bool in = inlier_w(fs->pt[k], c, g, tol);
+        score = add_rn(score, in ? fs->ps[k] : 0.0);
+        inl += in;
+      }
+    }
     const bool gated = (c.r < p.min_radius_frac) || (c.r > p.max_radius_frac) ||
                        (hypot(c.cx, c.cy) > p.max_center_offset_frac);
     const bool surv = c.alive && !gated;

@@ -1,8 +1,7 @@
-"""Small ncu target: 3x points (bounds + rescore) on a B=256 1080p batch."""
-import sys, ctypes, torch
+"""Small ncu target: 3x engine.run (bounds + rescore + fit) on a B=256 1080p batch."""
+import sys, torch
 sys.path.insert(0, '.')
 import paper_2210_14771_b200 as eb
-from paper_2210_14771_b200 import _lib, api
 import bench
 B = 256
 dev = torch.device('cuda', 0)
@@ -10,6 +9,6 @@ base = bench.base_frames(40)
 frames = torch.from_numpy(base[[i % 40 for i in range(B)]]).to(dev)
 eng = eb.ContentAreaEngine(1080, 1920, B, device=dev)
 for _ in range(3):
-    eng.points(frames)
+    eng.run(frames)
 torch.cuda.synchronize()
 print("ok")
