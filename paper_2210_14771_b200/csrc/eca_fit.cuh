@@ -449,24 +449,25 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
                        fs->pt[i2].y);
     }
     // iterated masked least squares (fitting.py:193-203); every lane runs the
-    // loop, dead hypotheses with an empty ring (adding +0.0 for an outlier
-    // leaves a sum that started at +0.0 bit-identical)
+    // loop, dead hypotheses with an empty ring.  Outliers contribute fma(0, v, s)
+    // = s + (+-0) = s exactly (the sums start at +0.0, so no -0.0 appears).
     for (int it = 0; it < p.ransac_iterations && __any_sync(kFull, c.alive); ++it) {
       const Ring g = c.alive ? ring_of(c, tol) : ring_dead();
       double mo[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll 4
       for (int k = 0; k < n; ++k) {
         const FitPt P = fs->pt[k];
-        const bool in = inlier_w(P, c, g, tol);
-        mo[0] = add_rn(mo[0], in ? P.x : 0.0);
-        mo[1] = add_rn(mo[1], in ? P.y : 0.0);
-        mo[2] = add_rn(mo[2], in ? P.z : 0.0);
-        mo[3] = add_rn(mo[3], in ? P.xx : 0.0);
-        mo[4] = add_rn(mo[4], in ? P.xy : 0.0);
-        mo[5] = add_rn(mo[5], in ? P.yy : 0.0);
-        mo[6] = add_rn(mo[6], in ? P.xz : 0.0);
-        mo[7] = add_rn(mo[7], in ? P.yz : 0.0);
-        mo[8] += in ? 1.0 : 0.0;
+        // w in {0, 1}: fma(1, v, s) == add_rn(s, v) and fma(0, v, s) == s
+        const double w = inlier_w(P, c, g, tol) ? 1.0 : 0.0;
+        mo[0] = __fma_rn(w, P.x, mo[0]);
+        mo[1] = __fma_rn(w, P.y, mo[1]);
+        mo[2] = __fma_rn(w, P.z, mo[2]);
+        mo[3] = __fma_rn(w, P.xx, mo[3]);
+        mo[4] = __fma_rn(w, P.xy, mo[4]);
+        mo[5] = __fma_rn(w, P.yy, mo[5]);
+        mo[6] = __fma_rn(w, P.xz, mo[6]);
+        mo[7] = __fma_rn(w, P.yz, mo[7]);
+        mo[8] = add_rn(mo[8], w);
       }
       double na, nb, nr;
       if (c.alive) {
@@ -486,7 +487,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
 #pragma unroll 4
       for (int k = 0; k < n; ++k) {
         const bool in = inlier_w(fs->pt[k], c, g, tol);
-        score = add_rn(score, in ? fs->ps[k] : 0.0);
+        score = __fma_rn(in ? 1.0 : 0.0, fs->ps[k], score);
         inl += in;
       }
     }
