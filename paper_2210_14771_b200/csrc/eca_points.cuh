@@ -1,4 +1,4 @@
-// K1 (v6): handcrafted candidate extraction as three dense stages
+// K1 (v7): handcrafted candidate extraction as two dense stages
 // (handcrafted.py:148-205, 120-138).
 //
 //  bounds_kernel   warp per HALF strip row, persistent, own TMA ring: exact
@@ -11,10 +11,25 @@
 //                  then the half-row argmax (outermost tie-break) by shuffles.
 //  (fit_kernel)    eca_fit.cuh, one warp per frame.
 //
-// Splitting the FP64 work out keeps its long latency chains off the pixel
-// warps and runs it at full lane occupancy.  A half row with more than kSlots
-// survivors (adversarial / near-flat rows) is resolved inside bounds_kernel
-// with the same FP64 code.
+// bounds_kernel, per half row:
+//  pass 1   chunks of 256 columns in scan order (left half: x ascending from
+//           the border, right half: x descending from the border), 8 columns
+//           per lane ("lane-chunk").  Each lane loads its 8 columns plus both
+//           neighbours straight from shared memory, so lanes exchange no
+//           pixels.  Per lane-chunk only the upper bound
+//           U = T_up(max |g|^2) * D_up(preceding sum before the lane-chunk)
+//           is kept; it bounds every column's score because T rises with |g|,
+//           D falls with the preceding sum and A <= 1.
+//  step A/B the 4 lane-chunks of highest U are evaluated column by column
+//           (one lane per column): L = T_lo*A_lo*D_lo is a lower bound of the
+//           half's max score, so LB = max L.
+//  step C   every other lane-chunk with U >= LB is compacted and evaluated
+//           the same way; columns with U_col = T_up*D_up*A_up >= LB survive.
+// A half whose LB is below the FP32 resolution (tau) keeps every non-flat
+// column instead (flat-row residues, see eca_prefilter_bound).  A half row
+// with more than kSlots survivors is resolved in this kernel with the same
+// FP64 code.  Splitting the FP64 work out keeps its long latency chains off
+// the pixel warps and runs it at full lane occupancy.
 #pragma once
 
 #include "eca_strip.cuh"
@@ -38,6 +53,40 @@ struct PointsJob {
   int32_t* counts;     // [n_halfrows]: survivors, or -1 when resolved in bounds_kernel
 };
 
+// RGB sums of the 10 pixels x0-1 .. x0+8 of one staged row; B = smem byte of
+// pixel x0.  `al`: B % 8 == 0 (warp-uniform), else funnel-shifted word loads.
+ECA_DEV void load10(const uint8_t* st, int B, bool al, int s[10]) {
+  uint32_t w[8];   // w[0]: bytes B-4..B-1, w[1..6]: B..B+23, w[7]: B+24..B+27
+  if (al) {
+    const uint2* p = reinterpret_cast<const uint2*>(st + B);
+    const uint2 a = p[0], b = p[1], c = p[2];
+    w[0] = *reinterpret_cast<const uint32_t*>(st + B - 4);
+    w[1] = a.x; w[2] = a.y; w[3] = b.x; w[4] = b.y; w[5] = c.x; w[6] = c.y;
+    w[7] = *reinterpret_cast<const uint32_t*>(st + B + 24);
+  } else {
+    const int a0 = (B - 4) & ~3;
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(st + a0);
+    const int sh = ((B - 4) - a0) * 8;
+    uint32_t v[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = wp[k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = __funnelshift_r(v[k], v[k + 1], sh);
+  }
+  s[0] = __dp4a(w[0], 0x01010100u, 0u);
+  sums8(w + 1, s + 1);
+  s[9] = __dp4a(w[7], 0x00010101u, 0u);
+}
+
+// One column evaluated by one lane (steps A-C).
+struct ColEval {
+  int x, pre;
+  int l[3], m[3], r[3];
+  float U, L;
+  bool ok;     // scoreable column of this half (x in [slo, shi])
+  bool flat;   // numpy's gx and gy are exactly 0.0 (score exactly 0)
+};
+
 template <int NS>
 __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ PointsJob PJ) {
   const StripJob& J = PJ.J;
@@ -52,7 +101,10 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
   float2* atab = reinterpret_cast<float2*>(smem + WL.atab);
   uint8_t* mine = smem + WL.warp0 + size_t(wib) * WL.per_warp;
   uint32_t* list = reinterpret_cast<uint32_t*>(mine + WL.list);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(mine + WL.list + kWListCap * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(mine + WL.bars);
+  float* ut_s = reinterpret_cast<float*>(mine + WL.ut);
+  uint16_t* ex_s = reinterpret_cast<uint16_t*>(mine + WL.exs);
+  uint16_t* sel_s = reinterpret_cast<uint16_t*>(mine + WL.sel);
 
   {
     const float lo_f = 1.0f - kPadRel, hi_f = 1.0f + kPadRel;
@@ -82,6 +134,10 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
   const TermK tk{float(-2.0 * log2e / (3.0 * J.p.gradient_threshold)),
                  float(2.0 * log2e / (3.0 * J.p.intensity_threshold))};
   const float lo_f = 1.0f - kPadRel, hi_f = 1.0f + kPadRel;
+  const double cxf = div_rn(double(W - 1), 2.0);
+  const double cyf = div_rn(double(H - 1), 2.0);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int gi = lane & 7;   // column within an evaluated lane-chunk
 
   int stage = 0;
   uint32_t phase = 0;
@@ -92,9 +148,10 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
     const int strip = fs - frame * S;
     const int y = J.rows[strip];
     const int d2y = (H - 1) - 2 * y;
-    const int xa = half ? split : 0, xb = half ? W : split;
-    const int xs = half ? split - 1 : 0;
-    const int xe = half ? W : min(split + 1, W);
+    const int hw = half ? W - split : split;        // columns in this half
+    const int xs = half ? split - 1 : 0;            // first staged column
+    const int lo = half ? split : 0, hi = half ? W - 1 : split - 1;   // the half, inclusive
+    const int slo = max(lo, 1), shi = min(hi, W - 2);                 // scoreable columns
     uint8_t* st = mine + stage * WL.stage;
     int rb[3];
     {
@@ -103,117 +160,122 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
 #pragma unroll
       for (int r = 0; r < 3; ++r)
         rb[r] = r * J.rowcap + int(reinterpret_cast<uintptr_t>(row0 + r * J.row_stride) & 15) -
-                3 * xs;
+                3 * xs;   // smem byte of column x in row r = rb[r] + 3x
     }
+    // first column (x order) of lane-chunk (k, l)
+    auto xa_of = [&](int k, int l) -> int {
+      return half ? W - kPx - kWChunk * k - kPx * l : kWChunk * k + kPx * l;
+    };
+    const int xa0 = xa_of(0, 0);
+    const bool al = (((rb[0] + 3 * xa0) | (rb[1] + 3 * xa0) | (rb[2] + 3 * xa0)) & 7) == 0;
+    const int nch = (hw + kWChunk - 1) / kWChunk;
     mbar_wait(&bars[stage], phase);
 
-    const int nch = (xb - xa + kWChunk - 1) / kWChunk;
-    auto chunk_x0 = [&](int k) -> int {
-      return half ? (xa + (nch - 1 - k) * kWChunk) : (xa + k * kWChunk);
-    };
-    auto abin = [&](int gx3, int gy3, int x) -> int {
-      const int d2x = (W - 1) - 2 * x;
-      const int dot = gx3 * d2x + gy3 * d2y;
-      const int crs = abs(gx3 * d2y - gy3 * d2x);
-      const float fd = float(abs(dot)), fc = float(crs);
-      const float ps = fc * rcpf(fd + fc);
-      const int k = min(int((dot >= 0 ? ps : 2.0f - ps) * (kABins / 2)), kABins - 1);
-      return (dot == 0 && crs == 0) ? kABins : k;
-    };
-    auto col_sum = [&](int r, int x) -> int { return px_sum(st, rb[r] + 3 * x); };
-    auto load_chunk = [&](int x0, int c[kPx + 2], int e[kPx + 2], int ctr[kPx]) {
-      int s0[kPx], s1[kPx], s2[kPx];
-      uint32_t w[6];
-      load24(st, rb[0] + 3 * x0, w);
-      sums8(w, s0);
-      load24(st, rb[1] + 3 * x0, w);
-      sums8(w, s1);
-      load24(st, rb[2] + 3 * x0, w);
-      sums8(w, s2);
-#pragma unroll
-      for (int i = 0; i < kPx; ++i) {
-        c[i + 1] = s0[i] + 2 * s1[i] + s2[i];
-        e[i + 1] = s2[i] - s0[i];
-        ctr[i] = (x0 + i >= xa && x0 + i < xb) ? s1[i] : 0;
-      }
-      c[0] = __shfl_up_sync(kFull, c[kPx], 1);
-      e[0] = __shfl_up_sync(kFull, e[kPx], 1);
-      c[kPx + 1] = __shfl_down_sync(kFull, c[1], 1);
-      e[kPx + 1] = __shfl_down_sync(kFull, e[1], 1);
-      if (lane == 0 && x0 - 1 >= xs) {
-        const int a0 = col_sum(0, x0 - 1), a1 = col_sum(1, x0 - 1), a2 = col_sum(2, x0 - 1);
-        c[0] = a0 + 2 * a1 + a2;
-        e[0] = a2 - a0;
-      }
-      if (lane == 31 && x0 + kPx < xe) {
-        const int a0 = col_sum(0, x0 + kPx), a1 = col_sum(1, x0 + kPx), a2 = col_sum(2, x0 + kPx);
-        c[kPx + 1] = a0 + 2 * a1 + a2;
-        e[kPx + 1] = a2 - a0;
-      }
-    };
-
-    // ---- pass 1: lane-chunk bounds (U over its columns, L of its best column)
-    float ut[kWMaxChunks];
-    int exk[kWMaxChunks];
-    float lb = 0.0f;
+    // ---- pass 1: U of every lane-chunk
     int carry = 0;
 #pragma unroll 1
     for (int k = 0; k < nch; ++k) {
-      const int x0 = chunk_x0(k) + kPx * lane;
-      int c[kPx + 2], e[kPx + 2], ctr[kPx];
-      load_chunk(x0, c, e, ctr);
-      int tmax = 0;
+      const int xa = xa_of(k, lane);
+      int s0[10], s1[10], s2[10];
+      load10(st, rb[0] + 3 * xa, al, s0);
+      load10(st, rb[1] + 3 * xa, al, s1);
+      load10(st, rb[2] + 3 * xa, al, s2);
+      int c[10], e[10];
 #pragma unroll
-      for (int i = 0; i < kPx; ++i) tmax = max(tmax, ctr[i]);
+      for (int i = 0; i < 10; ++i) {
+        c[i] = s0[i] + 2 * s1[i] + s2[i];
+        e[i] = s2[i] - s0[i];
+      }
+      int tmax = 0, qmax = 0;
+#pragma unroll
+      for (int i = 1; i <= kPx; ++i) tmax = max(tmax, s1[i]);
+      if (k == 0 || k == nch - 1) {   // border / tail chunk: only scoreable columns
+#pragma unroll
+        for (int i = 0; i < kPx; ++i) {
+          const int gx3 = c[i + 2] - c[i], gy3 = e[i] + 2 * e[i + 1] + e[i + 2];
+          const int q = gx3 * gx3 + gy3 * gy3;
+          const bool in = unsigned(xa + i - slo) <= unsigned(shi - slo);
+          qmax = max(qmax, in ? q : 0);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kPx; ++i) {
+          const int gx3 = c[i + 2] - c[i], gy3 = e[i] + 2 * e[i + 1] + e[i + 2];
+          qmax = max(qmax, gx3 * gx3 + gy3 * gy3);
+        }
+      }
       int sc = tmax;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const int v = half ? __shfl_down_sync(kFull, sc, d) : __shfl_up_sync(kFull, sc, d);
-        if (half ? (lane + d < 32) : (lane >= d)) sc = max(sc, v);
+        const int v = __shfl_up_sync(kFull, sc, d);
+        if (lane >= d) sc = max(sc, v);
       }
-      int ex = half ? __shfl_down_sync(kFull, sc, 1) : __shfl_up_sync(kFull, sc, 1);
-      if (half ? lane == 31 : lane == 0) ex = 0;
-      ex = max(ex, carry);
-      carry = max(carry, __shfl_sync(kFull, sc, half ? 0 : 31));
-      exk[k] = ex;
-      // per column: V = T_up * D_up needs the column's own preceding sum; the
-      // lane bound uses the head (smallest preceding) and the best column
-      float u = 0.0f, l = 0.0f;
-      int qmax = 0, bgx = 0, bgy = 0, bi = 0;
-#pragma unroll
-      for (int i = 0; i < kPx; ++i) {
-        const int x = x0 + i;
-        const int gx3 = c[i + 2] - c[i], gy3 = e[i] + 2 * e[i + 1] + e[i + 2];
-        const int q = (x >= xa && x < xb && x >= 1 && x <= W - 2) ? gx3 * gx3 + gy3 * gy3 : 0;
-        if (q > qmax) {
-          qmax = q;
-          bgx = gx3;
-          bgy = gy3;
-          bi = i;
-        }
-      }
-      if (qmax > 0) {
-        int pbi = ex;
-#pragma unroll
-        for (int i = 0; i < kPx; ++i)
-          if (half ? (i > bi) : (i < bi)) pbi = max(pbi, ctr[i]);
-        const float t = t_term(qmax, tk);
-        u = fminf(t * hi_f, 1.0f) * fminf(d_term(ex, tk) * hi_f, 1.0f);
-        l = t * lo_f * d_term(pbi, tk) * lo_f * atab[abin(bgx, bgy, x0 + bi)].x;
-      }
-      ut[k] = u;
-      lb = fmaxf(lb, l);
+      int ex = __shfl_up_sync(kFull, sc, 1);
+      ex = max(lane == 0 ? 0 : ex, carry);
+      carry = max(carry, __shfl_sync(kFull, sc, 31));
+      float u = 0.0f;
+      if (qmax > 0)
+        u = fminf(t_term(qmax, tk) * hi_f, 1.0f) * fminf(d_term(ex, tk) * hi_f, 1.0f);
+      ut_s[k * 32 + lane] = u;
+      ex_s[k * 32 + lane] = uint16_t(ex);
     }
-    lb = warp_max(lb);
-    const bool full = !(lb >= J.tau);
+    __syncwarp();
 
-    // ---- pass 2: survivors of chunks whose bound reaches LB
+    // ---- one lane per column of lane-chunk entry e = (k << 5 | l)
+    auto eval = [&](bool valid, int e) -> ColEval {
+      ColEval ce;
+      const int k = e >> 5, l = e & 31;
+      ce.x = xa_of(k, l) + gi;
+      const bool in_half = valid && ce.x >= lo && ce.x <= hi;
+      ce.ok = in_half && ce.x >= slo && ce.x <= shi;
+      const int xc = in_half ? ce.x : lo;   // keep the reads inside the staged rows
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        ce.l[r] = px_sum(st, rb[r] + 3 * (xc - 1));
+        ce.m[r] = px_sum(st, rb[r] + 3 * xc);
+        ce.r[r] = px_sum(st, rb[r] + 3 * (xc + 1));
+      }
+      // preceding sum: lane-chunk prefix + exclusive max over the earlier
+      // columns of the lane-chunk in scan order (x ascending left, descending right)
+      int v = in_half ? ce.m[1] : 0;
+#pragma unroll
+      for (int d = 1; d < kPx; d <<= 1) {
+        const int o = half ? __shfl_down_sync(kFull, v, d, kPx) : __shfl_up_sync(kFull, v, d, kPx);
+        if (half ? gi + d < kPx : gi >= d) v = max(v, o);
+      }
+      int pre = half ? __shfl_down_sync(kFull, v, 1, kPx) : __shfl_up_sync(kFull, v, 1, kPx);
+      if (half ? gi == kPx - 1 : gi == 0) pre = 0;
+      ce.pre = max(pre, valid ? int(ex_s[e]) : 0);
+      const int cl = ce.l[0] + 2 * ce.l[1] + ce.l[2], cr = ce.r[0] + 2 * ce.r[1] + ce.r[2];
+      const int gx3 = cr - cl;
+      const int gy3 = (ce.l[2] - ce.l[0]) + 2 * (ce.m[2] - ce.m[0]) + (ce.r[2] - ce.r[0]);
+      const int q = gx3 * gx3 + gy3 * gy3;
+      ce.U = 0.0f;
+      ce.L = 0.0f;
+      if (ce.ok && q > 0) {
+        const int d2x = (W - 1) - 2 * ce.x;
+        const int dot = gx3 * d2x + gy3 * d2y;
+        const int crs = abs(gx3 * d2y - gy3 * d2x);
+        const float fd = float(abs(dot)), fc = float(crs);
+        const float ps = fc * rcpf(fd + fc);
+        int ab = min(int((dot >= 0 ? ps : 2.0f - ps) * (kABins / 2)), kABins - 1);
+        if (dot == 0 && crs == 0) ab = kABins;
+        const float2 a = atab[ab];
+        const float t = t_term(q, tk), dd = d_term(ce.pre, tk);
+        ce.U = fminf(t * hi_f, 1.0f) * fminf(dd * hi_f, 1.0f) * a.y;
+        ce.L = t * lo_f * dd * lo_f * a.x;
+      }
+      ce.flat = ce.l[0] == ce.r[0] && ce.l[1] == ce.r[1] && ce.l[2] == ce.r[2] &&
+                ce.l[0] == ce.l[2] && ce.m[0] == ce.m[2] && ce.r[0] == ce.r[2];
+      return ce;
+    };
+
+    // survivors: list entries (x | pre << 16) with their column bound U
+    float* ulist = reinterpret_cast<float*>(mine + WL.ulist);
     int n_list = 0;
     bool flushed = false;
     Best best = half ? Best{0.0, W - 1} : Best{0.0, 0};   // border columns score 0
-    const double cxf = div_rn(double(W - 1), 2.0);
-    const double cyf = div_rn(double(H - 1), 2.0);
-    auto flush = [&]() {   // rare: score the pending survivors here
+    auto flush = [&]() {   // rare: score the pending survivors in this warp
       for (int k = lane; k < n_list; k += 32) {
         int x;
         const double s = score_entry(list[k], st, rb, y, cxf, cyf, J.p, x);
@@ -223,91 +285,118 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
       flushed = true;
       __syncwarp();
     };
-#pragma unroll 1
-    for (int k = 0; k < nch; ++k) {
-      const bool look = full || (ut[k] > 0.0f && ut[k] >= lb);
-      if (!__any_sync(kFull, look)) continue;
-      const int x0 = chunk_x0(k) + kPx * lane;
-      int c[kPx + 2], e[kPx + 2], ctr[kPx];
-      load_chunk(x0, c, e, ctr);
-      int pre[kPx];
-      {
-        int run = exk[k];
-        if (half) {
-#pragma unroll
-          for (int i = kPx - 1; i >= 0; --i) {
-            pre[i] = run;
-            run = max(run, ctr[i]);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < kPx; ++i) {
-            pre[i] = run;
-            run = max(run, ctr[i]);
-          }
+    auto compact = [&](float thr) {   // drop entries whose bound fell below LB
+      int out = 0;
+      for (int base = 0; base < n_list; base += 32) {
+        const int k = base + lane;
+        const uint32_t v = k < n_list ? list[k] : 0u;
+        const float u = k < n_list ? ulist[k] : 0.0f;
+        const bool keep = k < n_list && u >= thr;
+        const unsigned bm = __ballot_sync(kFull, keep);
+        __syncwarp();
+        if (keep) {
+          const int pos = out + __popc(bm & lt_mask);
+          list[pos] = v;
+          ulist[pos] = u;
         }
+        out += __popc(bm);
+        __syncwarp();
       }
-      uint32_t surv = 0;
-      if (look) {
-#pragma unroll
-        for (int i = 0; i < kPx; ++i) {
-          const int x = x0 + i;
-          if (x < xa || x >= xb || x < 1 || x > W - 2) continue;
-          bool s;
-          if (full) {
-            s = !flat_column(st, rb, x);
-          } else {
-            const int gx3 = c[i + 2] - c[i], gy3 = e[i] + 2 * e[i + 1] + e[i + 2];
-            const int q = gx3 * gx3 + gy3 * gy3;
-            s = false;
-            if (q > 0) {
-              const float v = fminf(t_term(q, tk) * hi_f, 1.0f) *
-                              fminf(d_term(pre[i], tk) * hi_f, 1.0f);
-              s = v >= lb && v * atab[abin(gx3, gy3, x)].y >= lb;
-            }
-          }
-          if (s) surv |= 1u << i;
-        }
-      }
-      const int cnt = __popc(surv);
-      int incl = cnt;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int v = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += v;
-      }
-      const int tot = __shfl_sync(kFull, incl, 31);
+      n_list = out;
+    };
+    float lb = 0.0f;
+    bool full = false;
+    auto emit = [&](bool valid, const ColEval& ce) {
+      const bool surv = valid && ce.ok && (full ? !ce.flat : ce.U >= lb);
+      const unsigned bm = __ballot_sync(kFull, surv);
+      const int tot = __popc(bm);
+      if (tot == 0) return;
+      if (n_list + tot > kWListCap && lb >= J.tau) compact(lb);
       if (n_list + tot > kWListCap) flush();
-      int base = n_list + incl - cnt;
-#pragma unroll
-      for (int i = 0; i < kPx; ++i)
-        if ((surv >> i) & 1u) list[base++] = uint32_t(x0 + i) | (uint32_t(pre[i]) << 16);
+      if (surv) {
+        const int pos = n_list + __popc(bm & lt_mask);
+        list[pos] = uint32_t(ce.x) | (uint32_t(ce.pre) << 16);
+        ulist[pos] = ce.U;
+      }
       n_list += tot;
       __syncwarp();
+    };
+
+    // ---- step A: the (up to) 4 lane-chunks of highest U, from distinct lanes
+    float bu = -1.0f;
+    int bk = 0;
+    for (int k = 0; k < nch; ++k) {
+      const float v = ut_s[k * 32 + lane];
+      if (v > bu) {
+        bu = v;
+        bk = k;
+      }
     }
+    int my_e = 0;   // entry this lane's 8-lane group evaluates in step B
+    int n_a = 0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const float m = warp_max(bu);
+      if (!(m > 0.0f)) break;
+      const int wl = __ffs(__ballot_sync(kFull, bu == m)) - 1;
+      const int wk = __shfl_sync(kFull, bk, wl);
+      if ((lane >> 3) == g) my_e = (wk << 5) | wl;
+      if (lane == wl) bu = -1.0f;
+      n_a = g + 1;
+    }
+    // ---- step B: evaluate them -> LB, then their survivors
+    const bool va = (lane >> 3) < n_a;
+    {
+      const ColEval ca = eval(va, my_e);
+      lb = warp_max(ca.L);
+      full = !(lb >= J.tau);
+      emit(va, ca);
+    }
+    if (va && gi == 0) ut_s[(my_e >> 5) * 32 + (my_e & 31)] = -1.0f;   // evaluated
+    __syncwarp();
+
+    // ---- step C: the other lane-chunks whose U reaches LB (all of them if
+    // full); LB tightens with every evaluated group
+    int n_sel = 0;
+    for (int k = 0; k < nch; ++k) {
+      const float v = ut_s[k * 32 + lane];
+      const bool s = full ? v >= 0.0f : (v > 0.0f && v >= lb);
+      const unsigned bm = __ballot_sync(kFull, s);
+      if (s) sel_s[n_sel + __popc(bm & lt_mask)] = uint16_t((k << 5) | lane);
+      n_sel += __popc(bm);
+    }
+    __syncwarp();
+    for (int g0 = 0; g0 < n_sel; g0 += 4) {
+      const int p = g0 + (lane >> 3);
+      const bool vc = p < n_sel;
+      const int e = vc ? int(sel_s[p]) : 0;
+      if (!full && !__any_sync(kFull, vc && ut_s[(e >> 5) * 32 + (e & 31)] >= lb)) continue;
+      const ColEval cc = eval(vc, e);
+      lb = fmaxf(lb, warp_max(cc.L));
+      emit(vc, cc);
+    }
+    if (lb >= J.tau) compact(lb);   // final LB: full rows keep every non-flat column
 
     // ---- hand the survivors to the rescore stage (or resolve here if many)
     const int hrow = item;
-    SurvSlot* out = PJ.slots + size_t(hrow) * kSlots;
     if (!flushed && n_list <= kSlots) {
       if (lane < n_list) {
         const uint32_t v = list[lane];
         const int x = int(v & 0xffffu);
-        SurvSlot s;
-        s.x = uint16_t(x);
-        s.pre = uint16_t(v >> 16);
+        SurvSlot sl;
+        sl.x = uint16_t(x);
+        sl.pre = uint16_t(v >> 16);
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
-          s.l[r] = uint16_t(col_sum(r, x - 1));
-          s.m[r] = uint16_t(col_sum(r, x));
-          s.r[r] = uint16_t(col_sum(r, x + 1));
+          sl.l[r] = uint16_t(px_sum(st, rb[r] + 3 * (x - 1)));
+          sl.m[r] = uint16_t(px_sum(st, rb[r] + 3 * x));
+          sl.r[r] = uint16_t(px_sum(st, rb[r] + 3 * (x + 1)));
         }
-        s.pad = 0;
-        out[lane] = s;
+        sl.pad = 0;
+        PJ.slots[size_t(hrow) * kSlots + lane] = sl;
       }
       if (lane == 0) PJ.counts[hrow] = n_list;
     } else {
-      // rare: more survivors than slots -> score them in this warp
       flush();
       best = warp_best(best, !half);
       if (lane == 0) {
