@@ -117,19 +117,55 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream) {
   const int W = J.p.width;
   const int split = (W + 1) / 2;
   const int half_w = split > W - split ? split : W - split;
-  const int nch = (half_w + kWChunk - 1) / kWChunk;
-  J.rowcap = (3 * (nch * kWChunk + 8) + 16 + 15) / 16 * 16;
+  // a row holds exactly the staged bytes (<= 15 B misalignment + the half and
+  // its neighbour column); lane-chunk reads past either end of a row land in
+  // the neighbouring row / per-warp scratch (< 3*257 B) and only feed masked
+  // columns
+  J.rowcap = (15 + 3 * (half_w + 1) + 15) / 16 * 16;
   static std::once_flag once;
   std::call_once(once, [kern] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
-  int warps = 8;   // largest CTA whose smem fits twice per SM
-  while (warps > 1 && warp_layout(NS, J.rowcap, warps).total > 113 * 1024) warps /= 2;
+  // CTA shape: the smallest CTA (>= 2 warps) whose resident warps per SM
+  // reach 90% of the best shape's.  Small independent CTAs measured faster
+  // than large ones at equal occupancy (B200, 1080p: 3 warps x 6 CTAs
+  // 51 us vs 5 x 4 57 us).
+  int occ[9] = {0};
+  int best_occ = 0;
+  for (int w = 1; w <= 8; ++w) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * w,
+                                                      warp_layout(NS, J.rowcap, w).total) !=
+        cudaSuccess)
+      return ECA_ERR_CUDA;
+    occ[w] = b;
+    if (b * w > best_occ) best_occ = b * w;
+    ECA_TRACE("bounds kernel: %d warps/CTA -> %d CTAs/SM (smem %zu)\n", w, b,
+              warp_layout(NS, J.rowcap, w).total);
+  }
+  int warps = 0, per_sm = 0;
+  for (int w = 2; w <= 8 && !warps; ++w)
+    if (10 * occ[w] * w >= 9 * best_occ) {
+      warps = w;
+      per_sm = occ[w];
+    }
+  if (!warps) {
+    warps = 1;
+    per_sm = occ[1];
+  }
+  static const int force_w = [] {   // tuning hook: ECA_BWARPS=<warps per CTA>
+    const char* v = std::getenv("ECA_BWARPS");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (force_w >= 1 && force_w <= 8) {
+    warps = force_w;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps,
+                                                      warp_layout(NS, J.rowcap, warps).total) !=
+        cudaSuccess)
+      return ECA_ERR_CUDA;
+  }
+  if (per_sm < 1) return ECA_ERR_CUDA;
   const size_t smem = warp_layout(NS, J.rowcap, warps).total;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem) != cudaSuccess ||
-      per_sm < 1)
-    return ECA_ERR_CUDA;
   const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
   const int64_t need = (n_hr + warps - 1) / warps;
   const int grid = int(need < int64_t(sm_count()) * per_sm ? need : int64_t(sm_count()) * per_sm);

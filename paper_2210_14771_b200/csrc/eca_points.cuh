@@ -32,6 +32,8 @@
 // the pixel warps and runs it at full lane occupancy.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "eca_strip.cuh"
 #include "eca_strip_w.cuh"
 
@@ -88,7 +90,8 @@ struct ColEval {
 };
 
 template <int NS>
-__global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ PointsJob PJ) {
+// 96 registers: 5 warps per SM sub-partition (112 would allow only 4)
+__global__ void __maxnreg__(96) bounds_kernel(const __grid_constant__ PointsJob PJ) {
   const StripJob& J = PJ.J;
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
   uint8_t* mine = smem + WL.warp0 + size_t(wib) * WL.per_warp;
   uint32_t* list = reinterpret_cast<uint32_t*>(mine + WL.list);
   uint64_t* bars = reinterpret_cast<uint64_t*>(mine + WL.bars);
-  float* ut_s = reinterpret_cast<float*>(mine + WL.ut);
+  __half* ut_s = reinterpret_cast<__half*>(mine + WL.ut);   // rounded up: still a bound
   uint16_t* ex_s = reinterpret_cast<uint16_t*>(mine + WL.exs);
   uint16_t* sel_s = reinterpret_cast<uint16_t*>(mine + WL.sel);
 
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
       float u = 0.0f;
       if (qmax > 0)
         u = fminf(t_term(qmax, tk) * hi_f, 1.0f) * fminf(d_term(ex, tk) * hi_f, 1.0f);
-      ut_s[k * 32 + lane] = u;
+      ut_s[k * 32 + lane] = __float2half_ru(u);
       ex_s[k * 32 + lane] = uint16_t(ex);
     }
     __syncwarp();
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
     float bu = -1.0f;
     int bk = 0;
     for (int k = 0; k < nch; ++k) {
-      const float v = ut_s[k * 32 + lane];
+      const float v = __half2float(ut_s[k * 32 + lane]);
       if (v > bu) {
         bu = v;
         bk = k;
@@ -352,14 +355,14 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
       full = !(lb >= J.tau);
       emit(va, ca);
     }
-    if (va && gi == 0) ut_s[(my_e >> 5) * 32 + (my_e & 31)] = -1.0f;   // evaluated
+    if (va && gi == 0) ut_s[(my_e >> 5) * 32 + (my_e & 31)] = __float2half(-1.0f);   // evaluated
     __syncwarp();
 
     // ---- step C: the other lane-chunks whose U reaches LB (all of them if
     // full); LB tightens with every evaluated group
     int n_sel = 0;
     for (int k = 0; k < nch; ++k) {
-      const float v = ut_s[k * 32 + lane];
+      const float v = __half2float(ut_s[k * 32 + lane]);
       const bool s = full ? v >= 0.0f : (v > 0.0f && v >= lb);
       const unsigned bm = __ballot_sync(kFull, s);
       if (s) sel_s[n_sel + __popc(bm & lt_mask)] = uint16_t((k << 5) | lane);
@@ -370,7 +373,8 @@ __global__ void __launch_bounds__(256, 2) bounds_kernel(const __grid_constant__ 
       const int p = g0 + (lane >> 3);
       const bool vc = p < n_sel;
       const int e = vc ? int(sel_s[p]) : 0;
-      if (!full && !__any_sync(kFull, vc && ut_s[(e >> 5) * 32 + (e & 31)] >= lb)) continue;
+      if (!full && !__any_sync(kFull, vc && __half2float(ut_s[(e >> 5) * 32 + (e & 31)]) >= lb))
+        continue;
       const ColEval cc = eval(vc, e);
       lb = fmaxf(lb, warp_max(cc.L));
       emit(vc, cc);

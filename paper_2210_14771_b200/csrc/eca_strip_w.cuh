@@ -19,7 +19,7 @@ namespace eca {
 
 constexpr int kWChunk = 256;       // columns per chunk (32 lanes x kPx)
 constexpr int kWMaxChunks = 8;     // half width <= 2048
-constexpr int kWListCap = 128;     // per-warp survivor list (flushed to FP64 when full)
+constexpr int kWListCap = 64;      // per-warp survivor list (flushed to FP64 when full)
 
 #ifdef ECA_STATS
 // diagnostic counters: [0] half-rows, [1] full halves, [2] chunks, [3] revisited
@@ -34,7 +34,7 @@ __device__ unsigned long long g_warp_stats[8];
 //   list  survivor entries (x | pre << 16), flushed to FP64 when full
 //   ulist their upper bounds (float)
 //   bars  NS mbarriers (16 reserved)
-//   ut    pass-1 upper bound of every lane-chunk      float   [kWMaxChunks][32]
+//   ut    pass-1 upper bound of every lane-chunk      half    [kWMaxChunks][32]
 //   exs   preceding sum before every lane-chunk      uint16  [kWMaxChunks][32]
 //   sel   compacted lane-chunk list (k << 5 | lane)  uint16  [kWMaxChunks * 32]
 struct WarpLayout {
@@ -52,7 +52,7 @@ __host__ __device__ inline WarpLayout warp_layout(int nstage, int rowcap_h, int 
   L.ulist = L.list + kWListCap * 4;
   L.bars = L.ulist + kWListCap * 4;
   L.ut = L.bars + 16 * 8;
-  L.exs = L.ut + kWMaxChunks * 32 * 4;
+  L.exs = L.ut + kWMaxChunks * 32 * 2;
   L.sel = L.exs + kWMaxChunks * 32 * 2;
   L.per_warp = (L.sel + kWMaxChunks * 32 * 2 + 127) & ~size_t(127);
   L.warp0 = o;
