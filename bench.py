@@ -11,7 +11,7 @@ with NCCL.  Rank 0 prints ONE JSON line.
 value : frames/s, whole job, frames already resident in HBM (a 2048-slot pool,
         566 MB of strip rows, so every step reads DRAM, not L2)
 e2e   : frames/s through ContentAreaEngine.run_host from pinned HOST frames:
-        strip-row H2D + fused launch + D2H of the records, every step
+        strip-row H2D + the step's launches + D2H of the records, every step
 --impl reference : the reference algorithm on the host cores (the numpy
         oracle port of /root/reference's eca package; the reference itself is
         pure Python and cannot be shipped to the GPU box).
@@ -243,8 +243,9 @@ def run_ours(args) -> None:
     value = world * BATCH * args.steps / (ms / 1e3)
     ms_step = ms / args.steps
 
-    # kernel-only timing of the dominant kernel of the step (strip scoring),
-    # launched alone on the same stream over the same rotating pool
+    # kernel-only timing of the dominant stage of the step (K1 points:
+    # bounds_kernel + its small rescore_kernel), launched alone on the same
+    # stream over the same rotating pool
     kt0, kt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     kt0.record(stream)
@@ -311,13 +312,15 @@ def run_ours(args) -> None:
                        "parallelism": f"dp{world}" + (" + NCCL all-gather of 40-B records" if world > 1 else "")},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "eca::strip_kernel<3,320,2,0,0> (strip scoring + candidates)",
+                         "kernel": "K1 points stage: eca::bounds_kernel<1> + eca::rescore_kernel "
+                                   "(strip scoring + candidates, 2 launches timed together)",
                          "kernel_share_of_step": round(k_ms / ms_step, 3),
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "kernel_ms": round(k_ms, 5), "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
             "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e_steps,
-                    "path": "ContentAreaEngine.run_host: strip-row H2D (cudaMemcpy2DAsync) + fused launch + record D2H"},
+                    "path": "ContentAreaEngine.run_host: strip-row H2D (cudaMemcpy2DAsync) + "
+                            "bounds/rescore/fit launches + record D2H"},
             "latency_ms": lat,
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * eng.launches_per_run,

@@ -57,14 +57,14 @@ class ContentAreaEngine:
             self.w_dev, self.norm = api._dev_net(variant.net, d)
         self.graph = None
         # Small batches (latency): one fused launch whose last strip CTA per
-        # frame runs the fit.  Large batches (throughput): strip kernel then a
-        # fit kernel (one warp per frame), which keeps the fits off the strip
-        # kernel's critical path.
+        # frame runs the fit.  Large batches (throughput): bound-and-prune
+        # kernel, FP64 rescore of the survivors, then a fit kernel (one warp
+        # per frame), which keeps the FP64 chains off the pixel warps.
         self.fused = batch <= self.FUSED_MAX_BATCH
         if isinstance(variant, api.Learned):
-            self.launches_per_run = 3
+            self.launches_per_run = 3          # CNN, candidate select, fit
         else:
-            self.launches_per_run = 1 if self.fused else 2
+            self.launches_per_run = 1 if self.fused else 3   # bounds, rescore, fit
 
     FUSED_MAX_BATCH = 16
 
