@@ -6,7 +6,10 @@ One step = the handcrafted pipeline (estimate: strip scoring -> candidates ->
 filter -> seeded RANSAC) over one batch of 256 synthetic 1080p frames
 (config C2); for N > 1 (torchrun, one process per GPU) every
 rank runs its own batch and the 40-byte per-frame records are all-gathered
-with NCCL.  Rank 0 prints ONE JSON line.
+with NCCL.  Steps stream: the FP64 rescore + fit of batch i run on a side
+stream under the bound-and-prune kernel of batch i+1 (ContentAreaEngine.
+run_pipelined); the timed region ends after the last batch's fit.  Rank 0
+prints ONE JSON line.
 
 value : frames/s, whole job, frames already resident in HBM (a 2048-slot pool,
         566 MB of strip rows, so every step reads DRAM, not L2)
@@ -211,13 +214,18 @@ def run_ours(args) -> None:
     n_slots = POOL // BATCH
 
     def step(i: int):
-        rec = eng.run(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
+        # streaming throughput mode: bound-and-prune of this batch on the main
+        # stream; FP64 rescore + fit (+ the record all-gather) on the engine's
+        # side stream, overlapping the next step's bound-and-prune
+        rec = eng.run_pipelined(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
         if world > 1:
-            dist.all_gather_into_tensor(gathered, rec)
+            with torch.cuda.stream(eng.side_stream):
+                dist.all_gather_into_tensor(gathered, rec)
 
     # parity spot-check of the benchmarked configuration against pool contents
     for i in range(args.warmup):
         step(i)
+    eng.fence()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -231,6 +239,7 @@ def run_ours(args) -> None:
         t0.record(stream)
         for i in range(args.steps):
             step(args.warmup + i)
+        eng.fence(stream)   # the last step's fit (and gather) are inside the timed region
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -309,7 +318,8 @@ def run_ours(args) -> None:
                        "pool_frames": POOL, "distinct_renders": N_BASE,
                        "l2": f"inputs larger than L2: {POOL}-slot HBM pool rotated "
                              f"({POOL * STRIP_BYTES_PER_FRAME / 1e6:.0f} MB of strip rows > 126 MB L2)",
-                       "parallelism": f"dp{world}" + (" + NCCL all-gather of 40-B records" if world > 1 else "")},
+                       "parallelism": f"dp{world}" + (" + NCCL all-gather of 40-B records" if world > 1 else ""),
+                       "pipelining": "2 streams: rescore+fit of batch i overlap bound-and-prune of batch i+1"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": "K1 points stage: eca::bounds_kernel<1> + eca::rescore_kernel "

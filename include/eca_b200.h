@@ -116,6 +116,20 @@ int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_strid
                            const EcaParams* params, int32_t* out_x, int32_t* out_y,
                            double* out_score, void* workspace, void* stream);
 
+/* The two stages of eca_points_handcrafted (workspace required) as separate
+ * launches, so a host pipeline can run the rescore of batch i on another
+ * stream under the bound-and-prune kernel of batch i+1 (order them with an
+ * event).  eca_bounds_handcrafted writes the workspace (and the candidates of
+ * half rows it resolves itself); eca_rescore_handcrafted completes out_*. */
+int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
+                           int64_t row_stride, const int32_t* strip_rows,
+                           const int32_t* band_rows, int n_strips,
+                           const EcaParams* params, int32_t* out_x, int32_t* out_y,
+                           double* out_score, void* workspace, void* stream);
+int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
+                            const EcaParams* params, int32_t* out_x, int32_t* out_y,
+                            double* out_score, void* workspace, void* stream);
+
 /* Same, plus every column's FP64 score: out_scores[batch][n_strips][width]
  * (StripScoreRow.scores, handcrafted.py:25-31). */
 int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,

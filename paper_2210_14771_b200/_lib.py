@@ -34,6 +34,9 @@ SIGNATURES = {
     "eca_points_workspace_bytes": [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)],
     "eca_points_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
                                _p, _p, _p, _p, _p],
+    "eca_bounds_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
+                               _p, _p, _p, _p, _p],
+    "eca_rescore_handcrafted": [ctypes.c_int, _I32P, ctypes.c_int, _PARAMS, _p, _p, _p, _p, _p],
     "eca_score_rows_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
                                    _p, _p, _p, _p, _p],
     "eca_fit": [_p, _p, _p, ctypes.c_int, ctypes.c_int, _PARAMS, _p, ctypes.c_int, _p, _p],

@@ -172,14 +172,10 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream) {
   ECA_TRACE("bounds kernel: NS %d warps %d smem %zu per_sm %d grid %d\n", NS, warps, smem, per_sm,
             grid);
   kern<<<grid, 32 * warps, smem, stream>>>(PJ);
-  if (cudaGetLastError() != cudaSuccess) return ECA_ERR_CUDA;
-  const int64_t blocks = (n_hr + 15) / 16;   // 4 warps x 4 half rows
-  rescore_kernel<<<unsigned(blocks), 128, 0, stream>>>(PJ);
   return check_launch();
 }
 
-int launch_points(const StripJob& J, void* workspace, cudaStream_t stream) {
-  if (J.batch == 0) return ECA_OK;
+PointsJob points_job(const StripJob& J, void* workspace) {
   const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
   PointsJob PJ;
   PJ.J = J;
@@ -187,11 +183,31 @@ int launch_points(const StripJob& J, void* workspace, cudaStream_t stream) {
   PJ.counts = reinterpret_cast<int32_t*>(
       reinterpret_cast<uint8_t*>(workspace) +
       ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)));
+  return PJ;
+}
+
+int launch_bounds(const StripJob& J, void* workspace, cudaStream_t stream) {
+  if (J.batch == 0) return ECA_OK;
   static const int ns = [] {
     const char* v = std::getenv("ECA_WSTAGES");
     return v ? std::atoi(v) : 1;
   }();
+  const PointsJob PJ = points_job(J, workspace);
   return ns == 2 ? launch_points_t<2>(PJ, stream) : launch_points_t<1>(PJ, stream);
+}
+
+// one warp per CTA (4 half rows): small CTAs slot in beside a running
+// bounds kernel of the next batch when the host pipelines the two
+int launch_rescore(const StripJob& J, void* workspace, cudaStream_t stream) {
+  if (J.batch == 0) return ECA_OK;
+  const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
+  rescore_kernel<<<unsigned((n_hr + 3) / 4), 32, 0, stream>>>(points_job(J, workspace));
+  return check_launch();
+}
+
+int launch_points(const StripJob& J, void* workspace, cudaStream_t stream) {
+  const int rc = launch_bounds(J, workspace, stream);
+  return rc ? rc : launch_rescore(J, workspace, stream);
 }
 
 template <bool kRows, bool kFused>
@@ -254,6 +270,43 @@ extern "C" int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t 
   J.out_score = out_score;
   if (!workspace) return launch_strips<false, false>(J, as_stream(stream));  // single-kernel path
   return launch_points(J, workspace, as_stream(stream));
+}
+
+extern "C" int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
+                                      int64_t row_stride, const int32_t* strip_rows,
+                                      const int32_t* band_rows, int n_strips,
+                                      const EcaParams* params, int32_t* out_x, int32_t* out_y,
+                                      double* out_score, void* workspace, void* stream) {
+  StripJob J;
+  int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
+                             n_strips, params);
+  if (rc) return rc;
+  if (!out_x || !out_y || !out_score || !workspace) return ECA_ERR_ARG;
+  J.out_x = out_x;
+  J.out_y = out_y;
+  J.out_score = out_score;
+  return launch_bounds(J, workspace, as_stream(stream));
+}
+
+extern "C" int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
+                                       const EcaParams* params, int32_t* out_x, int32_t* out_y,
+                                       double* out_score, void* workspace, void* stream) {
+  if (!strip_rows || !params || !out_x || !out_y || !out_score || !workspace || batch < 0)
+    return ECA_ERR_ARG;
+  if (n_strips < 1 || n_strips > ECA_MAX_STRIPS) return ECA_ERR_UNSUPPORTED;
+  StripJob J;
+  std::memset(&J, 0, sizeof(J));
+  J.batch = batch;
+  J.n_strips = n_strips;
+  J.p = *params;
+  for (int k = 0; k < n_strips; ++k) {
+    if (strip_rows[k] < 3 || strip_rows[k] > params->height - 4) return ECA_ERR_ARG;
+    J.rows[k] = int16_t(strip_rows[k]);
+  }
+  J.out_x = out_x;
+  J.out_y = out_y;
+  J.out_score = out_score;
+  return launch_rescore(J, workspace, as_stream(stream));
 }
 
 extern "C" int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,

@@ -56,6 +56,7 @@ class ContentAreaEngine:
             self.probs = torch.empty((batch, s, width - 6), dtype=torch.float32, device=d)
             self.w_dev, self.norm = api._dev_net(variant.net, d)
         self.graph = None
+        self._pipe = None
         # Small batches (latency): one fused launch whose last strip CTA per
         # frame runs the fit.  Large batches (throughput): bound-and-prune
         # kernel, FP64 rescore of the survivors, then a fit kernel (one warp
@@ -120,6 +121,66 @@ class ContentAreaEngine:
             self.n_strips, ctypes.byref(self.params), api._ptr(self.xs), api._ptr(self.ys),
             api._ptr(self.sc), api._ptr(self.workspace), api._stream(self.device))
         _lib.check(rc, "eca_points_handcrafted")
+
+    # ------------------------------------------------------------ pipeline
+    def _pipeline(self):
+        if self._pipe is None:
+            sets = []
+            for _ in range(2):
+                sets.append({"ws": torch.empty_like(self.workspace), "xs": torch.empty_like(self.xs),
+                             "ys": torch.empty_like(self.ys), "sc": torch.empty_like(self.sc),
+                             "rec": torch.empty_like(self.rec), "bounds": torch.cuda.Event(),
+                             "free": torch.cuda.Event()})
+            self._pipe = {"sets": sets, "side": torch.cuda.Stream(self.device), "i": 0, "done": None}
+        return self._pipe
+
+    @property
+    def side_stream(self) -> torch.cuda.Stream:
+        """Stream of the rescore + fit half of run_pipelined()."""
+        return self._pipeline()["side"]
+
+    def run_pipelined(self, frames: torch.Tensor) -> torch.Tensor:
+        """Throughput mode for a stream of batches: the bound-and-prune kernel
+        of this batch runs on the current stream, its FP64 rescore and the fit
+        on a side stream, where they overlap the NEXT call's bound-and-prune.
+        Two buffer sets alternate; the returned (B,5) records are complete once
+        ``fence()`` has made the reading stream wait, and are overwritten two
+        calls later.  Same records as run() (tests/test_gpu_parity.py)."""
+        if isinstance(self.variant, api.Learned) or self.fused:
+            return self.run(frames)
+        f = self._check_frames(frames)
+        if f.device != self.device:
+            raise ValueError(f"frames must live on {self.device}")
+        p = self._pipeline()
+        b = p["sets"][p["i"] & 1]
+        p["i"] += 1
+        lib = _lib.load()
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_event(b["free"])           # the fit two calls ago has read this set
+        s = self.n_strips
+        _lib.check(lib.eca_bounds_handcrafted(
+            ctypes.c_void_p(f.data_ptr()), self.batch, f.stride(0), f.stride(1), self._rows, None, s,
+            ctypes.byref(self.params), api._ptr(b["xs"]), api._ptr(b["ys"]), api._ptr(b["sc"]),
+            api._ptr(b["ws"]), ctypes.c_void_p(cur.cuda_stream)), "eca_bounds_handcrafted")
+        b["bounds"].record(cur)
+        side = p["side"]
+        side.wait_event(b["bounds"])
+        st = ctypes.c_void_p(side.cuda_stream)
+        _lib.check(lib.eca_rescore_handcrafted(
+            self.batch, self._rows, s, ctypes.byref(self.params), api._ptr(b["xs"]), api._ptr(b["ys"]),
+            api._ptr(b["sc"]), api._ptr(b["ws"]), st), "eca_rescore_handcrafted")
+        _lib.check(lib.eca_fit(api._ptr(b["xs"]), api._ptr(b["ys"]), api._ptr(b["sc"]), self.batch, 2 * s,
+                               ctypes.byref(self.params), api._ptr(self.trip), 0, api._ptr(b["rec"]), st),
+                   "eca_fit")
+        b["free"].record(side)
+        p["done"] = b["free"]
+        return b["rec"]
+
+    def fence(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Make ``stream`` (default: current) wait for every run_pipelined() so far."""
+        stream = stream or torch.cuda.current_stream(self.device)
+        if self._pipe is not None and self._pipe["done"] is not None:
+            stream.wait_event(self._pipe["done"])
 
     def run(self, frames: torch.Tensor) -> torch.Tensor:
         """Frames on this GPU -> device records (asynchronous)."""

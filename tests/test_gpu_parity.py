@@ -171,6 +171,58 @@ def test_c2_batch_1080p_vs_oracle():
         assert_fit_equal(got[k], want, k)
 
 
+def test_pipelined_matches_run():
+    """run_pipelined (bounds on the current stream, rescore + fit on a side
+    stream overlapping the next batch) gives run()'s records, batch by batch."""
+    specs = synth.bench_specs(40, 1920, 1080, seed=2024)
+    frames = torch.from_numpy(np.stack([synth.render(s, 30000 + k)
+                                        for k, (_, s) in enumerate(specs)])).cuda()
+    B = 20
+    eng = eb.ContentAreaEngine(1080, 1920, B)
+    assert not eng.fused
+    order = [0, 1, 1, 0, 1, 0, 0]
+    want = {i: eng.run(frames[i * B:(i + 1) * B]).clone() for i in (0, 1)}
+    got = []
+    for i in order:
+        rec = eng.run_pipelined(frames[i * B:(i + 1) * B])
+        if len(got) % 3 == 2:
+            eng.side_stream.synchronize()
+        got.append((i, rec))
+        if len(got) >= 2:   # a record set is reused two calls later: read it now
+            eng.fence()
+            j, r = got[-2]
+            assert torch.equal(r, want[j]), len(got)
+    eng.fence()
+    j, r = got[-1]
+    assert torch.equal(r, want[j])
+
+
+def test_split_stages_match_points():
+    """eca_bounds_handcrafted + eca_rescore_handcrafted == eca_points_handcrafted."""
+    import ctypes
+    from paper_2210_14771_b200 import _lib, api
+    specs = synth.bench_specs(12, 1280, 720, seed=5)
+    frames = torch.from_numpy(np.stack([synth.render(s, 7 + k) for k, (_, s) in enumerate(specs)])).cuda()
+    eng = eb.ContentAreaEngine(720, 1280, len(frames))
+    eng.points(frames)
+    torch.cuda.synchronize()
+    ref = (eng.xs.clone(), eng.ys.clone(), eng.sc.clone())
+    lib = _lib.load()
+    xs, ys, sc = torch.zeros_like(ref[0]), torch.zeros_like(ref[1]), torch.zeros_like(ref[2])
+    st = api._stream(eng.device)
+    _lib.check(lib.eca_bounds_handcrafted(
+        ctypes.c_void_p(frames.data_ptr()), len(frames), frames.stride(0), frames.stride(1), eng._rows,
+        None, eng.n_strips, ctypes.byref(eng.params), api._ptr(xs), api._ptr(ys), api._ptr(sc),
+        api._ptr(eng.workspace), st), "bounds")
+    _lib.check(lib.eca_rescore_handcrafted(
+        len(frames), eng._rows, eng.n_strips, ctypes.byref(eng.params), api._ptr(xs), api._ptr(ys),
+        api._ptr(sc), api._ptr(eng.workspace), st), "rescore")
+    torch.cuda.synchronize()
+    assert torch.equal(xs, ref[0]) and torch.equal(ys, ref[1]) and torch.equal(sc, ref[2])
+    assert lib.eca_rescore_handcrafted(1, eng._rows, eng.n_strips, None, api._ptr(xs), api._ptr(ys),
+                                       api._ptr(sc), api._ptr(eng.workspace), st) == _lib.ECA_ERR_ARG
+
+
 def test_graph_replay_matches_direct():
     frame = synth.c1_frame()
     t = torch.from_numpy(frame).cuda().unsqueeze(0)

@@ -28,8 +28,9 @@ def timeit(fn, n=50):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for i in range(n): fn(i)
+    eng.fence()
     b.record(); torch.cuda.synchronize()
     return a.elapsed_time(b) / n
-for name, fn in [("points(2-stage)", points), ("points(1-kernel)", lambda i: points(i, False)), ("fit", fit), ("fused", fused), ("engine.run", lambda i: eng.run(frames(i)))]:
+for name, fn in [("points(2-stage)", points), ("points(1-kernel)", lambda i: points(i, False)), ("fit", fit), ("fused", fused), ("engine.run", lambda i: eng.run(frames(i))), ("run_pipelined", lambda i: eng.run_pipelined(frames(i)))]:
     ms = timeit(fn)
     print(f"{name:18s} B={B} {ms*1e3:9.1f} us  {ms*1e3/B:7.3f} us/frame  {70778880*B/256/(ms/1e3)/1e9:8.1f} GB/s(strip bytes)", flush=True)
