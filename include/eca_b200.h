@@ -103,7 +103,9 @@ int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_stride,
                   int64_t host_row_stride, const int32_t* first_rows, int n_bands,
                   int rows_per_band, int width, uint8_t* dev, void* stream);
 
-/* Bytes of device workspace eca_points_handcrafted needs for (batch, n_strips). */
+/* Bytes of device workspace eca_points_handcrafted needs for (batch, n_strips).
+ * Zero it once before first use (the kernels hand out work through a ticket
+ * counter at its start and leave it zeroed); one launch at a time per workspace. */
 int eca_points_workspace_bytes(int batch, int n_strips, int64_t* out_bytes);
 
 /* score_frame_strips + select_candidates_batch, handcrafted variant

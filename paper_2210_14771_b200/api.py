@@ -252,13 +252,14 @@ _WORKSPACES: dict = {}
 
 
 def points_workspace(batch: int, n_strips: int, device) -> torch.Tensor:
-    """Device scratch for eca_points_handcrafted (survivor slots), cached per device."""
+    """Device scratch for eca_points_handcrafted (tickets + survivor slots),
+    zero-initialised once (the kernels leave the tickets zeroed), cached per device."""
     n = ctypes.c_int64()
     _lib.check(_lib.load().eca_points_workspace_bytes(batch, n_strips, ctypes.byref(n)),
                "eca_points_workspace_bytes")
     t = _WORKSPACES.get(str(device))
     if t is None or t.numel() < n.value:
-        t = torch.empty(max(n.value, 1 << 20), dtype=torch.uint8, device=device)
+        t = torch.zeros(max(n.value, 1 << 20), dtype=torch.uint8, device=device)
         _WORKSPACES[str(device)] = t
     return t
 

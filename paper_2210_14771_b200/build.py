@@ -57,7 +57,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     log = []
     for src in sources():
         obj = OBJ / (src.stem + ".o")
-        cmd = [nvcc(), *ARCH, *NVFLAGS, "-c", str(src), "-o", str(obj)]
+        # ECA_NVCC_DEFINES="-DX=1 ...": tuning experiments only
+        extra = os.environ.get("ECA_NVCC_DEFINES", "").split()
+        cmd = [nvcc(), *ARCH, *NVFLAGS, *extra, "-c", str(src), "-o", str(obj)]
         if src.suffix == ".cpp":
             cmd = ["g++", "-O2", "-std=c++17", "-fPIC",
                    "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]

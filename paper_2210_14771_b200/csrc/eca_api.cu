@@ -105,9 +105,10 @@ int launch_strips_t(const StripJob& J, cudaStream_t stream) {
 }
 
 // ---- v6 points pipeline: bounds_kernel (warp per half row) + rescore_kernel
+// workspace: [0, 256) item tickets (zero between launches) | slots | counts
 int64_t points_workspace(int batch, int n_strips) {
   const int64_t n_hr = int64_t(batch) * n_strips * 2;
-  return ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)) + n_hr * 4;
+  return 256 + ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)) + n_hr * 4;
 }
 
 template <int NS>
@@ -126,32 +127,23 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream) {
   std::call_once(once, [kern] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
-  // CTA shape: the smallest CTA (>= 2 warps) whose resident warps per SM
-  // reach 90% of the best shape's.  Small independent CTAs measured faster
-  // than large ones at equal occupancy (B200, 1080p: 3 warps x 6 CTAs
-  // 51 us vs 5 x 4 57 us).
-  int occ[9] = {0};
-  int best_occ = 0;
+  // CTA shape: the smallest CTA reaching the most resident warps per SM.
+  // Items are handed out dynamically, so independent small CTAs cost
+  // nothing; more resident warps shorten the end-of-kernel tail (B200,
+  // 1080p B=256: 4 warps x 5 CTAs 50 us, 2 x 9 52 us, 8 x 2 56 us).
+  int warps = 0, per_sm = 0;
   for (int w = 1; w <= 8; ++w) {
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * w,
                                                       warp_layout(NS, J.rowcap, w).total) !=
         cudaSuccess)
       return ECA_ERR_CUDA;
-    occ[w] = b;
-    if (b * w > best_occ) best_occ = b * w;
     ECA_TRACE("bounds kernel: %d warps/CTA -> %d CTAs/SM (smem %zu)\n", w, b,
               warp_layout(NS, J.rowcap, w).total);
-  }
-  int warps = 0, per_sm = 0;
-  for (int w = 2; w <= 8 && !warps; ++w)
-    if (10 * occ[w] * w >= 9 * best_occ) {
+    if (b * w > per_sm * warps) {
       warps = w;
-      per_sm = occ[w];
+      per_sm = b;
     }
-  if (!warps) {
-    warps = 1;
-    per_sm = occ[1];
   }
   static const int force_w = [] {   // tuning hook: ECA_BWARPS=<warps per CTA>
     const char* v = std::getenv("ECA_BWARPS");
@@ -179,10 +171,11 @@ PointsJob points_job(const StripJob& J, void* workspace) {
   const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
   PointsJob PJ;
   PJ.J = J;
-  PJ.slots = reinterpret_cast<SurvSlot*>(workspace);
+  uint8_t* w = reinterpret_cast<uint8_t*>(workspace);
+  PJ.ticket = reinterpret_cast<int32_t*>(w);
+  PJ.slots = reinterpret_cast<SurvSlot*>(w + 256);
   PJ.counts = reinterpret_cast<int32_t*>(
-      reinterpret_cast<uint8_t*>(workspace) +
-      ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)));
+      w + 256 + ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)));
   return PJ;
 }
 

@@ -74,6 +74,12 @@ ECA_DEV float warp_max(float v) {
   return v;
 }
 
+// max over the warp of a NON-NEGATIVE float: one REDUX on the bit patterns
+// (IEEE order of non-negative floats is their unsigned-integer order)
+ECA_DEV float warp_max_nonneg(float v) {
+  return __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(v)));
+}
+
 ECA_DEV double warp_sum(double v) {
 #pragma unroll
   for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(kFull, v, d);

@@ -40,6 +40,7 @@
 namespace eca {
 
 constexpr int kSlots = 8;
+constexpr float kEarlyD = 0.1f;   // D_up(carry) level that triggers the early LB (gray ~37)
 
 // one survivor: column, preceding sum and the 9 neighbourhood sums (rows h-1..h+1)
 struct SurvSlot {
@@ -53,6 +54,7 @@ struct PointsJob {
   StripJob J;          // geometry, params, candidate outputs
   SurvSlot* slots;     // [n_halfrows][kSlots]
   int32_t* counts;     // [n_halfrows]: survivors, or -1 when resolved in bounds_kernel
+  int32_t* ticket;     // [0] next item, [1] warps done; zero between launches
 };
 
 // RGB sums of the 10 pixels x0-1 .. x0+8 of one staged row; B = smem byte of
@@ -90,8 +92,16 @@ struct ColEval {
 };
 
 template <int NS>
-// 96 registers: 5 warps per SM sub-partition (112 would allow only 4)
-__global__ void __maxnreg__(96) bounds_kernel(const __grid_constant__ PointsJob PJ) {
+#ifndef ECA_BOUNDS_MAXREG   // 96: 5 warps per SM sub-partition (120 would allow 4)
+#define ECA_BOUNDS_MAXREG 96
+#endif
+#ifndef ECA_LOAD_ONLY
+#define ECA_LOAD_ONLY 0
+#endif
+#ifndef ECA_EARLY_EXIT
+#define ECA_EARLY_EXIT 1
+#endif
+__global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_constant__ PointsJob PJ) {
   const StripJob& J = PJ.J;
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -120,14 +130,18 @@ __global__ void __maxnreg__(96) bounds_kernel(const __grid_constant__ PointsJob 
     if (threadIdx.x == 0)
       atab[kABins] = make_float2(angle_term(3.14159265358979f, asc) * lo_f, 1.0f);
   }
-  const int gw = blockIdx.x * warps + wib, nw = gridDim.x * warps;
+  const int nw = gridDim.x * warps;
+  // items are handed out dynamically (item costs vary with the early exit);
+  // qitem[s] = item in flight in stage s
+  int* qitem = reinterpret_cast<int*>(bars + 8);
   uint64_t pol = 0;
   if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
     pol = l2_evict_first();
     for (int s = 0; s < NS; ++s) {
-      const int it = gw + s * nw;
+      const int it = atomicAdd(PJ.ticket, 1);
+      qitem[s] = it;
       if (it < n_items) issue_half(J, it, mine + s * WL.stage, &bars[s], pol, split);
     }
   }
@@ -144,7 +158,9 @@ __global__ void __maxnreg__(96) bounds_kernel(const __grid_constant__ PointsJob 
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int item = gw; item < n_items; item += nw) {
+  for (;;) {
+    const int item = qitem[stage];   // tickets rise: the first past the end ends the warp
+    if (item >= n_items) break;
     const int half = item & 1;
     const int fs = item >> 1;
     const int frame = fs / S;
@@ -173,56 +189,9 @@ __global__ void __maxnreg__(96) bounds_kernel(const __grid_constant__ PointsJob 
     const bool al = (((rb[0] + 3 * xa0) | (rb[1] + 3 * xa0) | (rb[2] + 3 * xa0)) & 7) == 0;
     const int nch = (hw + kWChunk - 1) / kWChunk;
     mbar_wait(&bars[stage], phase);
-
-    // ---- pass 1: U of every lane-chunk
-    int carry = 0;
-#pragma unroll 1
-    for (int k = 0; k < nch; ++k) {
-      const int xa = xa_of(k, lane);
-      int s0[10], s1[10], s2[10];
-      load10(st, rb[0] + 3 * xa, al, s0);
-      load10(st, rb[1] + 3 * xa, al, s1);
-      load10(st, rb[2] + 3 * xa, al, s2);
-      int c[10], e[10];
-#pragma unroll
-      for (int i = 0; i < 10; ++i) {
-        c[i] = s0[i] + 2 * s1[i] + s2[i];
-        e[i] = s2[i] - s0[i];
-      }
-      int tmax = 0, qmax = 0;
-#pragma unroll
-      for (int i = 1; i <= kPx; ++i) tmax = max(tmax, s1[i]);
-      if (k == 0 || k == nch - 1) {   // border / tail chunk: only scoreable columns
-#pragma unroll
-        for (int i = 0; i < kPx; ++i) {
-          const int gx3 = c[i + 2] - c[i], gy3 = e[i] + 2 * e[i + 1] + e[i + 2];
-          const int q = gx3 * gx3 + gy3 * gy3;
-          const bool in = unsigned(xa + i - slo) <= unsigned(shi - slo);
-          qmax = max(qmax, in ? q : 0);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < kPx; ++i) {
-          const int gx3 = c[i + 2] - c[i], gy3 = e[i] + 2 * e[i + 1] + e[i + 2];
-          qmax = max(qmax, gx3 * gx3 + gy3 * gy3);
-        }
-      }
-      int sc = tmax;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int v = __shfl_up_sync(kFull, sc, d);
-        if (lane >= d) sc = max(sc, v);
-      }
-      int ex = __shfl_up_sync(kFull, sc, 1);
-      ex = max(lane == 0 ? 0 : ex, carry);
-      carry = max(carry, __shfl_sync(kFull, sc, 31));
-      float u = 0.0f;
-      if (qmax > 0)
-        u = fminf(t_term(qmax, tk) * hi_f, 1.0f) * fminf(d_term(ex, tk) * hi_f, 1.0f);
-      ut_s[k * 32 + lane] = __float2half_ru(u);
-      ex_s[k * 32 + lane] = uint16_t(ex);
-    }
-    __syncwarp();
+#if ECA_LOAD_ONLY   // diagnostic: the TMA ring alone
+    if (lane == 0) PJ.counts[item] = 0;
+#else
 
     // ---- one lane per column of lane-chunk entry e = (k << 5 | l)
     auto eval = [&](bool valid, int e) -> ColEval {
@@ -325,10 +294,13 @@ __global__ void __maxnreg__(96) bounds_kernel(const __grid_constant__ PointsJob 
       __syncwarp();
     };
 
-    // ---- step A: the (up to) 4 lane-chunks of highest U, from distinct lanes
-    float bu = -1.0f;
+    // ---- steps A + B over the first nk chunks
+    bool ab_done = false;
+    auto step_ab = [&](int nk) {
+    // A: the (up to) 4 lane-chunks of highest U, from distinct lanes
+    float bu = 0.0f;   // lane-chunks with U == 0 (or marked -1) never qualify
     int bk = 0;
-    for (int k = 0; k < nch; ++k) {
+    for (int k = 0; k < nk; ++k) {
       const float v = __half2float(ut_s[k * 32 + lane]);
       if (v > bu) {
         bu = v;
@@ -339,29 +311,98 @@ __global__ void __maxnreg__(96) bounds_kernel(const __grid_constant__ PointsJob 
     int n_a = 0;
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-      const float m = warp_max(bu);
+      const float m = warp_max_nonneg(bu);
       if (!(m > 0.0f)) break;
       const int wl = __ffs(__ballot_sync(kFull, bu == m)) - 1;
       const int wk = __shfl_sync(kFull, bk, wl);
       if ((lane >> 3) == g) my_e = (wk << 5) | wl;
-      if (lane == wl) bu = -1.0f;
+      if (lane == wl) bu = 0.0f;
       n_a = g + 1;
     }
-    // ---- step B: evaluate them -> LB, then their survivors
+    // B: evaluate them -> LB, then their survivors
     const bool va = (lane >> 3) < n_a;
     {
       const ColEval ca = eval(va, my_e);
-      lb = warp_max(ca.L);
+      lb = warp_max_nonneg(ca.L);
       full = !(lb >= J.tau);
       emit(va, ca);
     }
     if (va && gi == 0) ut_s[(my_e >> 5) * 32 + (my_e & 31)] = __float2half(-1.0f);   // evaluated
     __syncwarp();
+    ab_done = true;
+    };
+
+    // ---- pass 1: U of every lane-chunk (stops early, see below)
+    int carry = 0;
+    int nch_eff = nch;
+#pragma unroll 1
+    for (int k = 0; k < nch; ++k) {
+      const int xa = xa_of(k, lane);
+      int s0[10], s1[10], s2[10];
+      load10(st, rb[0] + 3 * xa, al, s0);
+      load10(st, rb[1] + 3 * xa, al, s1);
+      load10(st, rb[2] + 3 * xa, al, s2);
+      int c[10], e[10];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) {
+        c[i] = s0[i] + 2 * s1[i] + s2[i];
+        e[i] = s2[i] - s0[i];
+      }
+      int tmax = 0, qmax = 0;
+#pragma unroll
+      for (int i = 1; i <= kPx; ++i) tmax = max(tmax, s1[i]);
+      if (k == 0 || k == nch - 1) {   // border / tail chunk: only scoreable columns
+#pragma unroll
+        for (int i = 0; i < kPx; ++i) {
+          const int gx3 = c[i + 2] - c[i], gy3 = e[i] + 2 * e[i + 1] + e[i + 2];
+          const int q = gx3 * gx3 + gy3 * gy3;
+          const bool in = unsigned(xa + i - slo) <= unsigned(shi - slo);
+          qmax = max(qmax, in ? q : 0);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kPx; ++i) {
+          const int gx3 = c[i + 2] - c[i], gy3 = e[i] + 2 * e[i + 1] + e[i + 2];
+          qmax = max(qmax, gx3 * gx3 + gy3 * gy3);
+        }
+      }
+      int sc = tmax;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(kFull, sc, d);
+        if (lane >= d) sc = max(sc, v);
+      }
+      int ex = __shfl_up_sync(kFull, sc, 1);
+      ex = max(lane == 0 ? 0 : ex, carry);
+      carry = max(carry, __shfl_sync(kFull, sc, 31));
+      float u = 0.0f;
+      if (qmax > 0)
+        u = fminf(t_term(qmax, tk) * hi_f, 1.0f) * fminf(d_term(ex, tk) * hi_f, 1.0f);
+      ut_s[k * 32 + lane] = __float2half_ru(u);
+      ex_s[k * 32 + lane] = uint16_t(ex);
+      // every later column has preceding sum >= carry, so its score is below
+      // D_up(carry) (T, A <= 1).  Once that is small, get LB from the chunks
+      // so far and stop the scan if no later column can reach it.  (Steps A+B
+      // have this one call site: the last chunk always triggers them.)
+      if (!ab_done) {
+        const bool last = k + 1 == nch;
+        const float dc = last ? 0.0f : d_term(carry, tk) * hi_f;
+        if (last || (ECA_EARLY_EXIT && dc < kEarlyD)) {
+          __syncwarp();
+          step_ab(k + 1);
+          if (!last && lb > dc) {
+            nch_eff = k + 1;
+            break;
+          }
+        }
+      }
+    }
+    __syncwarp();
 
     // ---- step C: the other lane-chunks whose U reaches LB (all of them if
     // full); LB tightens with every evaluated group
     int n_sel = 0;
-    for (int k = 0; k < nch; ++k) {
+    for (int k = 0; k < nch_eff; ++k) {
       const float v = __half2float(ut_s[k * 32 + lane]);
       const bool s = full ? v >= 0.0f : (v > 0.0f && v >= lb);
       const unsigned bm = __ballot_sync(kFull, s);
@@ -376,7 +417,7 @@ __global__ void __maxnreg__(96) bounds_kernel(const __grid_constant__ PointsJob 
       if (!full && !__any_sync(kFull, vc && __half2float(ut_s[(e >> 5) * 32 + (e & 31)]) >= lb))
         continue;
       const ColEval cc = eval(vc, e);
-      lb = fmaxf(lb, warp_max(cc.L));
+      lb = fmaxf(lb, warp_max_nonneg(cc.L));
       emit(vc, cc);
     }
     if (lb >= J.tau) compact(lb);   // final LB: full rows keep every non-flat column
@@ -411,15 +452,25 @@ __global__ void __maxnreg__(96) bounds_kernel(const __grid_constant__ PointsJob 
         PJ.counts[hrow] = -1;
       }
     }
+#endif
     __syncwarp();
     if (lane == 0) {
-      const int nxt = item + NS * nw;
+      // the ticket is taken only now: a warp never holds work it cannot start
+      // (prefetching it measured 30% slower from the end-of-kernel imbalance)
+      const int nxt = atomicAdd(PJ.ticket, 1);
+      qitem[stage] = nxt;
       if (nxt < n_items) issue_half(J, nxt, st, &bars[stage], pol, split);
     }
+    __syncwarp();
     if (++stage == NS) {
       stage = 0;
       phase ^= 1u;
     }
+  }
+  // the last warp out re-arms the tickets for the next launch on this workspace
+  if (lane == 0 && atomicAdd(PJ.ticket + 1, 1) == nw - 1) {
+    PJ.ticket[0] = 0;
+    PJ.ticket[1] = 0;
   }
 }
 

@@ -50,7 +50,7 @@ class ContentAreaEngine:
         nws = ctypes.c_int64()
         _lib.check(_lib.load().eca_points_workspace_bytes(batch, s, ctypes.byref(nws)),
                    "eca_points_workspace_bytes")
-        self.workspace = torch.empty(max(nws.value, 256), dtype=torch.uint8, device=d)
+        self.workspace = torch.zeros(max(nws.value, 256), dtype=torch.uint8, device=d)
         self.rec_host = torch.empty((batch, 5), dtype=torch.float64, pin_memory=True)
         if isinstance(variant, api.Learned):
             self.probs = torch.empty((batch, s, width - 6), dtype=torch.float32, device=d)
@@ -127,7 +127,7 @@ class ContentAreaEngine:
         if self._pipe is None:
             sets = []
             for _ in range(2):
-                sets.append({"ws": torch.empty_like(self.workspace), "xs": torch.empty_like(self.xs),
+                sets.append({"ws": torch.zeros_like(self.workspace), "xs": torch.empty_like(self.xs),
                              "ys": torch.empty_like(self.ys), "sc": torch.empty_like(self.sc),
                              "rec": torch.empty_like(self.rec), "bounds": torch.cuda.Event(),
                              "free": torch.cuda.Event()})
