@@ -123,11 +123,15 @@ int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_strid
  * stream under the bound-and-prune kernel of batch i+1 (order them with an
  * event).  eca_bounds_handcrafted writes the workspace (and the candidates of
  * half rows it resolves itself); eca_rescore_handcrafted completes out_*. */
+#define ECA_BOUNDS_OVERLAP_PREVIOUS 1  /* flags: programmatic dependent launch - the
+   grid may start while the previous kernel in `stream` drains; only when this
+   call neither reads what that kernel writes nor writes what it reads (e.g. the
+   previous batch's eca_bounds_handcrafted on another workspace/output set) */
 int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                            int64_t row_stride, const int32_t* strip_rows,
                            const int32_t* band_rows, int n_strips,
                            const EcaParams* params, int32_t* out_x, int32_t* out_y,
-                           double* out_score, void* workspace, void* stream);
+                           double* out_score, void* workspace, int flags, void* stream);
 int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
                             const EcaParams* params, int32_t* out_x, int32_t* out_y,
                             double* out_score, void* workspace, void* stream);

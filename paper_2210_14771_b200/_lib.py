@@ -19,6 +19,7 @@ ECA_OK, ECA_ERR_ARG, ECA_ERR_CUDA, ECA_ERR_UNSUPPORTED = 0, -1, -2, -3
 ACCEPTED, NO_CANDIDATES, LOW_SCORE, GEOMETRY_GATE = 0, 1, 2, 3
 MAX_STRIPS, MAX_WIDTH, MAX_ATTEMPTS = 128, 4096, 8192
 NET_FLOATS = 6209
+BOUNDS_OVERLAP_PREVIOUS = 1
 
 _p = ctypes.c_void_p
 _i32, _i64, _u64, _f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
@@ -35,7 +36,7 @@ SIGNATURES = {
     "eca_points_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
                                _p, _p, _p, _p, _p],
     "eca_bounds_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
-                               _p, _p, _p, _p, _p],
+                               _p, _p, _p, _p, ctypes.c_int, _p],
     "eca_rescore_handcrafted": [ctypes.c_int, _I32P, ctypes.c_int, _PARAMS, _p, _p, _p, _p, _p],
     "eca_score_rows_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
                                    _p, _p, _p, _p, _p],

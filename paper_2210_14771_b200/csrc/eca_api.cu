@@ -112,7 +112,7 @@ int64_t points_workspace(int batch, int n_strips) {
 }
 
 template <int NS>
-int launch_points_t(PointsJob PJ, cudaStream_t stream) {
+int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap) {
   auto kern = bounds_kernel<NS>;
   StripJob& J = PJ.J;
   const int W = J.p.width;
@@ -163,7 +163,20 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream) {
   const int grid = int(need < int64_t(sm_count()) * per_sm ? need : int64_t(sm_count()) * per_sm);
   ECA_TRACE("bounds kernel: NS %d warps %d smem %zu per_sm %d grid %d\n", NS, warps, smem, per_sm,
             grid);
-  kern<<<grid, 32 * warps, smem, stream>>>(PJ);
+  // overlap: programmatic dependent launch, so this grid's CTAs fill SMs as
+  // the previous kernel in the stream drains (bounds_kernel triggers its
+  // dependents at entry and reads nothing the previous kernel writes)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(32 * warps));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = overlap ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, kern, PJ) != cudaSuccess) return ECA_ERR_CUDA;
   return check_launch();
 }
 
@@ -179,14 +192,14 @@ PointsJob points_job(const StripJob& J, void* workspace) {
   return PJ;
 }
 
-int launch_bounds(const StripJob& J, void* workspace, cudaStream_t stream) {
+int launch_bounds(const StripJob& J, void* workspace, cudaStream_t stream, bool overlap = false) {
   if (J.batch == 0) return ECA_OK;
   static const int ns = [] {
     const char* v = std::getenv("ECA_WSTAGES");
     return v ? std::atoi(v) : 1;
   }();
   const PointsJob PJ = points_job(J, workspace);
-  return ns == 2 ? launch_points_t<2>(PJ, stream) : launch_points_t<1>(PJ, stream);
+  return ns == 2 ? launch_points_t<2>(PJ, stream, overlap) : launch_points_t<1>(PJ, stream, overlap);
 }
 
 // one warp per CTA (4 half rows): small CTAs slot in beside a running
@@ -269,7 +282,9 @@ extern "C" int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t 
                                       int64_t row_stride, const int32_t* strip_rows,
                                       const int32_t* band_rows, int n_strips,
                                       const EcaParams* params, int32_t* out_x, int32_t* out_y,
-                                      double* out_score, void* workspace, void* stream) {
+                                      double* out_score, void* workspace, int flags,
+                                      void* stream) {
+  if (flags & ~ECA_BOUNDS_OVERLAP_PREVIOUS) return ECA_ERR_ARG;
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
                              n_strips, params);
@@ -278,7 +293,7 @@ extern "C" int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t 
   J.out_x = out_x;
   J.out_y = out_y;
   J.out_score = out_score;
-  return launch_bounds(J, workspace, as_stream(stream));
+  return launch_bounds(J, workspace, as_stream(stream), (flags & ECA_BOUNDS_OVERLAP_PREVIOUS) != 0);
 }
 
 extern "C" int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
@@ -388,5 +403,11 @@ extern "C" int eca_debug_strip_stats(unsigned long long* out, int reset) {
     cudaMemcpyToSymbol(g_warp_stats, z, sizeof(z));
   }
   return ECA_OK;
+}
+#endif
+
+#ifdef ECA_WARP_TIMES
+extern "C" int eca_debug_warp_times(uint64_t* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_warp_times, sizeof(uint64_t) * 3 * n) == cudaSuccess ? 0 : -2;
 }
 #endif

@@ -103,6 +103,9 @@ template <int NS>
 #endif
 __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_constant__ PointsJob PJ) {
   const StripJob& J = PJ.J;
+  // a dependent launch (the next batch, ECA_BOUNDS_OVERLAP_PREVIOUS) may start
+  // filling SMs as soon as this grid's CTAs drain
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int warps = blockDim.x >> 5;
@@ -399,12 +402,35 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     }
     __syncwarp();
 
-    // ---- step C: the other lane-chunks whose U reaches LB (all of them if
-    // full); LB tightens with every evaluated group
+    // ---- step C: the other lane-chunks whose U reaches LB (if full: every
+    // one with U > 0 or a non-flat scoreable column); LB tightens with every
+    // evaluated group
     int n_sel = 0;
     for (int k = 0; k < nch_eff; ++k) {
       const float v = __half2float(ut_s[k * 32 + lane]);
-      const bool s = full ? v >= 0.0f : (v > 0.0f && v >= lb);
+      bool s;
+      if (full) {
+        // flat column: identical left/right sums per row and identical top and
+        // bottom rows (score exactly 0); lane-chunks of only such columns and
+        // U == 0 cannot hold the argmax.  Flat rows (black borders) would
+        // otherwise evaluate every column.
+        s = v > 0.0f;
+        if (v == 0.0f) {   // v < 0: evaluated in step B
+          const int xa = xa_of(k, lane);
+          int s0[10], s1[10], s2[10];
+          load10(st, rb[0] + 3 * xa, al, s0);
+          load10(st, rb[1] + 3 * xa, al, s1);
+          load10(st, rb[2] + 3 * xa, al, s2);
+#pragma unroll
+          for (int i = 0; i < kPx; ++i) {
+            const bool flat = s0[i] == s0[i + 2] && s1[i] == s1[i + 2] && s0[i] == s2[i] &&
+                              s0[i + 1] == s2[i + 1] && s0[i + 2] == s2[i + 2];
+            s |= !flat && unsigned(xa + i - slo) <= unsigned(shi - slo);
+          }
+        }
+      } else {
+        s = v > 0.0f && v >= lb;
+      }
       const unsigned bm = __ballot_sync(kFull, s);
       if (s) sel_s[n_sel + __popc(bm & lt_mask)] = uint16_t((k << 5) | lane);
       n_sel += __popc(bm);

@@ -57,6 +57,9 @@ class ContentAreaEngine:
             self.w_dev, self.norm = api._dev_net(variant.net, d)
         self.graph = None
         self._pipe = None
+        # consecutive run_pipelined() bounds launches touch different buffer
+        # sets: let each start while the previous one drains
+        self.pipeline_flags = _lib.BOUNDS_OVERLAP_PREVIOUS
         # Small batches (latency): one fused launch whose last strip CTA per
         # frame runs the fit.  Large batches (throughput): bound-and-prune
         # kernel, FP64 rescore of the survivors, then a fit kernel (one warp
@@ -161,7 +164,8 @@ class ContentAreaEngine:
         _lib.check(lib.eca_bounds_handcrafted(
             ctypes.c_void_p(f.data_ptr()), self.batch, f.stride(0), f.stride(1), self._rows, None, s,
             ctypes.byref(self.params), api._ptr(b["xs"]), api._ptr(b["ys"]), api._ptr(b["sc"]),
-            api._ptr(b["ws"]), ctypes.c_void_p(cur.cuda_stream)), "eca_bounds_handcrafted")
+            api._ptr(b["ws"]), self.pipeline_flags, ctypes.c_void_p(cur.cuda_stream)),
+            "eca_bounds_handcrafted")
         b["bounds"].record(cur)
         side = p["side"]
         side.wait_event(b["bounds"])

@@ -213,7 +213,7 @@ def test_split_stages_match_points():
     _lib.check(lib.eca_bounds_handcrafted(
         ctypes.c_void_p(frames.data_ptr()), len(frames), frames.stride(0), frames.stride(1), eng._rows,
         None, eng.n_strips, ctypes.byref(eng.params), api._ptr(xs), api._ptr(ys), api._ptr(sc),
-        api._ptr(eng.workspace), st), "bounds")
+        api._ptr(eng.workspace), 0, st), "bounds")
     _lib.check(lib.eca_rescore_handcrafted(
         len(frames), eng._rows, eng.n_strips, ctypes.byref(eng.params), api._ptr(xs), api._ptr(ys),
         api._ptr(sc), api._ptr(eng.workspace), st), "rescore")
@@ -221,6 +221,10 @@ def test_split_stages_match_points():
     assert torch.equal(xs, ref[0]) and torch.equal(ys, ref[1]) and torch.equal(sc, ref[2])
     assert lib.eca_rescore_handcrafted(1, eng._rows, eng.n_strips, None, api._ptr(xs), api._ptr(ys),
                                        api._ptr(sc), api._ptr(eng.workspace), st) == _lib.ECA_ERR_ARG
+    assert lib.eca_bounds_handcrafted(
+        ctypes.c_void_p(frames.data_ptr()), len(frames), frames.stride(0), frames.stride(1), eng._rows,
+        None, eng.n_strips, ctypes.byref(eng.params), api._ptr(xs), api._ptr(ys), api._ptr(sc),
+        api._ptr(eng.workspace), 2, st) == _lib.ECA_ERR_ARG
 
 
 def test_graph_replay_matches_direct():
