@@ -50,6 +50,10 @@ struct SurvSlot {
 };
 static_assert(sizeof(SurvSlot) == 24, "slot layout");
 
+#ifdef ECA_WARP_TIMES   // diagnostic builds: per-warp timeline (tools/warp_times.py)
+__device__ uint64_t g_warp_times[3 * 8192];
+#endif
+
 struct PointsJob {
   StripJob J;          // geometry, params, candidate outputs
   SurvSlot* slots;     // [n_halfrows][kSlots]
@@ -149,6 +153,13 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     }
   }
   __syncthreads();
+#ifdef ECA_WARP_TIMES
+  if (lane == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_warp_times[3 * (blockIdx.x * warps + wib)] = t;
+  }
+#endif
 
   const double log2e = 1.4426950408889634;
   const TermK tk{float(-2.0 * log2e / (3.0 * J.p.gradient_threshold)),
@@ -164,6 +175,11 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
   for (;;) {
     const int item = qitem[stage];   // tickets rise: the first past the end ends the warp
     if (item >= n_items) break;
+#ifdef ECA_WARP_TIMES
+    uint64_t t_item;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_item));
+    int dbg_groups = 0;
+#endif
     const int half = item & 1;
     const int fs = item >> 1;
     const int frame = fs / S;
@@ -443,6 +459,9 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
       if (!full && !__any_sync(kFull, vc && __half2float(ut_s[(e >> 5) * 32 + (e & 31)]) >= lb))
         continue;
       const ColEval cc = eval(vc, e);
+#ifdef ECA_WARP_TIMES
+      ++dbg_groups;
+#endif
       lb = fmaxf(lb, warp_max_nonneg(cc.L));
       emit(vc, cc);
     }
@@ -479,6 +498,16 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
       }
     }
 #endif
+#ifdef ECA_WARP_TIMES
+    if (lane == 0) {   // slowest item: (duration/32ns, full, step-C groups, item)
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      const uint64_t rec = (((t - t_item) / 32) << 40) | (uint64_t(full) << 39) |
+                           (uint64_t(min(dbg_groups, 127)) << 32) | uint64_t(item);
+      const int gw = blockIdx.x * warps + wib;
+      if (rec > g_warp_times[3 * gw + 2]) g_warp_times[3 * gw + 2] = rec;
+    }
+#endif
     __syncwarp();
     if (lane == 0) {
       // the ticket is taken only now: a warp never holds work it cannot start
@@ -493,6 +522,13 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
       phase ^= 1u;
     }
   }
+#ifdef ECA_WARP_TIMES
+  if (lane == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_warp_times[3 * (blockIdx.x * warps + wib) + 1] = t;
+  }
+#endif
   // the last warp out re-arms the tickets for the next launch on this workspace
   if (lane == 0 && atomicAdd(PJ.ticket + 1, 1) == nw - 1) {
     PJ.ticket[0] = 0;

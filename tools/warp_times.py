@@ -1,4 +1,6 @@
-"""Per-warp timeline of one bounds_kernel launch (diagnostic build with -DECA_WARP_TIMES)."""
+"""Per-warp timeline of one bounds_kernel launch.  Needs a diagnostic build:
+    ECA_NVCC_DEFINES=-DECA_WARP_TIMES python -m paper_2210_14771_b200.build --force
+"""
 import sys, ctypes, numpy as np, torch
 sys.path.insert(0, '.')
 import paper_2210_14771_b200 as eb
