@@ -127,6 +127,9 @@ int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_strid
    grid may start while the previous kernel in `stream` drains; only when this
    call neither reads what that kernel writes nor writes what it reads (e.g. the
    previous batch's eca_bounds_handcrafted on another workspace/output set) */
+#define ECA_BOUNDS_SHARE_SMS 2         /* flags: leave one CTA slot per SM free for
+   kernels running concurrently on other streams (e.g. the previous batch's
+   eca_rescore_handcrafted + eca_fit) */
 int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                            int64_t row_stride, const int32_t* strip_rows,
                            const int32_t* band_rows, int n_strips,

@@ -112,7 +112,7 @@ int64_t points_workspace(int batch, int n_strips) {
 }
 
 template <int NS>
-int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap) {
+int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share) {
   auto kern = bounds_kernel<NS>;
   StripJob& J = PJ.J;
   const int W = J.p.width;
@@ -156,6 +156,15 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap) {
         cudaSuccess)
       return ECA_ERR_CUDA;
   }
+  static const int cap_ctas = [] {   // tuning hook: ECA_BCTAS=<max CTAs per SM>
+    const char* v = std::getenv("ECA_BCTAS");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (cap_ctas > 0 && per_sm > cap_ctas) per_sm = cap_ctas;
+  // share: one CTA slot per SM stays free for kernels of other streams (the
+  // pipelined rescore + fit of the previous batch); measured on B200 1080p
+  // B=256: pipelined step 43 us vs 50 us with every slot taken
+  if (share && per_sm > 1) --per_sm;
   if (per_sm < 1) return ECA_ERR_CUDA;
   const size_t smem = warp_layout(NS, J.rowcap, warps).total;
   const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
@@ -192,14 +201,16 @@ PointsJob points_job(const StripJob& J, void* workspace) {
   return PJ;
 }
 
-int launch_bounds(const StripJob& J, void* workspace, cudaStream_t stream, bool overlap = false) {
+int launch_bounds(const StripJob& J, void* workspace, cudaStream_t stream, bool overlap = false,
+                  bool share = false) {
   if (J.batch == 0) return ECA_OK;
   static const int ns = [] {
     const char* v = std::getenv("ECA_WSTAGES");
     return v ? std::atoi(v) : 1;
   }();
   const PointsJob PJ = points_job(J, workspace);
-  return ns == 2 ? launch_points_t<2>(PJ, stream, overlap) : launch_points_t<1>(PJ, stream, overlap);
+  return ns == 2 ? launch_points_t<2>(PJ, stream, overlap, share)
+                 : launch_points_t<1>(PJ, stream, overlap, share);
 }
 
 // one warp per CTA (4 half rows): small CTAs slot in beside a running
@@ -234,16 +245,16 @@ struct FitJob {
 };
 
 // one warp per frame (same arithmetic order as the fused path's fit_warp)
-constexpr int kFitFramesPerCta = 1;   // spread the frames over every SM
-
-__global__ void __launch_bounds__(32 * kFitFramesPerCta) fit_kernel(const __grid_constant__ FitJob J,
-                                                                   int batch) {
-  __shared__ FitScratchW fs[kFitFramesPerCta];
-  const int w = threadIdx.x >> 5;
-  const int b = blockIdx.x * kFitFramesPerCta + w;
+// One frame per single-warp CTA with n_cand-sized shared scratch (2.3 KB at
+// 1080p): small CTAs slot in beside a running bounds kernel of the next batch.
+__global__ void __launch_bounds__(32) fit_kernel(const __grid_constant__ FitJob J, int batch) {
+  extern __shared__ __align__(16) uint8_t fit_smem[];
+  const int b = blockIdx.x;
   if (b >= batch) return;
+  FitPt* pt = reinterpret_cast<FitPt*>(fit_smem);
+  double* ps = reinterpret_cast<double*>(fit_smem + size_t(J.n_cand) * sizeof(FitPt));
   const size_t o = size_t(b) * J.n_cand;
-  fit_warp(J.x + o, J.y + o, J.s + o, J.n_cand, J.p, J.trip, J.exhaustive, &fs[w], J.out + b);
+  fit_warp(J.x + o, J.y + o, J.s + o, J.n_cand, J.p, J.trip, J.exhaustive, pt, ps, J.out + b);
 }
 
 int check_fit_params(const EcaParams* params) {
@@ -284,7 +295,7 @@ extern "C" int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t 
                                       const EcaParams* params, int32_t* out_x, int32_t* out_y,
                                       double* out_score, void* workspace, int flags,
                                       void* stream) {
-  if (flags & ~ECA_BOUNDS_OVERLAP_PREVIOUS) return ECA_ERR_ARG;
+  if (flags & ~(ECA_BOUNDS_OVERLAP_PREVIOUS | ECA_BOUNDS_SHARE_SMS)) return ECA_ERR_ARG;
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
                              n_strips, params);
@@ -293,7 +304,8 @@ extern "C" int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t 
   J.out_x = out_x;
   J.out_y = out_y;
   J.out_score = out_score;
-  return launch_bounds(J, workspace, as_stream(stream), (flags & ECA_BOUNDS_OVERLAP_PREVIOUS) != 0);
+  return launch_bounds(J, workspace, as_stream(stream), (flags & ECA_BOUNDS_OVERLAP_PREVIOUS) != 0,
+                       (flags & ECA_BOUNDS_SHARE_SMS) != 0);
 }
 
 extern "C" int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
@@ -343,7 +355,7 @@ extern "C" int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const doubl
   if (!cand_x || !cand_y || !cand_score || !out || (!exhaustive && !triplets)) return ECA_ERR_ARG;
   if (check_fit_params(params)) return ECA_ERR_ARG;
   FitJob J{cand_x, cand_y, cand_score, n_cand, exhaustive ? 1 : 0, *params, triplets, out};
-  fit_kernel<<<(batch + kFitFramesPerCta - 1) / kFitFramesPerCta, 32 * kFitFramesPerCta, 0,
+  fit_kernel<<<batch, 32, size_t(n_cand) * (sizeof(FitPt) + sizeof(double)),
                as_stream(stream)>>>(J, batch);
   return check_launch();
 }

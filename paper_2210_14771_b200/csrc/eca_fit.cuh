@@ -387,9 +387,10 @@ ECA_DEV Ring ring_dead() {   // matches no point (hypothesis no longer alive)
   return Ring{1.0, -1.0, -1.0, -1.0};
 }
 
+// pt / ps: shared scratch for n_cand points (FitScratchW, or n_cand-sized)
 ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double* cand_s,
                       int n_cand, const EcaParams& p, const int16_t* trip, int exhaustive,
-                      FitScratchW* fs, EcaFitRecord* out) {
+                      FitPt* pt, double* ps, EcaFitRecord* out) {
   const int lane = threadIdx.x & 31;
   const int W = p.width, H = p.height;
   int n = 0;
@@ -417,8 +418,8 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
       q.yy = mul_rn(q.y, q.y);
       q.xz = mul_rn(q.x, q.z);
       q.yz = mul_rn(q.y, q.z);
-      fs->pt[pos] = q;
-      fs->ps[pos] = s;
+      pt[pos] = q;
+      ps[pos] = s;
     }
     n += __popc(bal);
   }
@@ -445,8 +446,8 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
         i1 = t[1];
         i2 = t[2];
       }
-      c = circumcircle(fs->pt[i0].x, fs->pt[i0].y, fs->pt[i1].x, fs->pt[i1].y, fs->pt[i2].x,
-                       fs->pt[i2].y);
+      c = circumcircle(pt[i0].x, pt[i0].y, pt[i1].x, pt[i1].y, pt[i2].x,
+                       pt[i2].y);
     }
     // iterated masked least squares (fitting.py:193-203); every lane runs the
     // loop, dead hypotheses with an empty ring.  Outliers contribute fma(0, v, s)
@@ -456,7 +457,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
       double mo[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll 4
       for (int k = 0; k < n; ++k) {
-        const FitPt P = fs->pt[k];
+        const FitPt P = pt[k];
         // w in {0, 1}: fma(1, v, s) == add_rn(s, v) and fma(0, v, s) == s
         const double w = inlier_w(P, c, g, tol) ? 1.0 : 0.0;
         mo[0] = __fma_rn(w, P.x, mo[0]);
@@ -486,8 +487,8 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
       const Ring g = c.alive ? ring_of(c, tol) : ring_dead();
 #pragma unroll 4
       for (int k = 0; k < n; ++k) {
-        const bool in = inlier_w(fs->pt[k], c, g, tol);
-        score = __fma_rn(in ? 1.0 : 0.0, fs->ps[k], score);
+        const bool in = inlier_w(pt[k], c, g, tol);
+        score = __fma_rn(in ? 1.0 : 0.0, ps[k], score);
         inl += in;
       }
     }

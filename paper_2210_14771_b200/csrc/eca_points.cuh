@@ -40,6 +40,7 @@
 namespace eca {
 
 constexpr int kSlots = 8;
+constexpr int kRefineMin = 8;    // step C: refine lane-chunk bounds above this many
 constexpr float kEarlyD = 0.1f;   // D_up(carry) level that triggers the early LB (gray ~37)
 
 // one survivor: column, preceding sum and the 9 neighbourhood sums (rows h-1..h+1)
@@ -418,52 +419,123 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     }
     __syncwarp();
 
-    // ---- step C: the other lane-chunks whose U reaches LB (if full: every
-    // one with U > 0 or a non-flat scoreable column); LB tightens with every
-    // evaluated group
-    int n_sel = 0;
-    for (int k = 0; k < nch_eff; ++k) {
-      const float v = __half2float(ut_s[k * 32 + lane]);
-      bool s;
-      if (full) {
-        // flat column: identical left/right sums per row and identical top and
-        // bottom rows (score exactly 0); lane-chunks of only such columns and
-        // U == 0 cannot hold the argmax.  Flat rows (black borders) would
-        // otherwise evaluate every column.
-        s = v > 0.0f;
-        if (v == 0.0f) {   // v < 0: evaluated in step B
-          const int xa = xa_of(k, lane);
+    // ---- step C: the other lane-chunks whose U reaches LB; LB tightens (and
+    // a "full" row can become a normal one) with every evaluated group.
+    // Phase 0: lane-chunks with U >= LB (every U > 0 one while full).
+    // Phase 1, only if still full: lane-chunks of U == 0 holding a non-flat
+    // scoreable column (their scores are FP64 rounding residues).  Flat columns
+    // (identical left/right sums per row, identical top and bottom rows) score
+    // exactly 0; flat rows (black borders) would otherwise evaluate every column.
+    for (int phase1 = 0; phase1 < 2; ++phase1) {
+      if (phase1 && !full) break;
+      int n_sel = 0;
+      for (int k = 0; k < nch_eff; ++k) {
+        const float v = __half2float(ut_s[k * 32 + lane]);   // < 0: evaluated in step B
+        bool s;
+        if (!phase1) {
+          s = v > 0.0f && (full || v >= lb);
+        } else {
+          s = false;
+          if (v == 0.0f) {
+            const int xa = xa_of(k, lane);
+            int s0[10], s1[10], s2[10];
+            load10(st, rb[0] + 3 * xa, al, s0);
+            load10(st, rb[1] + 3 * xa, al, s1);
+            load10(st, rb[2] + 3 * xa, al, s2);
+#pragma unroll
+            for (int i = 0; i < kPx; ++i) {
+              const bool flat = s0[i] == s0[i + 2] && s1[i] == s1[i + 2] && s0[i] == s2[i] &&
+                                s0[i + 1] == s2[i + 1] && s0[i + 2] == s2[i + 2];
+              s |= !flat && unsigned(xa + i - slo) <= unsigned(shi - slo);
+            }
+          }
+        }
+        const unsigned bm = __ballot_sync(kFull, s);
+        if (s) sel_s[n_sel + __popc(bm & lt_mask)] = uint16_t((k << 5) | lane);
+        n_sel += __popc(bm);
+      }
+      __syncwarp();
+      if (!phase1 && !full && n_sel > kRefineMin) {
+        // refine: one lane per selected lane-chunk, its 8 columns' exact bounds
+        // (branch-free, so the columns overlap): U2 = max U_col replaces U,
+        // LB takes max L_col; then only lane-chunks with U2 >= LB stay
+        for (int p0 = 0; p0 < n_sel; p0 += 32) {
+          const int p = p0 + lane;
+          const bool valid = p < n_sel;
+          const int e = valid ? int(sel_s[p]) : 0;
+          const int xa = xa_of(e >> 5, e & 31);
           int s0[10], s1[10], s2[10];
           load10(st, rb[0] + 3 * xa, al, s0);
           load10(st, rb[1] + 3 * xa, al, s1);
           load10(st, rb[2] + 3 * xa, al, s2);
+          int pre[kPx];
+          int run = int(ex_s[e]);
+          if (half) {
+#pragma unroll
+            for (int i = kPx - 1; i >= 0; --i) {
+              pre[i] = run;
+              run = max(run, s1[i + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < kPx; ++i) {
+              pre[i] = run;
+              run = max(run, s1[i + 1]);
+            }
+          }
+          float umax = 0.0f, lmax = 0.0f;
 #pragma unroll
           for (int i = 0; i < kPx; ++i) {
-            const bool flat = s0[i] == s0[i + 2] && s1[i] == s1[i + 2] && s0[i] == s2[i] &&
-                              s0[i + 1] == s2[i + 1] && s0[i + 2] == s2[i + 2];
-            s |= !flat && unsigned(xa + i - slo) <= unsigned(shi - slo);
+            const int x = xa + i;
+            const int cl = s0[i] + 2 * s1[i] + s2[i], cr = s0[i + 2] + 2 * s1[i + 2] + s2[i + 2];
+            const int gx3 = cr - cl;
+            const int gy3 = (s2[i] - s0[i]) + 2 * (s2[i + 1] - s0[i + 1]) + (s2[i + 2] - s0[i + 2]);
+            const int q = gx3 * gx3 + gy3 * gy3;
+            const int d2x = (W - 1) - 2 * x;
+            const int dot = gx3 * d2x + gy3 * d2y;
+            const int crs = abs(gx3 * d2y - gy3 * d2x);
+            const float fd = float(abs(dot)), fc = float(crs);
+            const float ps = fc * rcpf(fmaxf(fd + fc, 1.0f));
+            int ab = min(int((dot >= 0 ? ps : 2.0f - ps) * (kABins / 2)), kABins - 1);
+            if (dot == 0 && crs == 0) ab = kABins;
+            const float2 at = atab[ab];
+            const float t = t_term(q, tk), dd = d_term(pre[i], tk);
+            const bool in = unsigned(x - slo) <= unsigned(shi - slo) && q > 0;
+            umax = fmaxf(umax, in ? fminf(t * hi_f, 1.0f) * fminf(dd * hi_f, 1.0f) * at.y : 0.0f);
+            lmax = fmaxf(lmax, in ? t * lo_f * dd * lo_f * at.x : 0.0f);
           }
+          if (valid) ut_s[(e >> 5) * 32 + (e & 31)] = __float2half_ru(umax);
+          lb = fmaxf(lb, warp_max_nonneg(valid ? lmax : 0.0f));
         }
-      } else {
-        s = v > 0.0f && v >= lb;
+        full = !(lb >= J.tau);
+        __syncwarp();
+        int n2 = 0;   // keep the lane-chunks whose refined bound reaches LB
+        for (int p0 = 0; p0 < n_sel; p0 += 32) {
+          const int p = p0 + lane;
+          const int e = p < n_sel ? int(sel_s[p]) : 0;
+          const bool keep = p < n_sel && __half2float(ut_s[(e >> 5) * 32 + (e & 31)]) >= lb;
+          const unsigned bm = __ballot_sync(kFull, keep);
+          __syncwarp();
+          if (keep) sel_s[n2 + __popc(bm & lt_mask)] = uint16_t(e);
+          n2 += __popc(bm);
+          __syncwarp();
+        }
+        n_sel = n2;
       }
-      const unsigned bm = __ballot_sync(kFull, s);
-      if (s) sel_s[n_sel + __popc(bm & lt_mask)] = uint16_t((k << 5) | lane);
-      n_sel += __popc(bm);
-    }
-    __syncwarp();
-    for (int g0 = 0; g0 < n_sel; g0 += 4) {
-      const int p = g0 + (lane >> 3);
-      const bool vc = p < n_sel;
-      const int e = vc ? int(sel_s[p]) : 0;
-      if (!full && !__any_sync(kFull, vc && __half2float(ut_s[(e >> 5) * 32 + (e & 31)]) >= lb))
-        continue;
-      const ColEval cc = eval(vc, e);
+      for (int g0 = 0; g0 < n_sel; g0 += 4) {
+        const int p = g0 + (lane >> 3);
+        const bool vc = p < n_sel;
+        const int e = vc ? int(sel_s[p]) : 0;
+        if (!full && !__any_sync(kFull, vc && __half2float(ut_s[(e >> 5) * 32 + (e & 31)]) >= lb))
+          continue;
+        const ColEval cc = eval(vc, e);
 #ifdef ECA_WARP_TIMES
-      ++dbg_groups;
+        ++dbg_groups;
 #endif
-      lb = fmaxf(lb, warp_max_nonneg(cc.L));
-      emit(vc, cc);
+        lb = fmaxf(lb, warp_max_nonneg(cc.L));
+        full = !(lb >= J.tau);
+        emit(vc, cc);
+      }
     }
     if (lb >= J.tau) compact(lb);   // final LB: full rows keep every non-flat column
 

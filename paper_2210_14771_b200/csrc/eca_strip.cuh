@@ -592,7 +592,8 @@ __global__ void __launch_bounds__(MAXT, MINB) strip_kernel(const __grid_constant
         if (__shfl_sync(kFull, last, 0)) {
           __threadfence();
           fit_warp(J.out_x + o, J.out_y + o, J.out_score + o, 2 * S, J.p, J.triplets,
-                   J.exhaustive, reinterpret_cast<FitScratchW*>(st), J.out_fit + frame);
+                   J.exhaustive, reinterpret_cast<FitScratchW*>(st)->pt,
+                   reinterpret_cast<FitScratchW*>(st)->ps, J.out_fit + frame);
           if (lane == 0) J.counters[frame] = 0;
         }
       }

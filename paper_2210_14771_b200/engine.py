@@ -58,8 +58,9 @@ class ContentAreaEngine:
         self.graph = None
         self._pipe = None
         # consecutive run_pipelined() bounds launches touch different buffer
-        # sets: let each start while the previous one drains
-        self.pipeline_flags = _lib.BOUNDS_OVERLAP_PREVIOUS
+        # sets: let each start while the previous one drains, and leave room
+        # on every SM for the side stream's rescore + fit
+        self.pipeline_flags = _lib.BOUNDS_OVERLAP_PREVIOUS | _lib.BOUNDS_SHARE_SMS
         # Small batches (latency): one fused launch whose last strip CTA per
         # frame runs the fit.  Large batches (throughput): bound-and-prune
         # kernel, FP64 rescore of the survivors, then a fit kernel (one warp

@@ -224,7 +224,7 @@ def test_split_stages_match_points():
     assert lib.eca_bounds_handcrafted(
         ctypes.c_void_p(frames.data_ptr()), len(frames), frames.stride(0), frames.stride(1), eng._rows,
         None, eng.n_strips, ctypes.byref(eng.params), api._ptr(xs), api._ptr(ys), api._ptr(sc),
-        api._ptr(eng.workspace), 2, st) == _lib.ECA_ERR_ARG
+        api._ptr(eng.workspace), 4, st) == _lib.ECA_ERR_ARG
 
 
 def test_graph_replay_matches_direct():
