@@ -252,14 +252,13 @@ def run_ours(args) -> None:
     value = world * BATCH * args.steps / (ms / 1e3)
     ms_step = ms / args.steps
 
-    # kernel-only timing of the dominant stage of the step (K1 points:
-    # bounds_kernel + its small rescore_kernel), launched alone on the same
-    # stream over the same rotating pool
+    # kernel-only timing of the step's dominant kernel (K1 bound-and-prune,
+    # bounds_kernel), launched alone on the same stream over the same pool
     kt0, kt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     kt0.record(stream)
     for i in range(args.steps):
-        eng.points(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
+        eng.bounds(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
     kt1.record(stream)
     torch.cuda.synchronize()
     k_ms = kt0.elapsed_time(kt1) / args.steps
@@ -322,8 +321,8 @@ def run_ours(args) -> None:
                        "pipelining": "2 streams: rescore+fit of batch i overlap bound-and-prune of batch i+1"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "K1 points stage: eca::bounds_kernel<1> + eca::rescore_kernel "
-                                   "(strip scoring + candidates, 2 launches timed together)",
+                         "kernel": "eca::bounds_kernel<1> (K1 strip scoring: exact integer Sobel / "
+                                   "preceding max, FP32 bound-and-prune, survivor slots)",
                          "kernel_share_of_step": round(k_ms / ms_step, 3),
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "kernel_ms": round(k_ms, 5), "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},

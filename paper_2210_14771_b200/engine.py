@@ -187,6 +187,16 @@ class ContentAreaEngine:
         if self._pipe is not None and self._pipe["done"] is not None:
             stream.wait_event(self._pipe["done"])
 
+    def bounds(self, frames: torch.Tensor) -> None:
+        """Only the bound-and-prune kernel (the step's dominant kernel; its
+        survivors land in the workspace): the bench's roofline timing."""
+        f = self._check_frames(frames)
+        _lib.check(_lib.load().eca_bounds_handcrafted(
+            ctypes.c_void_p(f.data_ptr()), self.batch, f.stride(0), f.stride(1), self._rows, None,
+            self.n_strips, ctypes.byref(self.params), api._ptr(self.xs), api._ptr(self.ys),
+            api._ptr(self.sc), api._ptr(self.workspace), 0, api._stream(self.device)),
+            "eca_bounds_handcrafted")
+
     def run(self, frames: torch.Tensor) -> torch.Tensor:
         """Frames on this GPU -> device records (asynchronous)."""
         f = self._check_frames(frames)
