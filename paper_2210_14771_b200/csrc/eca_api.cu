@@ -189,10 +189,46 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share)
   return check_launch();
 }
 
+// A bounds per pseudo-angle bin (as build_tables in eca_strip.cuh), in double
+// on the host, padded kPadRel outward
+void angle_table(double angle_scale, float2* at) {
+  const double pi = 3.14159265358979323846;
+  auto theta_of = [&](double ps) {
+    ps = std::fmin(std::fmax(ps, 0.0), 2.0);
+    return ps <= 1.0 ? std::atan2(ps, 1.0 - ps) : pi - std::atan2(2.0 - ps, ps - 1.0);
+  };
+  auto term = [&](double th) { return 2.0 / (1.0 + std::exp(2.0 * angle_scale * th)); };
+  const double lo_f = 1.0 - kPadRel, hi_f = 1.0 + kPadRel;
+  for (int k = 0; k < kABins; ++k) {
+    const double w = 2.0 / kABins;
+    const double th_lo = theta_of(k * w - 1e-5), th_hi = theta_of((k + 1) * w + 1e-5);
+    at[k] = make_float2(float(term(th_hi) * lo_f), float(std::fmin(term(th_lo) * hi_f, 1.0)));
+  }
+  at[kABins] = make_float2(float(term(pi) * lo_f), 1.0f);   // dot == cross == 0
+}
+
 PointsJob points_job(const StripJob& J, void* workspace) {
   const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
   PointsJob PJ;
   PJ.J = J;
+  {   // the table depends only on angle_scale: cached per host thread
+    thread_local double cached_scale = -1.0;
+    thread_local float2 cached[kABins + 1];
+    if (cached_scale != J.p.angle_scale) {
+      angle_table(J.p.angle_scale, cached);
+      cached_scale = J.p.angle_scale;
+    }
+    std::memcpy(PJ.atab, cached, sizeof(cached));
+  }
+  const double log2e = 1.4426950408889634;
+  PJ.kt = float(-2.0 * log2e / (3.0 * J.p.gradient_threshold));
+  PJ.kd = float(2.0 * log2e / (3.0 * J.p.intensity_threshold));
+  PJ.cxf = double(J.p.width - 1) / 2.0;   // exact (halving)
+  PJ.cyf = double(J.p.height - 1) / 2.0;
+  const int64_t nfs = int64_t(J.batch) * J.n_strips;
+  PJ.s_magic = nfs < (int64_t(1) << 25)
+                   ? uint32_t(((uint64_t(1) << 32) + uint64_t(J.n_strips) - 1) / uint64_t(J.n_strips))
+                   : 0u;
   uint8_t* w = reinterpret_cast<uint8_t*>(workspace);
   PJ.ticket = reinterpret_cast<int32_t*>(w);
   PJ.slots = reinterpret_cast<SurvSlot*>(w + 256);

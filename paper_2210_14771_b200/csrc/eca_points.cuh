@@ -40,6 +40,10 @@
 namespace eca {
 
 constexpr int kSlots = 8;
+#ifndef ECA_STATIC_ROUNDS
+#define ECA_STATIC_ROUNDS 1
+#endif
+constexpr int kStaticRounds = ECA_STATIC_ROUNDS;   // items per warp assigned before tickets
 constexpr int kRefineMin = 8;    // step C: refine lane-chunk bounds above this many
 constexpr float kEarlyD = 0.1f;   // D_up(carry) level that triggers the early LB (gray ~37)
 
@@ -60,7 +64,28 @@ struct PointsJob {
   SurvSlot* slots;     // [n_halfrows][kSlots]
   int32_t* counts;     // [n_halfrows]: survivors, or -1 when resolved in bounds_kernel
   int32_t* ticket;     // [0] next item, [1] warps done; zero between launches
+  // host-computed constants (launch_points_t): no FP64 division, atan2f or
+  // integer division in the kernel prologue / item decode
+  float2 atab[kABins + 1];   // A bounds per pseudo-angle bin (see eca_strip.cuh)
+  float kt, kd;              // TermK
+  double cxf, cyf;           // (W-1)/2, (H-1)/2
+  uint32_t s_magic;          // ceil(2^32 / n_strips) when batch*n_strips < 2^25, else 0
 };
+
+// item -> (frame, strip): multiply-high division when the host provided it
+ECA_DEV void decode_item(const PointsJob& PJ, int fs, int& frame, int& strip) {
+  const int S = PJ.J.n_strips;
+  frame = PJ.s_magic ? int(__umulhi(uint32_t(fs), PJ.s_magic)) : fs / S;
+  strip = fs - frame * S;
+}
+
+// first TMA copies of a half-row item (lane 0)
+ECA_DEV void issue_item_half(const PointsJob& PJ, int item, uint8_t* stage, uint64_t* bar,
+                             uint64_t pol, int split) {
+  int frame, strip;
+  decode_item(PJ, item >> 1, frame, strip);
+  issue_half(PJ.J, item & 1, frame, strip, stage, bar, pol, split);
+}
 
 // RGB sums of the 10 pixels x0-1 .. x0+8 of one staged row; B = smem byte of
 // pixel x0.  `al`: B % 8 == 0 (warp-uniform), else funnel-shifted word loads.
@@ -127,30 +152,27 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
   uint16_t* ex_s = reinterpret_cast<uint16_t*>(mine + WL.exs);
   uint16_t* sel_s = reinterpret_cast<uint16_t*>(mine + WL.sel);
 
-  {
-    const float lo_f = 1.0f - kPadRel, hi_f = 1.0f + kPadRel;
-    const float asc = float(J.p.angle_scale);
-    for (int k = threadIdx.x; k < kABins; k += blockDim.x) {
-      const float w = 2.0f / kABins;
-      const float th_lo = theta_of(k * w - 1e-5f), th_hi = theta_of((k + 1) * w + 1e-5f);
-      atab[k] = make_float2(angle_term(th_hi, asc) * lo_f, fminf(angle_term(th_lo, asc) * hi_f, 1.0f));
-    }
-    if (threadIdx.x == 0)
-      atab[kABins] = make_float2(angle_term(3.14159265358979f, asc) * lo_f, 1.0f);
-  }
-  const int nw = gridDim.x * warps;
-  // items are handed out dynamically (item costs vary with the early exit);
-  // qitem[s] = item in flight in stage s
+  for (int k = threadIdx.x; k <= kABins; k += blockDim.x) atab[k] = PJ.atab[k];
+  const int gw = blockIdx.x * warps + wib, nw = gridDim.x * warps;
+  // Items: the first kStaticRounds per warp are fixed (gw, gw + nw, ...), the
+  // rest come from a ticket counter (item costs vary ~5x with the early exit
+  // and row content; static assignment alone left a long tail, tickets alone
+  // cost an atomic round trip per item).  qitem[s] = item in flight in stage s.
   int* qitem = reinterpret_cast<int*>(bars + 8);
+  int assigned = 0;   // items handed to this warp so far (lane 0)
+  auto next_item = [&]() -> int {
+    const int r = assigned++;
+    return r < kStaticRounds ? gw + r * nw : kStaticRounds * nw + atomicAdd(PJ.ticket, 1);
+  };
   uint64_t pol = 0;
   if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
     pol = l2_evict_first();
     for (int s = 0; s < NS; ++s) {
-      const int it = atomicAdd(PJ.ticket, 1);
+      const int it = next_item();
       qitem[s] = it;
-      if (it < n_items) issue_half(J, it, mine + s * WL.stage, &bars[s], pol, split);
+      if (it < n_items) issue_item_half(PJ, it, mine + s * WL.stage, &bars[s], pol, split);
     }
   }
   __syncthreads();
@@ -162,12 +184,9 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
   }
 #endif
 
-  const double log2e = 1.4426950408889634;
-  const TermK tk{float(-2.0 * log2e / (3.0 * J.p.gradient_threshold)),
-                 float(2.0 * log2e / (3.0 * J.p.intensity_threshold))};
+  const TermK tk{PJ.kt, PJ.kd};
   const float lo_f = 1.0f - kPadRel, hi_f = 1.0f + kPadRel;
-  const double cxf = div_rn(double(W - 1), 2.0);
-  const double cyf = div_rn(double(H - 1), 2.0);
+  const double cxf = PJ.cxf, cyf = PJ.cyf;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int gi = lane & 7;   // column within an evaluated lane-chunk
 
@@ -183,8 +202,8 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
 #endif
     const int half = item & 1;
     const int fs = item >> 1;
-    const int frame = fs / S;
-    const int strip = fs - frame * S;
+    int frame, strip;
+    decode_item(PJ, fs, frame, strip);
     const int y = J.rows[strip];
     const int d2y = (H - 1) - 2 * y;
     const int hw = half ? W - split : split;        // columns in this half
@@ -584,9 +603,9 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     if (lane == 0) {
       // the ticket is taken only now: a warp never holds work it cannot start
       // (prefetching it measured 30% slower from the end-of-kernel imbalance)
-      const int nxt = atomicAdd(PJ.ticket, 1);
+      const int nxt = next_item();
       qitem[stage] = nxt;
-      if (nxt < n_items) issue_half(J, nxt, st, &bars[stage], pol, split);
+      if (nxt < n_items) issue_item_half(PJ, nxt, st, &bars[stage], pol, split);
     }
     __syncwarp();
     if (++stage == NS) {
@@ -621,16 +640,15 @@ __global__ void __launch_bounds__(128) rescore_kernel(const __grid_constant__ Po
   const int cnt = valid_hr ? __ldg(PJ.counts + hrow) : -1;
   const int half = hrow & 1;
   const int fs = hrow >> 1;
-  const int frame = fs / S, strip = fs - (fs / S) * S;
+  int frame, strip;
+  decode_item(PJ, fs, frame, strip);
   const int y = valid_hr ? J.rows[strip] : 0;
   Best b = half ? Best{0.0, W - 1} : Best{0.0, 0};
   if (valid_hr && k < cnt) {
     const SurvSlot s = PJ.slots[size_t(hrow) * kSlots + k];
     const int l[3] = {s.l[0], s.l[1], s.l[2]}, m[3] = {s.m[0], s.m[1], s.m[2]},
               r[3] = {s.r[0], s.r[1], s.r[2]};
-    const double cxf = div_rn(double(W - 1), 2.0);
-    const double cyf = div_rn(double(H - 1), 2.0);
-    b = Best{exact_score(l, m, r, s.pre, s.x, y, cxf, cyf, J.p), int(s.x)};
+    b = Best{exact_score(l, m, r, s.pre, s.x, y, PJ.cxf, PJ.cyf, J.p), int(s.x)};
   }
   // argmax inside each 8-lane group (half rows never mix)
 #pragma unroll

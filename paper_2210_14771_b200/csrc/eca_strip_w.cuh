@@ -95,13 +95,9 @@ ECA_DEV float t_term(int q, const TermK& k) {
 // 2 / (1 + exp(2 (p/3) / t_i)) for the integer preceding sum p
 ECA_DEV float d_term(int p, const TermK& k) { return 2.0f * rcpf(1.0f + ex2f(k.kd * float(p))); }
 
-// issue the three row copies of half-row item into `stage` (lane 0)
-ECA_DEV void issue_half(const StripJob& J, int item, uint8_t* stage, uint64_t* bar, uint64_t pol,
-                        int split) {
-  const int half = item & 1;
-  const int fs = item >> 1;
-  const int frame = fs / J.n_strips;
-  const int strip = fs - frame * J.n_strips;
+// issue the three row copies of one half strip row into `stage` (lane 0)
+ECA_DEV void issue_half(const StripJob& J, int half, int frame, int strip, uint8_t* stage,
+                        uint64_t* bar, uint64_t pol, int split) {
   const int W = J.p.width;
   const int xs = half ? split - 1 : 0;          // first staged column
   const int xe = half ? W : min(split + 1, W);  // one past the last staged column
