@@ -1,13 +1,17 @@
 // K3: learned strip scorer (edgenet.py) — fused RGBXY build + 3x(valid 3x3
 // conv + ReLU) + 1x1 head + sigmoid per strip, FP32 like the reference.
 //
-// One CTA = one column tile (kTX outputs) of one strip of one frame.  The
-// 7-row input window is built straight from the uint8 frame (no full-frame
-// make_rgbxy, edgenet.py:67-83: values computed in FP64 then rounded to FP32
-// exactly as numpy does), the three conv layers run out of shared memory with
-// each thread producing all output channels of one position (weights are
-// warp-broadcast float4 reads), and the head writes probabilities.  A second
-// small kernel selects the half-row winners (handcrafted.py:120-138 rules).
+// Persistent CTAs (2 per SM): the transposed weights, the exact per-byte
+// normalisation table and the biases are loaded once per CTA, which then loops
+// over tiles of kTX output columns of one strip of one frame.  The 7-row input
+// window is built straight from the uint8 frame (no full-frame make_rgbxy,
+// edgenet.py:67-83: values computed in FP64 then rounded to FP32 exactly as
+// numpy does; the per-byte table holds those exact values).  The conv layers
+// run out of shared memory, weights as warp-broadcast float4 reads; the
+// 32-channel layer is split over all 256 threads (two threads per column, 16
+// channels each; the head's channel sum continues in order through shared
+// memory).  A second small kernel selects the half-row winners
+// (handcrafted.py:120-138 rules).
 // Accumulation is sequential FMA over (c, ky, kx); the reference's sgemm
 // reassociates, so probabilities agree to ~1e-7, not bitwise.
 #include "eca_common.cuh"
@@ -16,7 +20,7 @@ using namespace eca;
 
 namespace {
 
-constexpr int kTX = 64;                  // output columns per CTA
+constexpr int kTX = 128;                 // output columns per tile
 constexpr int kW0 = 360, kB0 = 8, kW1 = 1152, kB1 = 16, kW2 = 4608, kB2 = 32, kW3 = 32;
 constexpr int kOffB0 = kW0, kOffW1 = kOffB0 + kB0, kOffB1 = kOffW1 + kW1, kOffW2 = kOffB1 + kB1;
 constexpr int kOffB2 = kOffW2 + kW2, kOffW3 = kOffB2 + kB2, kOffB3 = kOffW3 + kW3;
@@ -43,14 +47,14 @@ struct CnnSmem {
   float in[5][7][kTX + 8];
   float o1[8][5][kTX + 4];
   float o2[16][3][kTX + 2];
+  float lut[3][256];             // float((v - mean_c) / std_c), computed in FP64
+  float zpart[kTX];              // head partial sum over channels 0..15
 };
 
-__global__ void __launch_bounds__(256) cnn_kernel(const __grid_constant__ CnnJob J) {
+__global__ void __launch_bounds__(256, 2) cnn_kernel(const __grid_constant__ CnnJob J) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   CnnSmem& s = *reinterpret_cast<CnnSmem*>(smem_raw);
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int j0 = blockIdx.x * kTX;       // first output column (frame x = j0 + 3)
-  const int strip = blockIdx.y, b = blockIdx.z;
   const int W = J.W, H = J.H;
   const float* wg = J.weights;
 
@@ -77,27 +81,48 @@ __global__ void __launch_bounds__(256) cnn_kernel(const __grid_constant__ CnnJob
     s.w3[tid] = wg[kOffW3 + tid];
   }
   if (tid == 0) s.b3 = wg[kOffB3];
+  for (int i = tid; i < 3 * 256; i += nt) {
+    const int ch = i >> 8, v = i & 255;
+    s.lut[ch][v] = float(div_rn(sub_rn(double(v), J.mean[ch]), J.stdv[ch]));
+  }
+  const double xden = double(W - 1 > 1 ? W - 1 : 1), yden = double(H - 1 > 1 ? H - 1 : 1);
+  const double xc = div_rn(double(W - 1), 2.0), yc = div_rn(double(H - 1), 2.0);
+  const int tiles_x = (W - 6 + kTX - 1) / kTX;
+  const int n_tiles = tiles_x * J.S * J.batch;
+
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+  const int tx = t % tiles_x, fs = t / tiles_x;
+  const int strip = fs % J.S, b = fs / J.S;
+  const int j0 = tx * kTX;               // first output column (frame x = j0 + 3)
+  __syncthreads();                       // previous tile's buffers are free; tables ready
 
   // ---- RGBXY window (edgenet.py:75-82), rows h-3..h+3, columns j0..j0+kTX+5 ----
   const int h = J.rows[strip];
   const int band = J.band[strip];
   const uint8_t* fb = J.frames + int64_t(b) * J.fstride;
-  const double xden = double(W - 1 > 1 ? W - 1 : 1), yden = double(H - 1 > 1 ? H - 1 : 1);
-  const double xc = div_rn(double(W - 1), 2.0), yc = div_rn(double(H - 1), 2.0);
+  for (int c = tid; c < kTX + 6; c += nt) {   // X channel: one FP64 division per column
+    const int x = j0 + c;
+    const float fx = x < W ? float(div_rn(sub_rn(double(x), xc), xden)) : 0.f;
+#pragma unroll
+    for (int r = 0; r < 7; ++r) s.in[3][r][c] = fx;
+  }
+  if (tid < 7) {
+    const float fy = float(div_rn(sub_rn(double(h - 3 + tid), yc), yden));
+    for (int c = 0; c < kTX + 6; ++c) s.in[4][tid][c] = j0 + c < W ? fy : 0.f;
+  }
   for (int i = tid; i < 7 * (kTX + 6); i += nt) {
     const int r = i / (kTX + 6), c = i % (kTX + 6);
-    const int x = j0 + c, y = h - 3 + r;
-    float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    const int x = j0 + c;
+    float f0 = 0.f, f1 = 0.f, f2 = 0.f;
     if (x < W) {
       const uint8_t* px = fb + int64_t(band + r) * J.rstride + 3 * x;
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch)
-        f[ch] = float(div_rn(sub_rn(double(px[ch]), J.mean[ch]), J.stdv[ch]));
-      f[3] = float(div_rn(sub_rn(double(x), xc), xden));
-      f[4] = float(div_rn(sub_rn(double(y), yc), yden));
+      f0 = s.lut[0][px[0]];
+      f1 = s.lut[1][px[1]];
+      f2 = s.lut[2][px[2]];
     }
-#pragma unroll
-    for (int ch = 0; ch < 5; ++ch) s.in[ch][r][c] = f[ch];
+    s.in[0][r][c] = f0;
+    s.in[1][r][c] = f1;
+    s.in[2][r][c] = f2;
   }
   __syncthreads();
 
@@ -150,41 +175,57 @@ __global__ void __launch_bounds__(256) cnn_kernel(const __grid_constant__ CnnJob
   }
   __syncthreads();
 
-  // ---- layer 2: 16 -> 32 (one row) + 1x1 head + sigmoid ----
-  for (int c = tid; c < kTX; c += nt) {
-    const int j = j0 + c;
-    if (j >= W - 6) continue;
-    float acc[32];
+  // ---- layer 2: 16 -> 32 (one row), two threads per column (channels
+  // 16*hh .. 16*hh+15), then the 1x1 head + sigmoid ----
+  const int c = tid & (kTX - 1), hh = tid / kTX;   // hh is warp-uniform
+  float acc[16];
 #pragma unroll
-    for (int o = 0; o < 32; ++o) acc[o] = 0.f;
-    for (int ci = 0; ci < 16; ++ci)
+  for (int o = 0; o < 16; ++o) acc[o] = 0.f;
+  for (int ci = 0; ci < 16; ++ci)
 #pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const float v = s.o2[ci][k / 3][c + k % 3];
+    for (int k = 0; k < 9; ++k) {
+      const float v = s.o2[ci][k / 3][c + k % 3];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 w = s.w2[(ci * 9 + k) * 8 + q];
-          acc[4 * q + 0] = fmaf(w.x, v, acc[4 * q + 0]);
-          acc[4 * q + 1] = fmaf(w.y, v, acc[4 * q + 1]);
-          acc[4 * q + 2] = fmaf(w.z, v, acc[4 * q + 2]);
-          acc[4 * q + 3] = fmaf(w.w, v, acc[4 * q + 3]);
-        }
+      for (int q = 0; q < 4; ++q) {
+        const float4 w = s.w2[(ci * 9 + k) * 8 + 4 * hh + q];
+        acc[4 * q + 0] = fmaf(w.x, v, acc[4 * q + 0]);
+        acc[4 * q + 1] = fmaf(w.y, v, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(w.z, v, acc[4 * q + 2]);
+        acc[4 * q + 3] = fmaf(w.w, v, acc[4 * q + 3]);
       }
-    float z = 0.f;
+    }
+  // head: z = sum over channels 0..31 in order, so the second half continues
+  // the first half's partial sum
+  float z = 0.f;
+  if (hh == 0) {
 #pragma unroll
-    for (int o = 0; o < 32; ++o) {
+    for (int o = 0; o < 16; ++o) {
       const float y = acc[o] + s.b2[o];
       z = fmaf(s.w3[o], y > 0.f ? y : 0.f, z);
     }
-    z += s.b3;
-    float p;
-    if (z >= 0.f) {
-      p = 1.0f / (1.0f + expf(-z));
-    } else {
-      const float e = expf(z);
-      p = e / (1.0f + e);
+    s.zpart[c] = z;
+  }
+  __syncthreads();
+  if (hh == 1) {
+    z = s.zpart[c];
+#pragma unroll
+    for (int o = 0; o < 16; ++o) {
+      const float y = acc[o] + s.b2[16 + o];
+      z = fmaf(s.w3[16 + o], y > 0.f ? y : 0.f, z);
     }
-    J.probs[(size_t(b) * J.S + strip) * (W - 6) + j] = p;
+    z += s.b3;
+    const int j = j0 + c;
+    if (j < W - 6) {
+      float p;
+      if (z >= 0.f) {
+        p = 1.0f / (1.0f + expf(-z));
+      } else {
+        const float e = expf(z);
+        p = e / (1.0f + e);
+      }
+      J.probs[(size_t(b) * J.S + strip) * (W - 6) + j] = p;
+    }
+  }
   }
 }
 
@@ -264,13 +305,20 @@ extern "C" int eca_points_learned(const uint8_t* frames, int batch, int64_t fram
   J.probs = out_probs;
   auto st = reinterpret_cast<cudaStream_t>(stream);
   static bool attr = false;
+  static int per_sm = 1, sms = 148;
   if (!attr) {
     cudaFuncSetAttribute(cnn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(CnnSmem)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cnn_kernel, 256, sizeof(CnnSmem));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (per_sm < 1) per_sm = 1;
     attr = true;
   }
-  const int tiles = (width - 6 + kTX - 1) / kTX;
-  cnn_kernel<<<dim3(tiles, n_strips, batch), 256, sizeof(CnnSmem), st>>>(J);
+  const int64_t tiles = int64_t((width - 6 + kTX - 1) / kTX) * n_strips * batch;
+  const int grid = int(tiles < int64_t(sms) * per_sm ? tiles : int64_t(sms) * per_sm);
+  cnn_kernel<<<grid, 256, sizeof(CnnSmem), st>>>(J);
   select_kernel<<<dim3(n_strips, batch), 256, 0, st>>>(out_probs, n_strips, width, nullptr, out_x,
                                                         out_y, out_score, J);
   return cudaGetLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
