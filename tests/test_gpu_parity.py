@@ -227,6 +227,35 @@ def test_split_stages_match_points():
         api._ptr(eng.workspace), 4, st) == _lib.ECA_ERR_ARG
 
 
+@pytest.mark.parametrize("w,h,pad", [(333, 241, 7), (517, 300, 1), (1001, 480, 13), (2049, 200, 5),
+                                     (64, 40, 3)])
+def test_points_odd_sizes_and_strides(w, h, pad):
+    """Odd widths and padded, unaligned row strides: the bound-and-prune
+    kernel's unaligned loads, both halves' staging and the fused path against
+    the oracle."""
+    specs = synth.bench_specs(5, w, h, seed=w + h)
+    frames = np.stack([synth.render(s, 11 + k) for k, (_, s) in enumerate(specs)])
+    b = len(frames)
+    rs = 3 * w + pad                        # row stride (bytes), not a multiple of 4
+    fs = h * rs + 9                         # frame stride
+    buf = torch.zeros(b * fs + 64, dtype=torch.uint8, device="cuda")
+    t = torch.as_strided(buf[1:], (b, h, w, 3), (fs, rs, 3, 1))   # odd base address too
+    t.copy_(torch.from_numpy(frames).cuda())
+    cfg = eb.EcaConfig()
+    want = [orc.handcrafted_candidates(frames[k], cfg) for k in range(b)]
+    eng = eb.ContentAreaEngine(h, w, b)
+    eng.points(t)                           # bounds + rescore (workspace path)
+    xs, sc = eng.xs.cpu().numpy(), eng.sc.cpu().numpy()
+    for k in range(b):
+        assert xs[k].tolist() == want[k][0].tolist(), (k, xs[k], want[k][0])
+        assert close_scores(sc[k], want[k][2]).all(), k
+    rec = eng.run(t)                        # b <= 16: the fused single launch
+    for k, fit in enumerate(eng.fits(rec)):
+        ox, oy, osc = want[k][0], want[k][1], want[k][2]
+        keep = orc.keep_mask(ox, oy, osc, w, h, cfg)
+        assert_fit_equal(fit, orc.ransac(ox[keep], oy[keep], osc[keep], w, h, cfg, 0), k)
+
+
 def test_graph_replay_matches_direct():
     frame = synth.c1_frame()
     t = torch.from_numpy(frame).cuda().unsqueeze(0)
