@@ -293,9 +293,10 @@ def run_ours(args) -> None:
     h2d = BATCH * eng.n_strips * 3 * WIDTH * 3
     d2h = BATCH * 40
 
-    lat = None
+    lat = learned = None
     if rank == 0:
         lat = latency(eb, dev)
+        learned = learned_leg(eb, dev, pool, n_slots, peaks)
 
     out = None
     if rank == 0:
@@ -331,6 +332,7 @@ def run_ours(args) -> None:
                     "path": "ContentAreaEngine.run_host: strip-row H2D (cudaMemcpy2DAsync) + "
                             "bounds/rescore/fit launches + record D2H"},
             "latency_ms": lat,
+            "learned": learned,
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * eng.launches_per_run,
             "cpu_baseline": cpu,
@@ -340,6 +342,44 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
     if out is not None:
         print(json.dumps(out), flush=True)
+
+
+# FLOPs of the strip CNN per frame: 16 strips x
+# 2 x [5*8*9*5*(W-2) + 8*16*9*3*(W-4) + 16*32*9*(W-6) + 32*(W-6)]
+CNN_FLOP_PER_FRAME = 16 * 2 * (5 * 8 * 9 * 5 * (WIDTH - 2) + 8 * 16 * 9 * 3 * (WIDTH - 4)
+                               + 16 * 32 * 9 * (WIDTH - 6) + 32 * (WIDTH - 6))
+
+
+def learned_leg(eb, dev, pool, n_slots, peaks) -> dict:
+    """C3: the learned variant (EdgeNet strip CNN, random-init FP32 weights
+    of the reference architecture, edgenet.py) over the same 256-frame
+    batches: CNN + half-row selection + fit, frames resident in HBM."""
+    import torch
+    from paper_2210_14771_b200.engine import ContentAreaEngine
+    net = eb.EdgeNet(eb.ChannelStats([100.0] * 3, [50.0] * 3), seed=0)
+    eng = ContentAreaEngine(HEIGHT, WIDTH, BATCH, variant=eb.Learned(net), device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for i in range(3):
+        eng.run(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
+    steps = 20
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for i in range(steps):
+        eng.run(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    tflops = CNN_FLOP_PER_FRAME * BATCH / (ms * 1e-3) / 1e12
+    peak = peaks.get("bf16_tflops", 2250.0)
+    return {"metric": "learned-variant frames/s (C3: EdgeNet strip CNN + select + fit)",
+            "value": round(BATCH / (ms * 1e-3), 1), "unit": "frames/s", "ms_per_step": round(ms, 4),
+            "steps": steps, "dtype": "f32", "launches_per_step": eng.launches_per_run,
+            "roofline": {"bound": "tensor", "achieved": round(tflops, 2), "peak": peak,
+                         "unit": "TFLOP/s", "frac": round(tflops / peak, 4),
+                         "kernel": "cnn_kernel (SIMT FP32 this round; step time incl. select + fit)",
+                         "algorithmic_flop_per_frame": CNN_FLOP_PER_FRAME,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (measured)"}}
 
 
 def latency(eb, dev) -> dict:
