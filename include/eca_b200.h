@@ -139,6 +139,29 @@ int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
                             const EcaParams* params, int32_t* out_x, int32_t* out_y,
                             double* out_score, void* workspace, void* stream);
 
+/* Streamed throughput mode as one call per batch (what
+ * ContentAreaEngine.run_pipelined does): the bound-and-prune kernel of batch i
+ * runs on `stream`, its rescore + fit on the pipeline's own low-priority side
+ * stream, overlapping batch i+1's bound-and-prune.  Two buffer sets alternate
+ * in the caller's device `scratch` (eca_pipeline_bytes; zeroed by create):
+ * the records of step i stay valid until step i+2.  Same results as
+ * eca_points_handcrafted + eca_fit.  One host thread per pipeline. */
+typedef struct EcaPipeline EcaPipeline;
+int eca_pipeline_bytes(int batch, int n_strips, int64_t* out_bytes);
+int eca_pipeline_create(int batch, int height, int width, const int32_t* strip_rows,
+                        int n_strips, const EcaParams* params, const int16_t* triplets,
+                        void* scratch, int64_t scratch_bytes, EcaPipeline** out);
+/* Enqueue one batch; *out_records = this step's device records (batch x 40 B),
+ * complete once a stream has waited via eca_pipeline_fence. */
+int eca_pipeline_step(EcaPipeline* pipeline, const uint8_t* frames, int64_t frame_stride,
+                      int64_t row_stride, void* stream, EcaFitRecord** out_records);
+/* Make `stream` wait for every step enqueued so far. */
+int eca_pipeline_fence(EcaPipeline* pipeline, void* stream);
+/* The side stream (e.g. to gather the records of a step right after its fit). */
+int eca_pipeline_side_stream(EcaPipeline* pipeline, void** out_stream);
+/* Synchronises the side stream, releases streams/events (not the scratch). */
+int eca_pipeline_destroy(EcaPipeline* pipeline);
+
 /* Same, plus every column's FP64 score: out_scores[batch][n_strips][width]
  * (StripScoreRow.scores, handcrafted.py:25-31). */
 int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,

@@ -38,6 +38,13 @@ SIGNATURES = {
     "eca_bounds_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
                                _p, _p, _p, _p, ctypes.c_int, _p],
     "eca_rescore_handcrafted": [ctypes.c_int, _I32P, ctypes.c_int, _PARAMS, _p, _p, _p, _p, _p],
+    "eca_pipeline_bytes": [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)],
+    "eca_pipeline_create": [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I32P, ctypes.c_int, _PARAMS, _p,
+                            _p, _i64, ctypes.POINTER(ctypes.c_void_p)],
+    "eca_pipeline_step": [_p, _p, _i64, _i64, _p, ctypes.POINTER(ctypes.c_void_p)],
+    "eca_pipeline_fence": [_p, _p],
+    "eca_pipeline_side_stream": [_p, ctypes.POINTER(ctypes.c_void_p)],
+    "eca_pipeline_destroy": [_p],
     "eca_score_rows_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
                                    _p, _p, _p, _p, _p],
     "eca_fit": [_p, _p, _p, ctypes.c_int, ctypes.c_int, _PARAMS, _p, ctypes.c_int, _p, _p],

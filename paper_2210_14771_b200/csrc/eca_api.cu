@@ -131,19 +131,33 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share)
   // Items are handed out dynamically, so independent small CTAs cost
   // nothing; more resident warps shorten the end-of-kernel tail (B200,
   // 1080p B=256: 4 warps x 5 CTAs 50 us, 2 x 9 52 us, 8 x 2 56 us).
+  // (cached per host thread and row capacity: the occupancy queries cost
+  // microseconds, which matter at one launch per ~40 us batch)
+  thread_local int cached_rowcap = -1, cached_dev = -1, cached_warps = 0, cached_per_sm = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
   int warps = 0, per_sm = 0;
-  for (int w = 1; w <= 8; ++w) {
-    int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * w,
-                                                      warp_layout(NS, J.rowcap, w).total) !=
-        cudaSuccess)
-      return ECA_ERR_CUDA;
-    ECA_TRACE("bounds kernel: %d warps/CTA -> %d CTAs/SM (smem %zu)\n", w, b,
-              warp_layout(NS, J.rowcap, w).total);
-    if (b * w > per_sm * warps) {
-      warps = w;
-      per_sm = b;
+  if (cached_rowcap == J.rowcap && cached_dev == dev) {
+    warps = cached_warps;
+    per_sm = cached_per_sm;
+  } else {
+    for (int w = 1; w <= 8; ++w) {
+      int b = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * w,
+                                                        warp_layout(NS, J.rowcap, w).total) !=
+          cudaSuccess)
+        return ECA_ERR_CUDA;
+      ECA_TRACE("bounds kernel: %d warps/CTA -> %d CTAs/SM (smem %zu)\n", w, b,
+                warp_layout(NS, J.rowcap, w).total);
+      if (b * w > per_sm * warps) {
+        warps = w;
+        per_sm = b;
+      }
     }
+    cached_rowcap = J.rowcap;
+    cached_dev = dev;
+    cached_warps = warps;
+    cached_per_sm = per_sm;
   }
   static const int force_w = [] {   // tuning hook: ECA_BWARPS=<warps per CTA>
     const char* v = std::getenv("ECA_BWARPS");
@@ -383,6 +397,13 @@ extern "C" int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int6
   return launch_strips<true, false>(J, as_stream(stream));
 }
 
+namespace {
+int launch_fit(const FitJob& J, int batch, cudaStream_t stream) {
+  fit_kernel<<<batch, 32, size_t(J.n_cand) * (sizeof(FitPt) + sizeof(double)), stream>>>(J, batch);
+  return check_launch();
+}
+}  // namespace
+
 extern "C" int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const double* cand_score,
                        int batch, int n_cand, const EcaParams* params, const int16_t* triplets,
                        int exhaustive, EcaFitRecord* out, void* stream) {
@@ -391,9 +412,7 @@ extern "C" int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const doubl
   if (!cand_x || !cand_y || !cand_score || !out || (!exhaustive && !triplets)) return ECA_ERR_ARG;
   if (check_fit_params(params)) return ECA_ERR_ARG;
   FitJob J{cand_x, cand_y, cand_score, n_cand, exhaustive ? 1 : 0, *params, triplets, out};
-  fit_kernel<<<batch, 32, size_t(n_cand) * (sizeof(FitPt) + sizeof(double)),
-               as_stream(stream)>>>(J, batch);
-  return check_launch();
+  return launch_fit(J, batch, as_stream(stream));
 }
 
 extern "C" int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
@@ -453,6 +472,162 @@ extern "C" int eca_debug_strip_stats(unsigned long long* out, int reset) {
   return ECA_OK;
 }
 #endif
+
+
+// ---------------------------------------------------------------- pipeline
+// Streamed throughput mode as one native call per batch (ContentAreaEngine.
+// run_pipelined): bounds kernel of batch i on the caller's stream; rescore +
+// fit on the pipeline's side stream, overlapping batch i+1's bounds kernel.
+// Two buffer sets alternate inside the caller-provided scratch.
+struct EcaPipeline {
+  int batch, n_strips;
+  StripJob J;                 // template: geometry, params, tau
+  const int16_t* trip;
+  cudaStream_t side;
+  cudaEvent_t ev_bounds[2], ev_free[2];
+  bool used[2];
+  int step, last;
+  uint8_t* ws[2];
+  int32_t *xs[2], *ys[2];
+  double* sc[2];
+  EcaFitRecord* rec[2];
+};
+
+namespace {
+struct PipeLayout {
+  int64_t ws, xs, ys, sc, rec, set, total;
+};
+PipeLayout pipe_layout(int batch, int n_strips) {
+  auto up = [](int64_t v) { return (v + 255) & ~int64_t(255); };
+  PipeLayout L;
+  const int64_t nc = int64_t(batch) * 2 * n_strips;
+  L.ws = 0;
+  L.xs = up(points_workspace(batch, n_strips));
+  L.ys = L.xs + up(nc * 4);
+  L.sc = L.ys + up(nc * 4);
+  L.rec = L.sc + up(nc * 8);
+  L.set = L.rec + up(int64_t(batch) * int64_t(sizeof(EcaFitRecord)));
+  L.total = 2 * L.set;
+  return L;
+}
+}  // namespace
+
+extern "C" int eca_pipeline_bytes(int batch, int n_strips, int64_t* out_bytes) {
+  if (batch < 1 || n_strips < 1 || n_strips > ECA_MAX_STRIPS || !out_bytes) return ECA_ERR_ARG;
+  *out_bytes = pipe_layout(batch, n_strips).total;
+  return ECA_OK;
+}
+
+extern "C" int eca_pipeline_create(int batch, int height, int width, const int32_t* strip_rows,
+                                   int n_strips, const EcaParams* params, const int16_t* triplets,
+                                   void* scratch, int64_t scratch_bytes, EcaPipeline** out) {
+  if (!out || !scratch || !triplets || batch < 1) return ECA_ERR_ARG;
+  *out = nullptr;
+  if (!params || params->width != width || params->height != height) return ECA_ERR_ARG;
+  if (check_fit_params(params)) return ECA_ERR_ARG;
+  if (n_strips < 1 || n_strips > ECA_MAX_STRIPS) return ECA_ERR_UNSUPPORTED;
+  const PipeLayout L = pipe_layout(batch, n_strips);
+  if (scratch_bytes < L.total) return ECA_ERR_ARG;
+  static const uint8_t dummy[16] = {};
+  EcaPipeline* P = new EcaPipeline();
+  int rc = prepare_strip_job(P->J, dummy, batch, 0, 3LL * width, strip_rows, nullptr, n_strips,
+                             params);
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  P->batch = batch;
+  P->n_strips = n_strips;
+  P->trip = triplets;
+  P->step = 0;
+  P->last = -1;
+  uint8_t* base = reinterpret_cast<uint8_t*>(scratch);
+  for (int k = 0; k < 2; ++k) {
+    uint8_t* b = base + k * L.set;
+    P->ws[k] = b + L.ws;
+    P->xs[k] = reinterpret_cast<int32_t*>(b + L.xs);
+    P->ys[k] = reinterpret_cast<int32_t*>(b + L.ys);
+    P->sc[k] = reinterpret_cast<double*>(b + L.sc);
+    P->rec[k] = reinterpret_cast<EcaFitRecord*>(b + L.rec);
+    P->used[k] = false;
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (cudaMemset(scratch, 0, size_t(L.total)) != cudaSuccess ||   // tickets start at zero
+      cudaStreamCreateWithPriority(&P->side, cudaStreamNonBlocking, lo) != cudaSuccess) {
+    delete P;
+    return ECA_ERR_CUDA;
+  }
+  for (int k = 0; k < 2; ++k)
+    if (cudaEventCreateWithFlags(&P->ev_bounds[k], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_free[k], cudaEventDisableTiming) != cudaSuccess) {
+      cudaStreamDestroy(P->side);
+      delete P;
+      return ECA_ERR_CUDA;
+    }
+  *out = P;
+  return ECA_OK;
+}
+
+extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t frame_stride,
+                                 int64_t row_stride, void* stream, EcaFitRecord** out_records) {
+  if (!P || !frames || !out_records || row_stride < 3LL * P->J.p.width || frame_stride < 0)
+    return ECA_ERR_ARG;
+  const int s = P->step & 1;
+  cudaStream_t st = as_stream(stream);
+  StripJob J = P->J;
+  J.frames = frames;
+  J.frame_stride = frame_stride;
+  J.row_stride = row_stride;
+  J.contiguous = row_stride == 3LL * J.p.width ? 1 : 0;
+  J.out_x = P->xs[s];
+  J.out_y = P->ys[s];
+  J.out_score = P->sc[s];
+  // the fit two steps ago has finished reading this set
+  if (P->used[s] && cudaStreamWaitEvent(st, P->ev_free[s], 0) != cudaSuccess) return ECA_ERR_CUDA;
+  int rc = launch_bounds(J, P->ws[s], st, /*overlap=*/true, /*share=*/true);
+  if (rc) return rc;
+  if (cudaEventRecord(P->ev_bounds[s], st) != cudaSuccess ||
+      cudaStreamWaitEvent(P->side, P->ev_bounds[s], 0) != cudaSuccess)
+    return ECA_ERR_CUDA;
+  rc = launch_rescore(J, P->ws[s], P->side);
+  if (rc) return rc;
+  const FitJob F{P->xs[s], P->ys[s], P->sc[s], 2 * P->n_strips, 0, J.p, P->trip, P->rec[s]};
+  rc = launch_fit(F, P->batch, P->side);
+  if (rc) return rc;
+  if (cudaEventRecord(P->ev_free[s], P->side) != cudaSuccess) return ECA_ERR_CUDA;
+  P->used[s] = true;
+  P->last = s;
+  ++P->step;
+  *out_records = P->rec[s];
+  return ECA_OK;
+}
+
+extern "C" int eca_pipeline_fence(EcaPipeline* P, void* stream) {
+  if (!P) return ECA_ERR_ARG;
+  if (P->last < 0) return ECA_OK;
+  return cudaStreamWaitEvent(as_stream(stream), P->ev_free[P->last], 0) == cudaSuccess
+             ? ECA_OK
+             : ECA_ERR_CUDA;
+}
+
+extern "C" int eca_pipeline_side_stream(EcaPipeline* P, void** out_stream) {
+  if (!P || !out_stream) return ECA_ERR_ARG;
+  *out_stream = reinterpret_cast<void*>(P->side);
+  return ECA_OK;
+}
+
+extern "C" int eca_pipeline_destroy(EcaPipeline* P) {
+  if (!P) return ECA_OK;
+  cudaStreamSynchronize(P->side);
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(P->ev_bounds[k]);
+    cudaEventDestroy(P->ev_free[k]);
+  }
+  cudaStreamDestroy(P->side);
+  delete P;
+  return ECA_OK;
+}
 
 #ifdef ECA_WARP_TIMES
 extern "C" int eca_debug_warp_times(uint64_t* out, int n) {

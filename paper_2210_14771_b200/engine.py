@@ -57,10 +57,6 @@ class ContentAreaEngine:
             self.w_dev, self.norm = api._dev_net(variant.net, d)
         self.graph = None
         self._pipe = None
-        # consecutive run_pipelined() bounds launches touch different buffer
-        # sets: let each start while the previous one drains, and leave room
-        # on every SM for the side stream's rescore + fit
-        self.pipeline_flags = _lib.BOUNDS_OVERLAP_PREVIOUS | _lib.BOUNDS_SHARE_SMS
         # Small batches (latency): one fused launch whose last strip CTA per
         # frame runs the fit.  Large batches (throughput): bound-and-prune
         # kernel, FP64 rescore of the survivors, then a fit kernel (one warp
@@ -128,15 +124,36 @@ class ContentAreaEngine:
 
     # ------------------------------------------------------------ pipeline
     def _pipeline(self):
+        """The native streamed pipeline (eca_pipeline_*), created on first use."""
         if self._pipe is None:
-            sets = []
-            for _ in range(2):
-                sets.append({"ws": torch.zeros_like(self.workspace), "xs": torch.empty_like(self.xs),
-                             "ys": torch.empty_like(self.ys), "sc": torch.empty_like(self.sc),
-                             "rec": torch.empty_like(self.rec), "bounds": torch.cuda.Event(),
-                             "free": torch.cuda.Event()})
-            self._pipe = {"sets": sets, "side": torch.cuda.Stream(self.device), "i": 0, "done": None}
+            lib = _lib.load()
+            n = ctypes.c_int64()
+            _lib.check(lib.eca_pipeline_bytes(self.batch, self.n_strips, ctypes.byref(n)),
+                       "eca_pipeline_bytes")
+            scratch = torch.empty(n.value, dtype=torch.uint8, device=self.device)
+            handle = ctypes.c_void_p()
+            torch.cuda.synchronize(self.device)
+            _lib.check(lib.eca_pipeline_create(self.batch, self.height, self.width, self._rows,
+                                               self.n_strips, ctypes.byref(self.params),
+                                               api._ptr(self.trip), api._ptr(scratch), n.value,
+                                               ctypes.byref(handle)), "eca_pipeline_create")
+            side = ctypes.c_void_p()
+            _lib.check(lib.eca_pipeline_side_stream(handle, ctypes.byref(side)), "eca_pipeline_side_stream")
+            self._pipe = {"handle": handle, "scratch": scratch, "base": scratch.data_ptr(), "views": {},
+                          "side": torch.cuda.ExternalStream(side.value, device=self.device),
+                          "out": ctypes.c_void_p(), "step": lib.eca_pipeline_step}
         return self._pipe
+
+    def _release_pipeline(self):
+        if self._pipe is not None:
+            _lib.load().eca_pipeline_destroy(self._pipe["handle"])
+            self._pipe = None
+
+    def __del__(self):
+        try:
+            self._release_pipeline()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
 
     @property
     def side_stream(self) -> torch.cuda.Stream:
@@ -144,48 +161,38 @@ class ContentAreaEngine:
         return self._pipeline()["side"]
 
     def run_pipelined(self, frames: torch.Tensor) -> torch.Tensor:
-        """Throughput mode for a stream of batches: the bound-and-prune kernel
-        of this batch runs on the current stream, its FP64 rescore and the fit
-        on a side stream, where they overlap the NEXT call's bound-and-prune.
-        Two buffer sets alternate; the returned (B,5) records are complete once
-        ``fence()`` has made the reading stream wait, and are overwritten two
-        calls later.  Same records as run() (tests/test_gpu_parity.py)."""
+        """Throughput mode for a stream of batches, one native call per batch
+        (eca_pipeline_step): the bound-and-prune kernel of this batch runs on
+        the current stream, its FP64 rescore and the fit on a side stream,
+        where they overlap the NEXT call's bound-and-prune.  Two buffer sets
+        alternate; the returned (B,5) records are complete once ``fence()`` has
+        made the reading stream wait, and are overwritten two calls later.
+        Same records as run() (tests/test_gpu_parity.py)."""
         if isinstance(self.variant, api.Learned) or self.fused:
             return self.run(frames)
         f = self._check_frames(frames)
         if f.device != self.device:
             raise ValueError(f"frames must live on {self.device}")
         p = self._pipeline()
-        b = p["sets"][p["i"] & 1]
-        p["i"] += 1
-        lib = _lib.load()
-        cur = torch.cuda.current_stream(self.device)
-        cur.wait_event(b["free"])           # the fit two calls ago has read this set
-        s = self.n_strips
-        _lib.check(lib.eca_bounds_handcrafted(
-            ctypes.c_void_p(f.data_ptr()), self.batch, f.stride(0), f.stride(1), self._rows, None, s,
-            ctypes.byref(self.params), api._ptr(b["xs"]), api._ptr(b["ys"]), api._ptr(b["sc"]),
-            api._ptr(b["ws"]), self.pipeline_flags, ctypes.c_void_p(cur.cuda_stream)),
-            "eca_bounds_handcrafted")
-        b["bounds"].record(cur)
-        side = p["side"]
-        side.wait_event(b["bounds"])
-        st = ctypes.c_void_p(side.cuda_stream)
-        _lib.check(lib.eca_rescore_handcrafted(
-            self.batch, self._rows, s, ctypes.byref(self.params), api._ptr(b["xs"]), api._ptr(b["ys"]),
-            api._ptr(b["sc"]), api._ptr(b["ws"]), st), "eca_rescore_handcrafted")
-        _lib.check(lib.eca_fit(api._ptr(b["xs"]), api._ptr(b["ys"]), api._ptr(b["sc"]), self.batch, 2 * s,
-                               ctypes.byref(self.params), api._ptr(self.trip), 0, api._ptr(b["rec"]), st),
-                   "eca_fit")
-        b["free"].record(side)
-        p["done"] = b["free"]
-        return b["rec"]
+        out = p["out"]
+        _lib.check(p["step"](p["handle"], ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1),
+                             ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
+                             ctypes.byref(out)), "eca_pipeline_step")
+        rec = p["views"].get(out.value)
+        if rec is None:   # a view of this buffer set's records inside the scratch
+            off = out.value - p["base"]
+            rec = p["scratch"][off:off + self.batch * 40].view(torch.float64).view(self.batch, 5)
+            p["views"][out.value] = rec
+        return rec
 
     def fence(self, stream: torch.cuda.Stream | None = None) -> None:
         """Make ``stream`` (default: current) wait for every run_pipelined() so far."""
+        if self._pipe is None:
+            return
         stream = stream or torch.cuda.current_stream(self.device)
-        if self._pipe is not None and self._pipe["done"] is not None:
-            stream.wait_event(self._pipe["done"])
+        _lib.check(_lib.load().eca_pipeline_fence(self._pipe["handle"],
+                                                  ctypes.c_void_p(stream.cuda_stream)),
+                   "eca_pipeline_fence")
 
     def bounds(self, frames: torch.Tensor) -> None:
         """Only the bound-and-prune kernel (the step's dominant kernel; its

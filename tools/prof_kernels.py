@@ -22,10 +22,6 @@ def fit(i):
 def fused(i):
     f = frames(i)
     _lib.check(lib.eca_estimate_handcrafted(api._ptr(f), B, f.stride(0), f.stride(1), eng._rows, None, S, ctypes.byref(eng.params), api._ptr(eng.trip), api._ptr(eng.counters), api._ptr(eng.xs), api._ptr(eng.ys), api._ptr(eng.sc), api._ptr(eng.rec), st), "fused")
-def pipe_nopdl(i):
-    eng.pipeline_flags = _lib.BOUNDS_SHARE_SMS
-    eng.run_pipelined(frames(i))
-    eng.pipeline_flags = _lib.BOUNDS_OVERLAP_PREVIOUS | _lib.BOUNDS_SHARE_SMS
 def timeit(fn, n=50):
     for i in range(5): fn(i)
     torch.cuda.synchronize()
@@ -35,6 +31,6 @@ def timeit(fn, n=50):
     eng.fence()
     b.record(); torch.cuda.synchronize()
     return a.elapsed_time(b) / n
-for name, fn in [("points(2-stage)", points), ("points(1-kernel)", lambda i: points(i, False)), ("fit", fit), ("fused", fused), ("engine.run", lambda i: eng.run(frames(i))), ("run_pipelined", lambda i: eng.run_pipelined(frames(i))), ("pipelined noPDL", pipe_nopdl)]:
+for name, fn in [("points(2-stage)", points), ("points(1-kernel)", lambda i: points(i, False)), ("fit", fit), ("fused", fused), ("engine.run", lambda i: eng.run(frames(i))), ("run_pipelined", lambda i: eng.run_pipelined(frames(i)))]:
     ms = timeit(fn)
     print(f"{name:18s} B={B} {ms*1e3:9.1f} us  {ms*1e3/B:7.3f} us/frame  {70778880*B/256/(ms/1e3)/1e9:8.1f} GB/s(strip bytes)", flush=True)
