@@ -130,6 +130,12 @@ int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_strid
 #define ECA_BOUNDS_SHARE_SMS 2         /* flags: leave one CTA slot per SM free for
    kernels running concurrently on other streams (e.g. the previous batch's
    eca_rescore_handcrafted + eca_fit) */
+#define ECA_BOUNDS_ZERO_COPY 4         /* flags: fetch each half strip row chunk by
+   chunk (256 columns), only as far as the scan gets (the exact early exit stops
+   most rows well before the centre).  For `frames` in pinned host memory
+   (mapped, e.g. cudaHostAlloc / torch pin_memory) this reads the strip rows
+   straight over PCIe and only the visited columns cross it; the workspace's
+   third int32 (offset 8) accumulates the 16-byte units fetched. */
 int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                            int64_t row_stride, const int32_t* strip_rows,
                            const int32_t* band_rows, int n_strips,

@@ -225,6 +225,7 @@ PointsJob points_job(const StripJob& J, void* workspace) {
   const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
   PointsJob PJ;
   PJ.J = J;
+  PJ.chunked = 0;
   {   // the table depends only on angle_scale: cached per host thread
     thread_local double cached_scale = -1.0;
     thread_local float2 cached[kABins + 1];
@@ -252,13 +253,15 @@ PointsJob points_job(const StripJob& J, void* workspace) {
 }
 
 int launch_bounds(const StripJob& J, void* workspace, cudaStream_t stream, bool overlap = false,
-                  bool share = false) {
+                  bool share = false, bool chunked = false) {
   if (J.batch == 0) return ECA_OK;
   static const int ns = [] {
     const char* v = std::getenv("ECA_WSTAGES");
     return v ? std::atoi(v) : 1;
   }();
-  const PointsJob PJ = points_job(J, workspace);
+  PointsJob PJ = points_job(J, workspace);
+  PJ.chunked = chunked ? 1 : 0;
+  if (chunked) return launch_points_t<1>(PJ, stream, overlap, share);   // one stage, chunk by chunk
   return ns == 2 ? launch_points_t<2>(PJ, stream, overlap, share)
                  : launch_points_t<1>(PJ, stream, overlap, share);
 }
@@ -345,7 +348,8 @@ extern "C" int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t 
                                       const EcaParams* params, int32_t* out_x, int32_t* out_y,
                                       double* out_score, void* workspace, int flags,
                                       void* stream) {
-  if (flags & ~(ECA_BOUNDS_OVERLAP_PREVIOUS | ECA_BOUNDS_SHARE_SMS)) return ECA_ERR_ARG;
+  if (flags & ~(ECA_BOUNDS_OVERLAP_PREVIOUS | ECA_BOUNDS_SHARE_SMS | ECA_BOUNDS_ZERO_COPY))
+    return ECA_ERR_ARG;
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
                              n_strips, params);
@@ -355,7 +359,7 @@ extern "C" int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t 
   J.out_y = out_y;
   J.out_score = out_score;
   return launch_bounds(J, workspace, as_stream(stream), (flags & ECA_BOUNDS_OVERLAP_PREVIOUS) != 0,
-                       (flags & ECA_BOUNDS_SHARE_SMS) != 0);
+                       (flags & ECA_BOUNDS_SHARE_SMS) != 0, (flags & ECA_BOUNDS_ZERO_COPY) != 0);
 }
 
 extern "C" int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,

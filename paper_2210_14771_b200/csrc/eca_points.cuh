@@ -63,7 +63,9 @@ struct PointsJob {
   StripJob J;          // geometry, params, candidate outputs
   SurvSlot* slots;     // [n_halfrows][kSlots]
   int32_t* counts;     // [n_halfrows]: survivors, or -1 when resolved in bounds_kernel
-  int32_t* ticket;     // [0] next item, [1] warps done; zero between launches
+  int32_t* ticket;     // [0] next item, [1] warps done (zero between launches);
+                       // [2] 16-byte units fetched in zero-copy mode (diagnostic)
+  int chunked;         // zero-copy mode: fetch scan chunks on demand (NS == 1)
   // host-computed constants (launch_points_t): no FP64 division, atan2f or
   // integer division in the kernel prologue / item decode
   float2 atab[kABins + 1];   // A bounds per pseudo-angle bin (see eca_strip.cuh)
@@ -79,12 +81,18 @@ ECA_DEV void decode_item(const PointsJob& PJ, int fs, int& frame, int& strip) {
   strip = fs - frame * S;
 }
 
-// first TMA copies of a half-row item (lane 0)
+// first TMA copies of a half-row item (lane 0): the whole half, or in
+// zero-copy mode its first scan chunk
 ECA_DEV void issue_item_half(const PointsJob& PJ, int item, uint8_t* stage, uint64_t* bar,
                              uint64_t pol, int split) {
   int frame, strip;
   decode_item(PJ, item >> 1, frame, strip);
-  issue_half(PJ.J, item & 1, frame, strip, stage, bar, pol, split);
+  if (PJ.chunked) {
+    const uint32_t b = issue_chunk(PJ.J, item & 1, frame, strip, 0, stage, bar, pol, split);
+    atomicAdd(PJ.ticket + 2, int(b >> 4));
+  } else {
+    issue_half(PJ.J, item & 1, frame, strip, stage, bar, pol, split);
+  }
 }
 
 // RGB sums of the 10 pixels x0-1 .. x0+8 of one staged row; B = smem byte of
@@ -228,6 +236,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     const bool al = (((rb[0] + 3 * xa0) | (rb[1] + 3 * xa0) | (rb[2] + 3 * xa0)) & 7) == 0;
     const int nch = (hw + kWChunk - 1) / kWChunk;
     mbar_wait(&bars[stage], phase);
+    uint32_t cpar = phase ^ 1u;   // zero-copy mode: parity of the next chunk's copy
 #if ECA_LOAD_ONLY   // diagnostic: the TMA ring alone
     if (lane == 0) PJ.counts[item] = 0;
 #else
@@ -376,6 +385,14 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     int nch_eff = nch;
 #pragma unroll 1
     for (int k = 0; k < nch; ++k) {
+      if (PJ.chunked && k > 0) {   // zero-copy: fetch this chunk only now
+        if (lane == 0) {
+          const uint32_t b = issue_chunk(J, half, frame, strip, k, st, &bars[stage], pol, split);
+          atomicAdd(PJ.ticket + 2, int(b >> 4));
+        }
+        mbar_wait(&bars[stage], cpar);
+        cpar ^= 1u;
+      }
       const int xa = xa_of(k, lane);
       int s0[10], s1[10], s2[10];
       load10(st, rb[0] + 3 * xa, al, s0);
@@ -599,6 +616,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
       if (rec > g_warp_times[3 * gw + 2]) g_warp_times[3 * gw + 2] = rec;
     }
 #endif
+    if (PJ.chunked) phase = cpar ^ 1u;   // (flipped back to cpar below, NS == 1)
     __syncwarp();
     if (lane == 0) {
       // the ticket is taken only now: a warp never holds work it cannot start

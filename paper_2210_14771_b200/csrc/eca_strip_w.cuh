@@ -119,4 +119,44 @@ ECA_DEV void issue_half(const StripJob& J, int half, int frame, int strip, uint8
     bulk_g2s(stage + r * J.rowcap, reinterpret_cast<const void*>(starts[r]), sizes[r], bar, pol);
 }
 
+// Zero-copy mode: issue only scan-order chunk k (kWChunk columns plus one
+// neighbour column on each side, 3 rows) of a half strip row into the same
+// stage positions issue_half would fill (lane 0).  Returns the bytes copied.
+ECA_DEV uint32_t issue_chunk(const StripJob& J, int half, int frame, int strip, int k,
+                             uint8_t* stage, uint64_t* bar, uint64_t pol, int split) {
+  const int W = J.p.width;
+  const int xs = half ? split - 1 : 0;          // first staged column
+  const int xe = half ? W : min(split + 1, W);  // one past the last staged column
+  int x_lo, x_hi;                               // inclusive column range of the chunk
+  if (half) {
+    x_hi = W - 1 - kWChunk * k + 1;
+    x_lo = W - 1 - kWChunk * k - kWChunk;
+  } else {
+    x_lo = kWChunk * k - 1;
+    x_hi = kWChunk * k + kWChunk;
+  }
+  x_lo = max(x_lo, xs);
+  x_hi = min(x_hi, xe - 1);
+  const uint8_t* row0 = J.frames + int64_t(frame) * J.frame_stride +
+                        int64_t(J.band[strip]) * J.row_stride + 3 * xs;
+  uintptr_t src[3];
+  uint32_t dst[3], sizes[3], total = 0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(row0 + r * J.row_stride);
+    const uintptr_t base = a & ~uintptr_t(15);   // = issue_half's copy start of this row
+    const uintptr_t lo = (a + 3 * (x_lo - xs)) & ~uintptr_t(15);
+    const uintptr_t hi = (a + 3 * (x_hi - xs) + 3 + 15) & ~uintptr_t(15);
+    src[r] = lo;
+    dst[r] = uint32_t(r * J.rowcap + (lo - base));
+    sizes[r] = uint32_t(hi - lo);
+    total += sizes[r];
+  }
+  mbar_arrive_expect_tx(bar, total);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    bulk_g2s(stage + dst[r], reinterpret_cast<const void*>(src[r]), sizes[r], bar, pol);
+  return total;
+}
+
 }  // namespace eca

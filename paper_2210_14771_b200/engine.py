@@ -242,6 +242,41 @@ class ContentAreaEngine:
         torch.cuda.current_stream(self.device).synchronize()
         return self.rec_host
 
+    def run_host_zero_copy(self, host_frames: torch.Tensor) -> torch.Tensor:
+        """Pinned host frames -> pinned host records (synchronises the stream),
+        without copying the frames: the bound-and-prune kernel reads the
+        strip rows straight from pinned host memory over PCIe, scan chunk by
+        scan chunk (ECA_BOUNDS_ZERO_COPY), so only the columns it visits cross
+        the bus.  Handcrafted variant; same records as run()."""
+        a = host_frames
+        if not isinstance(a, torch.Tensor) or a.is_cuda or not a.is_pinned():
+            raise ValueError("run_host_zero_copy takes a pinned host tensor")
+        if tuple(a.shape) != (self.batch, self.height, self.width, 3) or a.dtype != torch.uint8 \
+                or a.stride(3) != 1 or a.stride(2) != 3:
+            raise ValueError("host frames must be (B,H,W,3) uint8 with packed pixels")
+        if isinstance(self.variant, api.Learned):
+            raise ValueError("zero-copy ingest is implemented for the handcrafted variant")
+        lib = _lib.load()
+        st = api._stream(self.device)
+        s = self.n_strips
+        _lib.check(lib.eca_bounds_handcrafted(
+            ctypes.c_void_p(a.data_ptr()), self.batch, a.stride(0), a.stride(1), self._rows, None, s,
+            ctypes.byref(self.params), api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc),
+            api._ptr(self.workspace), _lib.BOUNDS_ZERO_COPY, st), "eca_bounds_handcrafted")
+        _lib.check(lib.eca_rescore_handcrafted(
+            self.batch, self._rows, s, ctypes.byref(self.params), api._ptr(self.xs), api._ptr(self.ys),
+            api._ptr(self.sc), api._ptr(self.workspace), st), "eca_rescore_handcrafted")
+        _lib.check(lib.eca_fit(api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), self.batch, 2 * s,
+                               ctypes.byref(self.params), api._ptr(self.trip), 0, api._ptr(self.rec), st),
+                   "eca_fit")
+        self.rec_host.copy_(self.rec, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return self.rec_host
+
+    def zero_copy_bytes(self) -> int:
+        """Bytes fetched over PCIe by run_host_zero_copy() calls so far."""
+        return int(self.workspace[8:12].view(torch.int32).item()) * 16
+
     # --------------------------------------------------------------- graphs
     def capture(self, frames: torch.Tensor) -> None:
         """Capture run(frames) (fixed input pointer) into a CUDA graph."""

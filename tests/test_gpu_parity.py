@@ -224,7 +224,7 @@ def test_split_stages_match_points():
     assert lib.eca_bounds_handcrafted(
         ctypes.c_void_p(frames.data_ptr()), len(frames), frames.stride(0), frames.stride(1), eng._rows,
         None, eng.n_strips, ctypes.byref(eng.params), api._ptr(xs), api._ptr(ys), api._ptr(sc),
-        api._ptr(eng.workspace), 4, st) == _lib.ECA_ERR_ARG
+        api._ptr(eng.workspace), 8, st) == _lib.ECA_ERR_ARG
 
 
 @pytest.mark.parametrize("w,h,pad", [(333, 241, 7), (517, 300, 1), (1001, 480, 13), (2049, 200, 5),
@@ -254,6 +254,38 @@ def test_points_odd_sizes_and_strides(w, h, pad):
         ox, oy, osc = want[k][0], want[k][1], want[k][2]
         keep = orc.keep_mask(ox, oy, osc, w, h, cfg)
         assert_fit_equal(fit, orc.ransac(ox[keep], oy[keep], osc[keep], w, h, cfg, 0), k)
+
+
+def test_zero_copy_host_frames_match_run():
+    """ECA_BOUNDS_ZERO_COPY: the bound-and-prune kernel reads pinned host
+    frames chunk by chunk over PCIe; records equal the device-resident path,
+    and fewer bytes than the strip rows cross the bus."""
+    specs = synth.bench_specs(20, 1920, 1080, seed=2024)
+    frames = np.stack([synth.render(s, 30000 + k) for k, (_, s) in enumerate(specs)])
+    eng = eb.ContentAreaEngine(1080, 1920, len(frames))
+    want = eng.run(torch.from_numpy(frames).cuda()).clone()
+    host = torch.from_numpy(frames).pin_memory()
+    b0 = eng.zero_copy_bytes()
+    got = eng.run_host_zero_copy(host).clone()
+    assert torch.equal(got, want.cpu())
+    moved = eng.zero_copy_bytes() - b0
+    strip_bytes = len(frames) * eng.n_strips * 3 * 1920 * 3
+    assert 0 < moved < strip_bytes
+    # device frames through the same chunked loads (ECA_BOUNDS_ZERO_COPY on HBM)
+    import ctypes
+    from paper_2210_14771_b200 import _lib, api
+    f = torch.from_numpy(frames).cuda()
+    lib = _lib.load()
+    _lib.check(lib.eca_bounds_handcrafted(
+        ctypes.c_void_p(f.data_ptr()), len(frames), f.stride(0), f.stride(1), eng._rows, None,
+        eng.n_strips, ctypes.byref(eng.params), api._ptr(eng.xs), api._ptr(eng.ys), api._ptr(eng.sc),
+        api._ptr(eng.workspace), _lib.BOUNDS_ZERO_COPY, api._stream(eng.device)), "bounds")
+    _lib.check(lib.eca_rescore_handcrafted(
+        len(frames), eng._rows, eng.n_strips, ctypes.byref(eng.params), api._ptr(eng.xs),
+        api._ptr(eng.ys), api._ptr(eng.sc), api._ptr(eng.workspace), api._stream(eng.device)), "rs")
+    xs = eng.xs.clone()
+    eng.points(f)
+    assert torch.equal(xs, eng.xs)
 
 
 def test_graph_replay_matches_direct():

@@ -4,6 +4,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tma_ring_bench tools/tma_ring_bench.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t sa(const void* p) {
@@ -84,7 +85,46 @@ __global__ void ring(const uint8_t* src, int64_t item_bytes, int copies, int n_i
   if (acc == 0xdeadbeef) *sink = acc;
 }
 
-int main() {
+int host_mode(int sms) {
+  // 1-D bulk copies whose SOURCE is mapped pinned host memory (zero-copy over PCIe)
+  const int64_t total = int64_t(256) << 20;
+  uint8_t* h = nullptr;
+  if (cudaHostAlloc(&h, total, cudaHostAllocMapped) != cudaSuccess) { printf("hostalloc failed\n"); return 1; }
+  memset(h, 1, total);
+  uint8_t* d = nullptr;
+  cudaHostGetDevicePointer(&d, h, 0);
+  int* ticket; cudaMalloc(&ticket, 4);
+  unsigned long long* sink; cudaMalloc(&sink, 8);
+  for (int item : {2304, 8832, 32768}) {
+    for (int ns : {1, 2, 4}) {
+      const int warps = 2, n_items = int(total / item), stage = (item + 127) / 128 * 128;
+      const size_t smem = size_t(warps) * (ns * stage + 128);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ring, 32 * warps, smem);
+      if (per_sm < 1) continue;
+      cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+      float best = 1e9;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(a);
+        ring<<<sms * per_sm, 32 * warps, smem>>>(d, item, 1, n_items, ns, stage, 0, ticket, sink);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+      }
+      printf("HOST-mapped source: item %6d B stages %d (%2d warps/SM): %6.1f GB/s  (%s)\n", item, ns,
+             per_sm * warps, double(n_items) * item / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  cudaFreeHost(h);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaFuncSetAttribute(ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    return host_mode(sms);
+  }
   const int64_t total = int64_t(2048) * 1080 * 5760;   // 2048 1080p frames (12.7 GB)
   uint8_t* buf;
   if (cudaMalloc(&buf, total + (1 << 20)) != cudaSuccess) { printf("alloc failed\n"); return 1; }
