@@ -111,9 +111,9 @@ int64_t points_workspace(int batch, int n_strips) {
   return 256 + ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)) + n_hr * 4;
 }
 
-template <int NS>
+template <int NS, bool kChunked>
 int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share) {
-  auto kern = bounds_kernel<NS>;
+  auto kern = bounds_kernel<NS, kChunked>;
   StripJob& J = PJ.J;
   const int W = J.p.width;
   const int split = (W + 1) / 2;
@@ -261,9 +261,9 @@ int launch_bounds(const StripJob& J, void* workspace, cudaStream_t stream, bool 
   }();
   PointsJob PJ = points_job(J, workspace);
   PJ.chunked = chunked ? 1 : 0;
-  if (chunked) return launch_points_t<1>(PJ, stream, overlap, share);   // one stage, chunk by chunk
-  return ns == 2 ? launch_points_t<2>(PJ, stream, overlap, share)
-                 : launch_points_t<1>(PJ, stream, overlap, share);
+  if (chunked) return launch_points_t<1, true>(PJ, stream, overlap, share);   // one stage
+  return ns == 2 ? launch_points_t<2, false>(PJ, stream, overlap, share)
+                 : launch_points_t<1, false>(PJ, stream, overlap, share);
 }
 
 // one warp per CTA (4 half rows): small CTAs slot in beside a running

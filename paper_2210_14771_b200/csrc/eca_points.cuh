@@ -83,11 +83,12 @@ ECA_DEV void decode_item(const PointsJob& PJ, int fs, int& frame, int& strip) {
 
 // first TMA copies of a half-row item (lane 0): the whole half, or in
 // zero-copy mode its first scan chunk
+template <bool kChunked>
 ECA_DEV void issue_item_half(const PointsJob& PJ, int item, uint8_t* stage, uint64_t* bar,
                              uint64_t pol, int split) {
   int frame, strip;
   decode_item(PJ, item >> 1, frame, strip);
-  if (PJ.chunked) {
+  if (kChunked) {
     const uint32_t b = issue_chunk(PJ.J, item & 1, frame, strip, 0, stage, bar, pol, split);
     atomicAdd(PJ.ticket + 2, int(b >> 4));
   } else {
@@ -129,7 +130,6 @@ struct ColEval {
   bool flat;   // numpy's gx and gy are exactly 0.0 (score exactly 0)
 };
 
-template <int NS>
 #ifndef ECA_BOUNDS_MAXREG   // 96: 5 warps per SM sub-partition (120 would allow 4)
 #define ECA_BOUNDS_MAXREG 96
 #endif
@@ -139,6 +139,9 @@ template <int NS>
 #ifndef ECA_EARLY_EXIT
 #define ECA_EARLY_EXIT 1
 #endif
+// kChunked: zero-copy mode (ECA_BOUNDS_ZERO_COPY), a separate instantiation so
+// the device-resident kernel carries none of its code
+template <int NS, bool kChunked>
 __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_constant__ PointsJob PJ) {
   const StripJob& J = PJ.J;
   // a dependent launch (the next batch, ECA_BOUNDS_OVERLAP_PREVIOUS) may start
@@ -180,7 +183,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     for (int s = 0; s < NS; ++s) {
       const int it = next_item();
       qitem[s] = it;
-      if (it < n_items) issue_item_half(PJ, it, mine + s * WL.stage, &bars[s], pol, split);
+      if (it < n_items) issue_item_half<kChunked>(PJ, it, mine + s * WL.stage, &bars[s], pol, split);
     }
   }
   __syncthreads();
@@ -385,7 +388,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     int nch_eff = nch;
 #pragma unroll 1
     for (int k = 0; k < nch; ++k) {
-      if (PJ.chunked && k > 0) {   // zero-copy: fetch this chunk only now
+      if (kChunked && k > 0) {   // zero-copy: fetch this chunk only now
         if (lane == 0) {
           const uint32_t b = issue_chunk(J, half, frame, strip, k, st, &bars[stage], pol, split);
           atomicAdd(PJ.ticket + 2, int(b >> 4));
@@ -616,14 +619,14 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
       if (rec > g_warp_times[3 * gw + 2]) g_warp_times[3 * gw + 2] = rec;
     }
 #endif
-    if (PJ.chunked) phase = cpar ^ 1u;   // (flipped back to cpar below, NS == 1)
+    if (kChunked) phase = cpar ^ 1u;   // (flipped back to cpar below, NS == 1)
     __syncwarp();
     if (lane == 0) {
       // the ticket is taken only now: a warp never holds work it cannot start
       // (prefetching it measured 30% slower from the end-of-kernel imbalance)
       const int nxt = next_item();
       qitem[stage] = nxt;
-      if (nxt < n_items) issue_item_half(PJ, nxt, st, &bars[stage], pol, split);
+      if (nxt < n_items) issue_item_half<kChunked>(PJ, nxt, st, &bars[stage], pol, split);
     }
     __syncwarp();
     if (++stage == NS) {
