@@ -50,12 +50,15 @@ def main():
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"{len(v):6d} launches  {sum(v):12.1f} us total  {sum(v)/len(v):10.2f} us mean  "
                      f"{100*sum(v)/total:5.1f}%  {k}")
-    step = {k: v for k, v in agg.items() if any(n in k for n in STEP_KERNELS)}
+    # the throughput step's kernels (bounds_kernel<1, 1> is the zero-copy e2e leg)
+    step = {k: v for k, v in agg.items()
+            if any(n in k for n in STEP_KERNELS) and "bounds_kernel<1, 1>" not in k}
     if step:
         per = {k: sum(v) / len(v) for k, v in step.items()}
         tot_step = sum(per.values())
         lines += ["", "# shares of one throughput step (mean launch time of each step kernel; the",
-                  "# fused strip_kernel launches above are the single-frame latency leg)"]
+                  "# fused strip_kernel launches are the single-frame latency leg, bounds_kernel<1, 1>",
+                  "# the zero-copy e2e leg, cnn/select the learned leg)"]
         for k, v in sorted(per.items(), key=lambda kv: -kv[1]):
             lines.append(f"{v:10.2f} us mean  {100 * v / tot_step:5.1f}% of step  {k}")
     (PROF / f"{rnd}_launches.txt").write_text("\n".join(lines) + "\n")
@@ -87,8 +90,8 @@ def main():
     out.append("")
     out.append("warp stall samples: " + ", ".join(
         f"{k} {100*v/tot:.0f}%" for k, v in sorted(st.items(), key=lambda kv: -kv[1]) if v / tot >= 0.02))
-    short = "strip" if "strip_kernel" in name else name.split("(")[0].split()[-1].replace("::", "_")
-    short = short.split("<")[0]
+    base = name.split("<")[0].split("(")[0].split()[-1]   # drop "void", template args, params
+    short = "strip" if "strip_kernel" in name else base.split("::")[-1]
     (PROF / f"{rnd}_{short}_ncu.txt").write_text("\n".join(out) + "\n")
 
     def num(h):
