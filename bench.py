@@ -305,10 +305,11 @@ def run_ours(args) -> None:
     h2d_copy = BATCH * eng.n_strips * 3 * WIDTH * 3
     d2h = BATCH * 40
 
-    lat = learned = None
+    lat = learned = mask = None
     if rank == 0:
         lat = latency(eb, dev)
         learned = learned_leg(eb, dev, pool, n_slots, peaks)
+        mask = mask_leg(eb, dev, eng, pool, peaks)
 
     out = None
     if rank == 0:
@@ -349,6 +350,7 @@ def run_ours(args) -> None:
                                               "strip row, then the device-resident kernels"}},
             "latency_ms": lat,
             "learned": learned,
+            "mask": mask,
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * eng.launches_per_run,
             "cpu_baseline": cpu,
@@ -396,6 +398,45 @@ def learned_leg(eb, dev, pool, n_slots, peaks) -> dict:
                          "kernel": "cnn_kernel (SIMT FP32 this round; step time incl. select + fit)",
                          "algorithmic_flop_per_frame": CNN_FLOP_PER_FRAME,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (measured)"}}
+
+
+def mask_leg(eb, dev, eng, pool, peaks) -> dict:
+    """draw_mask (K4) for the 256 records of one step: H*W bytes written per
+    frame, event-timed; HBM-write bound."""
+    import ctypes
+    import torch
+    from paper_2210_14771_b200 import _lib, api
+    rec = eng.run(pool[:BATCH]).clone()
+    out = torch.empty((BATCH, HEIGHT, WIDTH), dtype=torch.uint8, device=dev)
+    lib = _lib.load()
+    st = api._stream(dev)
+
+    def launch():
+        _lib.check(lib.eca_draw_mask(api._ptr(rec), BATCH, HEIGHT, WIDTH, api._ptr(out), HEIGHT * WIDTH, st),
+                   "eca_draw_mask")
+    for _ in range(3):
+        launch()
+    steps = 20
+    stream = torch.cuda.current_stream(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(steps):
+        launch()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    nbytes = BATCH * HEIGHT * WIDTH
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    accepted = int((eng.status(rec) == 0).sum().item())
+    return {"metric": "draw_mask masks/s (K4, 1080p uint8 masks from one step's records)",
+            "value": round(BATCH / (ms * 1e-3), 1), "unit": "masks/s", "ms_per_launch": round(ms, 5),
+            "accepted_circles": accepted, "frames": BATCH,
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "kernel": "mask_kernel",
+                         "algorithmic_bytes_per_launch": nbytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy: read+write)"}}
 
 
 def latency(eb, dev) -> dict:

@@ -44,43 +44,62 @@ ECA_DEV void row_interval(double cx, double dy2, double r2, int W, int& lo, int&
   }
 }
 
+// 16 mask bytes of columns xb..xb+15 for the inside interval [lo, hi]
+ECA_DEV uint4 mask16(int xb, int lo, int hi) {
+  if (xb >= lo && xb + 15 <= hi) return make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+  if (xb + 15 < lo || xb > hi) return make_uint4(0u, 0u, 0u, 0u);
+  uint32_t w[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int x = xb + q * 4 + k;
+      word |= uint32_t(x >= lo && x <= hi) << (8 * k);
+    }
+    w[q] = word;
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// A warp takes 32 rows at a time: lane i finds row i's interval (the FP64
+// chains run in parallel across lanes), then the warp streams the 32 rows as
+// 16-byte stores; only the <= 2 chunks per row that straddle an interval end
+// are built bytewise.
 __global__ void __launch_bounds__(256) mask_kernel(const EcaFitRecord* fits, int batch, int H,
                                                    int W, uint8_t* out, int64_t fstride) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t n_rows = int64_t(batch) * H;
-  for (int64_t row = warp; row < n_rows; row += (int64_t(gridDim.x) * blockDim.x) >> 5) {
-    const int b = int(row / H);
-    const int y = int(row - int64_t(b) * H);
-    const EcaFitRecord f = fits[b];
+  for (int64_t r0 = warp * 32; r0 < n_rows; r0 += n_warps * 32) {
     int lo = 0, hi = W - 1;
-    if (f.status == ECA_ACCEPTED) {
-      const double dy = sub_rn(double(y), f.cy);
-      row_interval(f.cx, mul_rn(dy, dy), mul_rn(f.r, f.r), W, lo, hi);
-    }
-    uint8_t* dst = out + int64_t(b) * fstride + int64_t(y) * W;
-    // head bytes up to 16-byte alignment, 16-byte body, tail bytes
-    const int head = int((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15);
-    const int h = head < W ? head : W;
-    for (int x = lane; x < h; x += 32) dst[x] = (x >= lo && x <= hi) ? 1 : 0;
-    const int n16 = (W - h) >> 4;
-    uint4* body = reinterpret_cast<uint4*>(dst + h);
-    for (int v = lane; v < n16; v += 32) {
-      const int xb = h + v * 16;
-      uint32_t w[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int x = xb + q * 4 + k;
-          word |= uint32_t(x >= lo && x <= hi) << (8 * k);
-        }
-        w[q] = word;
+    uintptr_t my_dst = 0;   // this lane's row start
+    const int64_t my = r0 + lane;
+    if (my < n_rows) {
+      const int b = int(my / H);
+      const int y = int(my - int64_t(b) * H);
+      my_dst = reinterpret_cast<uintptr_t>(out + int64_t(b) * fstride + int64_t(y) * W);
+      const EcaFitRecord f = fits[b];
+      if (f.status == ECA_ACCEPTED) {
+        const double dy = sub_rn(double(y), f.cy);
+        row_interval(f.cx, mul_rn(dy, dy), mul_rn(f.r, f.r), W, lo, hi);
       }
-      body[v] = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    for (int x = h + n16 * 16 + lane; x < W; x += 32) dst[x] = (x >= lo && x <= hi) ? 1 : 0;
+    const int nr = int(n_rows - r0 < 32 ? n_rows - r0 : 32);
+    for (int i = 0; i < nr; ++i) {
+      const int rlo = __shfl_sync(kFull, lo, i), rhi = __shfl_sync(kFull, hi, i);
+      uint8_t* dst = reinterpret_cast<uint8_t*>(
+          static_cast<uintptr_t>(__shfl_sync(kFull, static_cast<unsigned long long>(my_dst), i)));
+      // head bytes up to 16-byte alignment, 16-byte body, tail bytes
+      const int head = int((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15);
+      const int h = head < W ? head : W;
+      if (lane < h) dst[lane] = (lane >= rlo && lane <= rhi) ? 1 : 0;
+      const int n16 = (W - h) >> 4;
+      uint4* body = reinterpret_cast<uint4*>(dst + h);
+      for (int v = lane; v < n16; v += 32) body[v] = mask16(h + v * 16, rlo, rhi);
+      for (int x = h + n16 * 16 + lane; x < W; x += 32) dst[x] = (x >= rlo && x <= rhi) ? 1 : 0;
+    }
   }
 }
 
@@ -150,8 +169,8 @@ extern "C" int eca_draw_mask(const EcaFitRecord* fits, int batch, int height, in
   if (batch == 0) return ECA_OK;
   if (!fits || !out) return ECA_ERR_ARG;
   const int64_t rows = int64_t(batch) * height;
-  const int64_t blocks64 = (rows + 7) / 8;
-  const int blocks = int(blocks64 < 148 * 64 ? blocks64 : 148 * 64);
+  const int64_t blocks64 = (rows + 255) / 256;   // 8 warps x 32 rows per CTA pass
+  const int blocks = int(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
   mask_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(fits, batch, height,
                                                                           width, out,
                                                                           out_frame_stride);
