@@ -158,9 +158,14 @@ int eca_pipeline_create(int batch, int height, int width, const int32_t* strip_r
                         int n_strips, const EcaParams* params, const int16_t* triplets,
                         void* scratch, int64_t scratch_bytes, EcaPipeline** out);
 /* Enqueue one batch; *out_records = this step's device records (batch x 40 B),
- * complete once a stream has waited via eca_pipeline_fence. */
+ * complete once a stream has waited via eca_pipeline_fence.  flags: 0 or
+ * ECA_BOUNDS_ZERO_COPY (frames in pinned host memory, read over PCIe chunk by
+ * chunk; they must stay unchanged until the step's records are fenced).
+ * host_records (optional, pinned): the records are also copied there on the
+ * side stream after the fit. */
 int eca_pipeline_step(EcaPipeline* pipeline, const uint8_t* frames, int64_t frame_stride,
-                      int64_t row_stride, void* stream, EcaFitRecord** out_records);
+                      int64_t row_stride, int flags, EcaFitRecord* host_records, void* stream,
+                      EcaFitRecord** out_records);
 /* Make `stream` wait for every step enqueued so far. */
 int eca_pipeline_fence(EcaPipeline* pipeline, void* stream);
 /* The side stream (e.g. to gather the records of a step right after its fit). */

@@ -41,7 +41,7 @@ SIGNATURES = {
     "eca_pipeline_bytes": [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)],
     "eca_pipeline_create": [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I32P, ctypes.c_int, _PARAMS, _p,
                             _p, _i64, ctypes.POINTER(ctypes.c_void_p)],
-    "eca_pipeline_step": [_p, _p, _i64, _i64, _p, ctypes.POINTER(ctypes.c_void_p)],
+    "eca_pipeline_step": [_p, _p, _i64, _i64, ctypes.c_int, _p, _p, ctypes.POINTER(ctypes.c_void_p)],
     "eca_pipeline_fence": [_p, _p],
     "eca_pipeline_side_stream": [_p, ctypes.POINTER(ctypes.c_void_p)],
     "eca_pipeline_destroy": [_p],

@@ -574,9 +574,11 @@ extern "C" int eca_pipeline_create(int batch, int height, int width, const int32
 }
 
 extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t frame_stride,
-                                 int64_t row_stride, void* stream, EcaFitRecord** out_records) {
+                                 int64_t row_stride, int flags, EcaFitRecord* host_records,
+                                 void* stream, EcaFitRecord** out_records) {
   if (!P || !frames || !out_records || row_stride < 3LL * P->J.p.width || frame_stride < 0)
     return ECA_ERR_ARG;
+  if (flags & ~ECA_BOUNDS_ZERO_COPY) return ECA_ERR_ARG;
   const int s = P->step & 1;
   cudaStream_t st = as_stream(stream);
   StripJob J = P->J;
@@ -589,7 +591,8 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   J.out_score = P->sc[s];
   // the fit two steps ago has finished reading this set
   if (P->used[s] && cudaStreamWaitEvent(st, P->ev_free[s], 0) != cudaSuccess) return ECA_ERR_CUDA;
-  int rc = launch_bounds(J, P->ws[s], st, /*overlap=*/true, /*share=*/true);
+  int rc = launch_bounds(J, P->ws[s], st, /*overlap=*/true, /*share=*/true,
+                         (flags & ECA_BOUNDS_ZERO_COPY) != 0);
   if (rc) return rc;
   if (cudaEventRecord(P->ev_bounds[s], st) != cudaSuccess ||
       cudaStreamWaitEvent(P->side, P->ev_bounds[s], 0) != cudaSuccess)
@@ -599,6 +602,10 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   const FitJob F{P->xs[s], P->ys[s], P->sc[s], 2 * P->n_strips, 0, J.p, P->trip, P->rec[s]};
   rc = launch_fit(F, P->batch, P->side);
   if (rc) return rc;
+  if (host_records &&   // the records of this step back to the host, in stream order
+      cudaMemcpyAsync(host_records, P->rec[s], sizeof(EcaFitRecord) * size_t(P->batch),
+                      cudaMemcpyDeviceToHost, P->side) != cudaSuccess)
+    return ECA_ERR_CUDA;
   if (cudaEventRecord(P->ev_free[s], P->side) != cudaSuccess) return ECA_ERR_CUDA;
   P->used[s] = true;
   P->last = s;

@@ -175,7 +175,7 @@ class ContentAreaEngine:
             raise ValueError(f"frames must live on {self.device}")
         p = self._pipeline()
         out = p["out"]
-        _lib.check(p["step"](p["handle"], ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1),
+        _lib.check(p["step"](p["handle"], ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1), 0, None,
                              ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
                              ctypes.byref(out)), "eca_pipeline_step")
         rec = p["views"].get(out.value)
@@ -184,6 +184,30 @@ class ContentAreaEngine:
             rec = p["scratch"][off:off + self.batch * 40].view(torch.float64).view(self.batch, 5)
             p["views"][out.value] = rec
         return rec
+
+    def run_host_pipelined(self, host_frames: torch.Tensor, host_records: torch.Tensor) -> None:
+        """Streaming end-to-end mode: pinned host frames in, pinned host
+        records out, no synchronisation.  The bound-and-prune kernel reads the
+        frames over PCIe chunk by chunk (zero-copy) on the current stream; the
+        rescore, the fit and the D2H copy of the records into ``host_records``
+        ((B,5) float64, pinned) run on the side stream, overlapping the next
+        call.  Both buffers must stay untouched until fence() + synchronize."""
+        a = host_frames
+        if not isinstance(a, torch.Tensor) or a.is_cuda or not a.is_pinned():
+            raise ValueError("run_host_pipelined takes a pinned host frame tensor")
+        if tuple(a.shape) != (self.batch, self.height, self.width, 3) or a.dtype != torch.uint8 \
+                or a.stride(3) != 1 or a.stride(2) != 3:
+            raise ValueError("host frames must be (B,H,W,3) uint8 with packed pixels")
+        r = host_records
+        if r.is_cuda or not r.is_pinned() or tuple(r.shape) != (self.batch, 5) or r.dtype != torch.float64:
+            raise ValueError("host_records must be a pinned (B,5) float64 tensor")
+        if isinstance(self.variant, api.Learned) or self.fused:
+            raise ValueError("run_host_pipelined streams the handcrafted variant at batch > 16")
+        p = self._pipeline()
+        _lib.check(p["step"](p["handle"], ctypes.c_void_p(a.data_ptr()), a.stride(0), a.stride(1),
+                             _lib.BOUNDS_ZERO_COPY, ctypes.c_void_p(r.data_ptr()),
+                             ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
+                             ctypes.byref(p["out"])), "eca_pipeline_step")
 
     def fence(self, stream: torch.cuda.Stream | None = None) -> None:
         """Make ``stream`` (default: current) wait for every run_pipelined() so far."""

@@ -288,6 +288,25 @@ def test_zero_copy_host_frames_match_run():
     assert torch.equal(xs, eng.xs)
 
 
+def test_host_pipelined_matches_run_host():
+    """run_host_pipelined (zero-copy reads, records D2H on the side stream,
+    overlapping steps) lands the same records in host memory as run_host."""
+    specs = synth.bench_specs(40, 1920, 1080, seed=2024)
+    frames = np.stack([synth.render(s, 30000 + k) for k, (_, s) in enumerate(specs)])
+    B = 20
+    eng = eb.ContentAreaEngine(1080, 1920, B)
+    hosts = [torch.from_numpy(frames[i * B:(i + 1) * B]).pin_memory() for i in (0, 1)]
+    want = [eng.run_host(h).clone() for h in hosts]
+    recs = [torch.zeros((B, 5), dtype=torch.float64).pin_memory() for _ in range(2)]
+    for i in range(4):
+        eng.run_host_pipelined(hosts[i % 2], recs[i % 2])
+    eng.fence()
+    torch.cuda.synchronize()
+    assert torch.equal(recs[0], want[0]) and torch.equal(recs[1], want[1])
+    with pytest.raises(ValueError):
+        eng.run_host_pipelined(hosts[0].clone(), recs[0])   # not pinned
+
+
 def test_graph_replay_matches_direct():
     frame = synth.c1_frame()
     t = torch.from_numpy(frame).cuda().unsqueeze(0)
