@@ -399,19 +399,25 @@ def learned_leg(eb, dev, pool, n_slots, peaks) -> dict:
     import torch
     from paper_2210_14771_b200.engine import ContentAreaEngine
     net = eb.EdgeNet(eb.ChannelStats([100.0] * 3, [50.0] * 3), seed=0)
-    eng = ContentAreaEngine(HEIGHT, WIDTH, BATCH, variant=eb.Learned(net), device=dev)
     stream = torch.cuda.current_stream(dev)
-    for i in range(3):
-        eng.run(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
     steps = 20
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    a.record(stream)
-    for i in range(steps):
-        eng.run(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
-    b.record(stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / steps
+
+    def step_ms(eng):
+        for i in range(3):
+            eng.run(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for i in range(steps):
+            eng.run(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / steps
+
+    eng = ContentAreaEngine(HEIGHT, WIDTH, BATCH, variant=eb.Learned(net), device=dev)
+    ms = step_ms(eng)
+    ms_tc = step_ms(ContentAreaEngine(HEIGHT, WIDTH, BATCH, variant=eb.Learned(net), device=dev,
+                                      tensor_cores=True))
     tflops = CNN_FLOP_PER_FRAME * BATCH / (ms * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops", 2250.0)
     return {"metric": "learned-variant frames/s (C3: EdgeNet strip CNN + select + fit)",
@@ -419,9 +425,13 @@ def learned_leg(eb, dev, pool, n_slots, peaks) -> dict:
             "steps": steps, "dtype": "f32", "launches_per_step": eng.launches_per_run,
             "roofline": {"bound": "tensor", "achieved": round(tflops, 2), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(tflops / peak, 4),
-                         "kernel": "cnn_kernel (SIMT FP32 this round; step time incl. select + fit)",
+                         "kernel": "cnn_kernel (SIMT FP32; step time incl. select + fit)",
                          "algorithmic_flop_per_frame": CNN_FLOP_PER_FRAME,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (measured)"}}
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (measured)"},
+            "tcgen05_variant": {"value": round(BATCH / (ms_tc * 1e-3), 1), "unit": "frames/s",
+                                "ms_per_step": round(ms_tc, 4),
+                                "kernel": "cnn_kernel_tc: 16->32 conv on tcgen05 kind::tf32 (3xTF32), "
+                                          "layers 0-1 SIMT (ECA_LEARNED_TCGEN05)"}}
 
 
 def mask_leg(eb, dev, eng, pool, peaks) -> dict:

@@ -210,6 +210,17 @@ int eca_points_learned(const uint8_t* frames, int batch, int64_t frame_stride,
                        float* out_probs /* [batch][n_strips][width-6] */,
                        int32_t* out_x, int32_t* out_y, double* out_score, void* stream);
 
+/* Same with flags: ECA_LEARNED_TCGEN05 runs the 16->32-channel layer on the
+ * tensor cores (tcgen05 kind::tf32, 3xTF32 split: FP32-level error).  Default
+ * (0) is the SIMT kernel, faster at this network size (K3). */
+#define ECA_LEARNED_TCGEN05 1
+int eca_points_learned_ex(const uint8_t* frames, int batch, int64_t frame_stride,
+                          int64_t row_stride, const int32_t* strip_rows,
+                          const int32_t* band_rows, int n_strips, int height, int width,
+                          const float* weights, const double* norm, int flags,
+                          float* out_probs, int32_t* out_x, int32_t* out_y, double* out_score,
+                          void* stream);
+
 /* -------------------------------------------------------- mask / crop ---- */
 
 /* Vectorised circle_contains (geometry.py:30-34): out[b][y][x] = 1 inside the

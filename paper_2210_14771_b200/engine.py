@@ -25,12 +25,15 @@ class ContentAreaEngine:
     """
 
     def __init__(self, height: int, width: int, batch: int, cfg: EcaConfig | None = None,
-                 seed: int = 0, variant: api.EstimatorVariant = api.HANDCRAFTED, device=None):
+                 seed: int = 0, variant: api.EstimatorVariant = api.HANDCRAFTED, device=None,
+                 tensor_cores: bool = False):
         self.cfg = cfg or config_default()
         self.height, self.width, self.batch = height, width, batch
         self.device = api._device(device)
         self.variant = variant
         self.seed = seed
+        # learned variant: ECA_LEARNED_TCGEN05 puts the 16->32 conv on tcgen05
+        self.cnn_flags = _lib.LEARNED_TCGEN05 if tensor_cores else 0
         self.rows = api.strip_heights(height, self.cfg.strip_count, self.cfg.strip_weighting)
         s = self.n_strips = len(self.rows)
         self.half = api.HALF_WINDOW if isinstance(variant, api.Learned) else 1
@@ -75,11 +78,11 @@ class ContentAreaEngine:
         st = api._stream(self.device)
         s = self.n_strips
         if isinstance(self.variant, api.Learned):
-            rc = lib.eca_points_learned(ctypes.c_void_p(ptr), self.batch, fstride, rstride, self._rows,
-                                        band, s, self.height, self.width, api._ptr(self.w_dev),
-                                        self.norm, api._ptr(self.probs), api._ptr(self.xs),
-                                        api._ptr(self.ys), api._ptr(self.sc), st)
-            _lib.check(rc, "eca_points_learned")
+            rc = lib.eca_points_learned_ex(ctypes.c_void_p(ptr), self.batch, fstride, rstride, self._rows,
+                                           band, s, self.height, self.width, api._ptr(self.w_dev),
+                                           self.norm, self.cnn_flags, api._ptr(self.probs),
+                                           api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), st)
+            _lib.check(rc, "eca_points_learned_ex")
             rc = lib.eca_fit(api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), self.batch,
                              2 * s, ctypes.byref(self.params), api._ptr(self.trip), 0,
                              api._ptr(self.rec), st)

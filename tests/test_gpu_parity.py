@@ -343,6 +343,33 @@ def test_learned_matches_reference():
     assert agree / total >= 0.9
 
 
+def test_learned_tensor_cores_match_reference():
+    """ECA_LEARNED_TCGEN05 (layer 2 on tcgen05, 3xTF32): probabilities within
+    1e-5 of the reference, candidates equal to the SIMT kernel's except at
+    near-ties."""
+    npz = load_npz("learned.npz")
+    net = eb.EdgeNet(eb.ChannelStats([100.0] * 3, [50.0] * 3), seed=0)
+    for c in load_json("learned.json"):
+        frame = make_frame(c["recipe"])
+        h, w = frame.shape[:2]
+        t = torch.from_numpy(frame).cuda().unsqueeze(0)
+        e_tc = eb.ContentAreaEngine(h, w, 1, variant=eb.Learned(net), tensor_cores=True)
+        e_ref = eb.ContentAreaEngine(h, w, 1, variant=eb.Learned(net))
+        e_tc.run(t)
+        e_ref.run(t)
+        torch.cuda.synchronize()
+        got = e_tc.probs[0].cpu().numpy()
+        want = npz[c["name"]][:, 3:w - 3]
+        assert np.abs(got - want).max() <= 1e-5, c["name"]
+        assert np.abs(got - e_ref.probs[0].cpu().numpy()).max() <= 1e-5
+        xt, xr = e_tc.xs[0].cpu().tolist(), e_ref.xs[0].cpu().tolist()
+        full = npz[c["name"]]
+        for k, (a, b) in enumerate(zip(xt, xr)):
+            if a != b:
+                row = full[k % len(full)]
+                assert abs(row[a] - row[b]) <= 2e-5, (c["name"], k)
+
+
 def test_mask_bit_exact_vs_oracle():
     rng = np.random.default_rng(0)
     circles = [eb.Circle(319.5, 239.5, 200.0), eb.Circle(10.25, 400.75, 333.3),
