@@ -325,11 +325,15 @@ def run_ours(args) -> None:
         dist.all_reduce(e_ms_t, op=dist.ReduceOp.MAX)
     e2e = world * BATCH * e_steps / (float(e_ms_t.item()) / 1e3)
 
-    lat = learned = mask = None
+    lat = learned = mask = crop = uhd = None
     if rank == 0:
         lat = latency(eb, dev)
         learned = learned_leg(eb, dev, pool, n_slots, peaks)
         mask = mask_leg(eb, dev, eng, pool, peaks)
+        crop = crop_leg(eb, dev, eng, pool, peaks)
+        uhd = uhd_leg(eb, dev, peaks)
+        if world == 1 and not args.no_cpu:
+            learned["cpu_baseline"] = learned_cpu(base)
 
     out = None
     if rank == 0:
@@ -375,6 +379,8 @@ def run_ours(args) -> None:
             "latency_ms": lat,
             "learned": learned,
             "mask": mask,
+            "crop": crop,
+            "uhd_4k": uhd,
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * eng.launches_per_run,
             "cpu_baseline": cpu,
@@ -471,6 +477,131 @@ def mask_leg(eb, dev, eng, pool, peaks) -> dict:
                          "frac": round(gbs / peak, 4), "kernel": "mask_kernel",
                          "algorithmic_bytes_per_launch": nbytes,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy: read+write)"}}
+
+
+_CPU_LEARNED = None
+
+
+def _cpu_learned(idx: int):
+    from oracle import eca_oracle as orc
+    from paper_2210_14771_b200.params import EcaConfig
+    frames, layers = _CPU_LEARNED
+    return orc.estimate(frames[idx % len(frames)], EcaConfig(), 0, layers=layers,
+                        norm=([100.0] * 3, [50.0] * 3))[0]
+
+
+def learned_cpu(frames) -> dict:
+    """The learned variant on the host cores: the numpy oracle port of the
+    reference's EdgeNet path, a process pool, a bounded sample."""
+    global _CPU_LEARNED
+    from oracle import eca_oracle as orc
+    _CPU_LEARNED = (frames, orc.glorot_layers(0))
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    import multiprocessing as mp
+    with ProcessPoolExecutor(cores, mp_context=mp.get_context("fork")) as ex:
+        list(ex.map(_cpu_learned, range(cores)))
+        n = cores * 2
+        t0 = time.perf_counter()
+        list(ex.map(_cpu_learned, range(n)))
+        dt = time.perf_counter() - t0
+    return {"value": round(n / dt, 2), "unit": "frames/s", "cores": cores, "kind": "port",
+            "sample": f"{n} frames of the C2 1080p mix, learned variant (EdgeNet, seed 0) through the "
+                      f"numpy oracle port, process pool of {cores}"}
+
+
+def crop_leg(eb, dev, eng, pool, peaks) -> dict:
+    """crop_augment geometry + copy (K5) for one step's records: bounds kernel,
+    then the packed HWC crops (read + write bytes)."""
+    import torch
+    from paper_2210_14771_b200 import _lib, api
+    rec = eng.run(pool[:BATCH]).clone()
+    f = pool[:BATCH]
+    lib = _lib.load()
+    st = api._stream(dev)
+    bounds = torch.empty((BATCH, 4), dtype=torch.int32, device=dev)
+    _lib.check(lib.eca_crop_bounds(api._ptr(rec), BATCH, HEIGHT, WIDTH, api._ptr(bounds), st), "crop_bounds")
+    bh = bounds.cpu().numpy()
+    sizes = [(0 if r[0] < 0 else (r[2] - r[0] + 1) * (r[3] - r[1] + 1) * 3) for r in bh]
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    offs_d = torch.from_numpy(offs).to(dev)
+    out = torch.empty(max(1, int(sum(sizes))), dtype=torch.uint8, device=dev)
+    max_rows = int(max([1] + [r[3] - r[1] + 1 for r in bh if r[0] >= 0]))
+
+    def launch():
+        _lib.check(lib.eca_crop_bounds(api._ptr(rec), BATCH, HEIGHT, WIDTH, api._ptr(bounds), st), "crop_bounds")
+        _lib.check(lib.eca_crop_copy(api._ptr(f), BATCH, f.stride(0), f.stride(1), api._ptr(bounds),
+                                     api._ptr(offs_d), api._ptr(out), max_rows, st), "crop_copy")
+    for _ in range(3):
+        launch()
+    steps = 20
+    stream = torch.cuda.current_stream(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(steps):
+        launch()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    nbytes = 2 * int(sum(sizes))
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    return {"metric": "crop_augment crops/s (K5: bounds + packed HWC copy, 1080p)",
+            "value": round(BATCH / (ms * 1e-3), 1), "unit": "crops/s", "ms_per_step": round(ms, 5),
+            "crops": int(sum(1 for r in bh if r[0] >= 0)),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "kernel": "crop_bounds_kernel + crop_copy_kernel",
+                         "algorithmic_bytes_per_step": nbytes}}
+
+
+def uhd_leg(eb, dev, peaks) -> dict:
+    """BASELINE config 4: 3840x2160 frames (the C2 mix rendered at 4K), 64 per
+    step, through the same streamed path, frames resident in HBM."""
+    import torch
+    from paper_2210_14771_b200 import synth
+    from paper_2210_14771_b200.engine import ContentAreaEngine
+    w, h, b = 3840, 2160, 64
+    specs = synth.bench_specs(8, w, h, seed=2024)
+    base = torch.from_numpy(np.stack([synth.render(sp, 40000 + k) for k, (_, sp) in enumerate(specs)])).to(dev)
+    slots = 4
+    pool = torch.empty((slots * b, h, w, 3), dtype=torch.uint8, device=dev)   # 6.4 GB
+    for i in range(slots * b):
+        pool[i].copy_(base[i % len(base)])
+    del base
+    eng = ContentAreaEngine(h, w, b, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for i in range(3):
+        eng.run_pipelined(pool[(i % slots) * b:(i % slots + 1) * b])
+    eng.fence()
+    steps = 40
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for i in range(steps):
+        eng.run_pipelined(pool[(i % slots) * b:(i % slots + 1) * b])
+    eng.fence(stream)
+    e.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(e) / steps
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for i in range(steps):
+        eng.bounds(pool[(i % slots) * b:(i % slots + 1) * b])
+    k1.record(stream)
+    torch.cuda.synchronize()
+    k_ms = k0.elapsed_time(k1) / steps
+    nbytes = b * eng.n_strips * 3 * w * 3
+    gbs = nbytes / (k_ms * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    del pool
+    torch.cuda.empty_cache()
+    return {"metric": "4K frames/s (3840x2160, C2 mix rendered at 4K, 64 per step, streamed)",
+            "value": round(b / (ms * 1e-3), 1), "unit": "frames/s", "ms_per_step": round(ms, 5),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "kernel": "eca::bounds_kernel<1, 0>",
+                         "kernel_ms": round(k_ms, 5), "algorithmic_bytes_per_launch": nbytes}}
 
 
 def latency(eb, dev) -> dict:
