@@ -465,17 +465,6 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
   return ECA_OK;
 }
 
-#ifdef ECA_STATS
-extern "C" int eca_debug_strip_stats(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, g_warp_stats, sizeof(unsigned long long) * 8) != cudaSuccess)
-    return ECA_ERR_CUDA;
-  if (reset) {
-    unsigned long long z[8] = {};
-    cudaMemcpyToSymbol(g_warp_stats, z, sizeof(z));
-  }
-  return ECA_OK;
-}
-#endif
 
 
 // ---------------------------------------------------------------- pipeline

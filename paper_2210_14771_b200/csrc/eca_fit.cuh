@@ -6,28 +6,17 @@
 // Only the moment sums (numpy: OpenBLAS dgemm) and the 3x3 solve (LAPACK
 // gesv) reassociate; the survey measured that headroom at <=2.3e-13 px.
 //
-// Mapping (one CTA per frame): LANE = hypothesis (32 attempts per chunk), so a
-// hypothesis' circle, inlier test and 3x3 solve live in one thread and need
-// no shuffles; the candidate list is split across up to kFitWarps WARPS, each
-// accumulating partial moments of its contiguous candidate range; partials
-// meet in shared memory and every warp finishes the (identical) solve.  Ties
-// between hypotheses resolve to the lowest attempt index (fitting.py:222).
+// Mapping (fit_warp, one warp per frame): LANE = hypothesis (32 attempts per
+// pass), so a hypothesis' circle, inlier tests, moment sums and 3x3 solve live
+// in one thread and need no shuffles.  Ties between hypotheses resolve to the
+// lowest attempt index (fitting.py:222).
 #pragma once
 
 #include "eca_common.cuh"
 
 namespace eca {
 
-constexpr int kFitWarps = 8;
 constexpr int kMom = 10;   // sx sy sz sxx sxy syy sxz syz count score
-
-struct FitScratch {
-  double px[2 * ECA_MAX_STRIPS];
-  double py[2 * ECA_MAX_STRIPS];
-  double ps[2 * ECA_MAX_STRIPS];
-  double part[kFitWarps][kMom][32];
-  int n;
-};
 
 struct Circ {
   double cx, cy, r;
@@ -168,196 +157,12 @@ ECA_DEV Ring ring_of(const Circ& c, double tol) {
   return g;
 }
 
-ECA_DEV bool is_inlier_fast(double x, double y, const Circ& c, const Ring& g, double tol) {
-  const double dx = x - c.cx, dy = y - c.cy;
-  const double d2 = fma(dx, dx, dy * dy);
-  if (d2 <= g.in_hi && d2 >= g.in_lo) return true;
-  if (d2 > g.out_hi || d2 < g.out_lo) return false;
-  return is_inlier(x, y, c, tol);
-}
-
-// One frame on the whole CTA.  cand_* hold n_cand candidates in estimator.py:69
-// order; `l2_loads` reads them through L2 (written by other CTAs this launch).
-ECA_DEV void fit_frame(const int32_t* cand_x, const int32_t* cand_y, const double* cand_s,
-                       int n_cand, bool l2_loads, const EcaParams& p, const int16_t* trip,
-                       int exhaustive, FitScratch* fs, EcaFitRecord* out) {
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int n_warps = blockDim.x >> 5;
-  const int W = p.width, H = p.height;
-  // ---- filter_candidates (fitting.py:39-52), order-preserving compaction
-  if (warp == 0) {
-    int cnt = 0;
-    for (int base = 0; base < n_cand; base += 32) {
-      const int i = base + lane;
-      bool keep = false;
-      int x = 0, y = 0;
-      double s = 0.0;
-      if (i < n_cand) {
-        if (l2_loads) {
-          x = __ldcg(cand_x + i);
-          y = __ldcg(cand_y + i);
-          s = __ldcg(cand_s + i);
-        } else {
-          x = cand_x[i];
-          y = cand_y[i];
-          s = cand_s[i];
-        }
-        const int edge = min(min(x, W - 1 - x), min(y, H - 1 - y));
-        keep = edge >= p.edge_margin_px && s >= p.min_point_score;
-      }
-      const unsigned bal = __ballot_sync(kFull, keep);
-      if (keep) {
-        const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
-        // (pts - (cx0, cy0)) / width  (fitting.py:187)
-        fs->px[pos] = div_rn(sub_rn(double(x), p.center_x), double(W));
-        fs->py[pos] = div_rn(sub_rn(double(y), p.center_y), double(W));
-        fs->ps[pos] = s;
-      }
-      cnt += __popc(bal);
-    }
-    if (lane == 0) fs->n = cnt;
-  }
-  __syncthreads();
-  const int n = fs->n;
-  if (n < 3) {
-    if (threadIdx.x == 0) *out = EcaFitRecord{0.0, 0.0, 0.0, 0.0, 0, ECA_NO_CANDIDATES};
-    __syncthreads();
-    return;
-  }
-  const int G = n_warps < kFitWarps ? n_warps : kFitWarps;
-  const bool worker = warp < G;
-  const int kb = worker ? (n * warp) / G : 0, ke = worker ? (n * (warp + 1)) / G : 0;
-  const int attempts = exhaustive ? n * (n - 1) * (n - 2) / 6 : p.ransac_attempts;
-  const double tol = p.inlier_tol;
-
-  double best_s = -1.0, bcx = 0.0, bcy = 0.0, br = 0.0;
-  int best_a = -1, best_inl = 0, any_live = 0, any_gated = 0;
-  for (int c0 = 0; c0 < attempts; c0 += 32) {
-    const int a = c0 + lane;
-    Circ c{0.0, 0.0, 1.0, false};
-    if (a < attempts) {
-      int i0, i1, i2;
-      if (exhaustive) {
-        unrank3(a, n, i0, i1, i2);
-      } else {
-        const int16_t* t = trip + (size_t(n - 3) * p.ransac_attempts + a) * 3;
-        i0 = t[0];
-        i1 = t[1];
-        i2 = t[2];
-      }
-      c = circumcircle(fs->px[i0], fs->py[i0], fs->px[i1], fs->py[i1], fs->px[i2], fs->py[i2]);
-    }
-    // ---- iterated least squares (fitting.py:198-205)
-    for (int it = 0; it < p.ransac_iterations; ++it) {
-      if (!__syncthreads_or(c.alive ? 1 : 0)) break;   // identical in every warp
-      if (worker) {
-        double acc[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-        if (c.alive) {
-          for (int k = kb; k < ke; ++k) {
-            const double x = fs->px[k], y = fs->py[k];
-            if (is_inlier(x, y, c, tol)) {
-              const double z = add_rn(mul_rn(x, x), mul_rn(y, y));
-              acc[0] = add_rn(acc[0], x);
-              acc[1] = add_rn(acc[1], y);
-              acc[2] = add_rn(acc[2], z);
-              acc[3] = add_rn(acc[3], mul_rn(x, x));
-              acc[4] = add_rn(acc[4], mul_rn(x, y));
-              acc[5] = add_rn(acc[5], mul_rn(y, y));
-              acc[6] = add_rn(acc[6], mul_rn(x, z));
-              acc[7] = add_rn(acc[7], mul_rn(y, z));
-              acc[8] += 1.0;
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < kMom - 1; ++q) fs->part[warp][q][lane] = acc[q];
-      }
-      __syncthreads();
-      double mo[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      for (int g = 0; g < G; ++g)
-#pragma unroll
-        for (int q = 0; q < kMom - 1; ++q) mo[q] = add_rn(mo[q], fs->part[g][q][lane]);
-      __syncthreads();   // partials may be overwritten after this
-      if (c.alive) {
-        double na, nb, nr;
-        if (lsq_solve(mo, int(mo[8]), na, nb, nr)) {
-          c.cx = na;
-          c.cy = nb;
-          c.r = nr;
-        } else {
-          c.alive = false;
-        }
-      }
-    }
-    // ---- final membership + score (fitting.py:206-208)
-    if (worker) {
-      double s = 0.0, cnt = 0.0;
-      if (c.alive)
-        for (int k = kb; k < ke; ++k)
-          if (is_inlier(fs->px[k], fs->py[k], c, tol)) {
-            s = add_rn(s, fs->ps[k]);
-            cnt += 1.0;
-          }
-      fs->part[warp][0][lane] = s;
-      fs->part[warp][1][lane] = cnt;
-    }
-    __syncthreads();
-    double score = 0.0, inl = 0.0;
-    for (int g = 0; g < G; ++g) {
-      score = add_rn(score, fs->part[g][0][lane]);
-      inl += fs->part[g][1][lane];
-    }
-    __syncthreads();
-    // ---- gates (normalised units, fitting.py:210-216) + first-index argmax
-    const bool gated = (c.r < p.min_radius_frac) || (c.r > p.max_radius_frac) ||
-                       (hypot(c.cx, c.cy) > p.max_center_offset_frac);
-    const bool surv = c.alive && !gated;
-    any_live |= __any_sync(kFull, surv);
-    any_gated |= __any_sync(kFull, c.alive && gated);
-    double s_l = surv ? score : -1.0;
-    int a_l = surv ? a : 0x7fffffff;
-#pragma unroll
-    for (int d = 16; d; d >>= 1) {
-      const double os = __shfl_xor_sync(kFull, s_l, d);
-      const int oa = __shfl_xor_sync(kFull, a_l, d);
-      if (os > s_l || (os == s_l && oa < a_l)) {
-        s_l = os;
-        a_l = oa;
-      }
-    }
-    if (a_l != 0x7fffffff && s_l > best_s) {   // chunks ascend: strict keeps the first
-      const int src = a_l - c0;
-      best_s = s_l;
-      best_a = a_l;
-      bcx = __shfl_sync(kFull, c.cx, src);
-      bcy = __shfl_sync(kFull, c.cy, src);
-      br = __shfl_sync(kFull, c.r, src);
-      best_inl = int(__shfl_sync(kFull, inl, src));
-    }
-  }
-  if (threadIdx.x == 0) {
-    EcaFitRecord rec{0.0, 0.0, 0.0, 0.0, 0, ECA_LOW_SCORE};
-    if (!any_live) {
-      rec.status = any_gated ? ECA_GEOMETRY_GATE : ECA_LOW_SCORE;
-    } else if (!(best_s < p.circle_score_threshold)) {
-      rec.status = ECA_ACCEPTED;
-      rec.cx = add_rn(p.center_x, mul_rn(bcx, double(W)));
-      rec.cy = add_rn(p.center_y, mul_rn(bcy, double(W)));
-      rec.r = mul_rn(br, double(W));
-      rec.score = best_s;
-      rec.inliers = best_inl;
-    }
-    (void)best_a;
-    *out = rec;
-  }
-  __syncthreads();
-}
 
 // ---------------------------------------------------------------------------
-// Single-warp variant (no CTA barriers): lane = hypothesis, each lane walks the
-// whole candidate list.  Used by the fused strip kernel, where the warp that
-// completes a frame fits it while the CTA's other warps keep scoring strips.
+// fit_warp: lane = hypothesis, each lane walks the whole candidate list; no CTA
+// barriers.  Used by fit_kernel (one warp per frame) and by the fused strip
+// kernel, where the warp that completes a frame fits it while the CTA's other
+// warps keep scoring strips.
 // Per-candidate moment terms (identical for every hypothesis, so computed
 // once per frame in fitting.py's per-point order): x, y, z = x^2+y^2 and the
 // products the masked least squares sums.

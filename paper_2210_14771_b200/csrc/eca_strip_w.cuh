@@ -21,14 +21,6 @@ constexpr int kWChunk = 256;       // columns per chunk (32 lanes x kPx)
 constexpr int kWMaxChunks = 8;     // half width <= 2048
 constexpr int kWListCap = 64;      // per-warp survivor list (flushed to FP64 when full)
 
-#ifdef ECA_STATS
-// diagnostic counters: [0] half-rows, [1] full halves, [2] chunks, [3] revisited
-// chunks, [4] survivors, [5] uniform lane-chunks, [6] lanes with u >= lb
-__device__ unsigned long long g_warp_stats[8];
-#define ECA_WSTAT(k, v) atomicAdd(&g_warp_stats[k], (unsigned long long)(v))
-#else
-#define ECA_WSTAT(k, v)
-#endif
 
 // Per-warp region: [stages][list][ulist][bars][ut][exs][sel]
 //   list  survivor entries (x | pre << 16), flushed to FP64 when full
