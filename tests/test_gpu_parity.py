@@ -307,6 +307,66 @@ def test_host_pipelined_matches_run_host():
         eng.run_host_pipelined(hosts[0].clone(), recs[0])   # not pinned
 
 
+def test_native_api_argument_errors():
+    """The C-ABI entry points added for streaming reject bad arguments."""
+    import ctypes
+    from paper_2210_14771_b200 import _lib, api
+    lib = _lib.load()
+    eng = eb.ContentAreaEngine(480, 640, 20)
+    n = ctypes.c_int64()
+    assert lib.eca_pipeline_bytes(0, 16, ctypes.byref(n)) == _lib.ECA_ERR_ARG
+    assert lib.eca_pipeline_bytes(20, 16, ctypes.byref(n)) == _lib.ECA_OK and n.value > 0
+    scratch = torch.zeros(n.value, dtype=torch.uint8, device="cuda")
+    pl = ctypes.c_void_p()
+    # too-small scratch, then mismatched params
+    assert lib.eca_pipeline_create(20, 480, 640, eng._rows, eng.n_strips, ctypes.byref(eng.params),
+                                   api._ptr(eng.trip), api._ptr(scratch), n.value - 1,
+                                   ctypes.byref(pl)) == _lib.ECA_ERR_ARG
+    assert lib.eca_pipeline_create(20, 480, 641, eng._rows, eng.n_strips, ctypes.byref(eng.params),
+                                   api._ptr(eng.trip), api._ptr(scratch), n.value,
+                                   ctypes.byref(pl)) == _lib.ECA_ERR_ARG
+    assert lib.eca_pipeline_create(20, 480, 640, eng._rows, eng.n_strips, ctypes.byref(eng.params),
+                                   api._ptr(eng.trip), api._ptr(scratch), n.value,
+                                   ctypes.byref(pl)) == _lib.ECA_OK
+    f = torch.zeros((20, 480, 640, 3), dtype=torch.uint8, device="cuda")
+    out = ctypes.c_void_p()
+    st = api._stream(eng.device)
+    assert lib.eca_pipeline_step(pl, ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1), 8, None, st,
+                                 ctypes.byref(out)) == _lib.ECA_ERR_ARG           # unknown flag
+    assert lib.eca_pipeline_step(pl, ctypes.c_void_p(f.data_ptr()), f.stride(0), 100, 0, None, st,
+                                 ctypes.byref(out)) == _lib.ECA_ERR_ARG           # row stride < 3W
+    assert lib.eca_pipeline_step(pl, ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1), 0, None, st,
+                                 ctypes.byref(out)) == _lib.ECA_OK
+    assert lib.eca_pipeline_fence(pl, st) == _lib.ECA_OK
+    torch.cuda.synchronize()
+    rec = torch.empty((20, 5), dtype=torch.float64, device="cuda")
+    rec.view(torch.uint8).view(-1).copy_(scratch[out.value - scratch.data_ptr():][:20 * 40])
+    assert (eng.status(rec) == _lib.NO_CANDIDATES).all()   # black frames: no candidates
+    assert lib.eca_pipeline_destroy(pl) == _lib.ECA_OK
+    # the learned entry point rejects unknown flags
+    net = eb.EdgeNet(eb.ChannelStats([100.0] * 3, [50.0] * 3), seed=0)
+    el = eb.ContentAreaEngine(480, 640, 2, variant=eb.Learned(net))
+    assert lib.eca_points_learned_ex(ctypes.c_void_p(f.data_ptr()), 2, f.stride(0), f.stride(1), el._rows,
+                                     None, el.n_strips, 480, 640, api._ptr(el.w_dev), el.norm, 2,
+                                     api._ptr(el.probs), api._ptr(el.xs), api._ptr(el.ys),
+                                     api._ptr(el.sc), st) == _lib.ECA_ERR_ARG
+
+
+def test_zero_copy_padded_host_strides():
+    """Zero-copy reads from pinned host frames with padded, unaligned rows."""
+    w, h, b, pad = 1001, 480, 18, 7
+    specs = synth.bench_specs(b, w, h, seed=9)
+    frames = np.stack([synth.render(s, 70 + k) for k, (_, s) in enumerate(specs)])
+    rs = 3 * w + pad
+    fs = h * rs + 5
+    host = torch.zeros(b * fs + 32, dtype=torch.uint8).pin_memory()
+    view = torch.as_strided(host[3:], (b, h, w, 3), (fs, rs, 3, 1))
+    view.copy_(torch.from_numpy(frames))
+    eng = eb.ContentAreaEngine(h, w, b)
+    want = eng.run(torch.from_numpy(frames).cuda()).cpu()
+    assert torch.equal(eng.run_host_zero_copy(view).clone(), want)
+
+
 def test_graph_replay_matches_direct():
     frame = synth.c1_frame()
     t = torch.from_numpy(frame).cuda().unsqueeze(0)
