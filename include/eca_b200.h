@@ -240,6 +240,34 @@ int eca_crop_copy(const uint8_t* frames, int batch, int64_t frame_stride, int64_
                   const int32_t* bounds, const int64_t* out_offsets, uint8_t* out,
                   int max_rows, void* stream);
 
+/* ------------------------------------------------ evaluation */
+
+/* Normalised-Hausdorff evaluation (metrics.py:148-213).  A record with status
+ * ECA_ACCEPTED is a circle, anything else the full frame (metrics.as_circle).
+ * Per sample b (dims[2b] = width, dims[2b+1] = height, each <= max_*):
+ * out_hd[b] = hausdorff(boundary_points(pred[b]), boundary_points(truth[b]))
+ * (metrics.py:193-203: exact FP64 distances, no KD-tree), or NaN with
+ * out_status[b] != 0: bit 0 / bit 1 = the prediction's / truth's boundary is
+ * empty (a circle that misses the frame: the reference raises ValueError).
+ * The caller scales by REF_DIAGONAL / hypot(W, H) (metrics.py:206-208). */
+int eca_nh_workspace_bytes(int batch, int max_width, int max_height, double spacing,
+                           int64_t* bytes);
+int eca_area_hausdorff(const EcaFitRecord* pred, const EcaFitRecord* truth, const int32_t* dims,
+                       int batch, int max_width, int max_height, double spacing, void* workspace,
+                       int64_t workspace_bytes, double* out_hd, int32_t* out_status, void* stream);
+
+/* boundary_points (metrics.py:148-176) of one area: out_xy[2i], out_xy[2i+1];
+ * *out_count = the number of samples (nothing is written when it exceeds cap;
+ * 0: the circle does not intersect the frame). */
+int eca_boundary_points(const EcaFitRecord* area, int width, int height, double spacing,
+                        double* out_xy, int cap, int32_t* out_count, void* stream);
+
+/* hausdorff(a, b) (metrics.py:193-203) of two device point sets [n][2] f64. */
+int eca_hausdorff_workspace_bytes(int max_points, int64_t* bytes);
+int eca_hausdorff_points(const double* a, int na, const double* b, int nb, void* workspace,
+                         int64_t workspace_bytes, double* out_hd, int32_t* out_status,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -329,3 +329,100 @@ def crop_bounds(cx: float, cy: float, r: float, width: int, height: int):
     if x1 - x0 + 1 < MIN_CROP or y1 - y0 + 1 < MIN_CROP:
         return None
     return (x0, y0, x1, y1)
+
+
+# ----------------------------------------------------------------------------
+# normalised-Hausdorff evaluation                            metrics.py:52-223
+# ----------------------------------------------------------------------------
+REF_DIAGONAL = math.hypot(1920.0, 1080.0)   # metrics.py:23
+
+
+def _linspace_cols(x0: float, dx: float, y0: float, dy: float, n: int) -> np.ndarray:
+    ts = np.linspace(0.0, 1.0, n + 1)
+    return np.column_stack((x0 + ts * dx, y0 + ts * dy))
+
+
+def boundary_pieces(circle, width: int, height: int):
+    """Arcs (t0, t1) then covered edge runs ((x0, y0), (x1, y1)) of the border of
+    disk ∩ [0, W-1] x [0, H-1] (metrics.py:52-130).  circle = (cx, cy, r) or None."""
+    xhi, yhi = float(width - 1), float(height - 1)
+    if circle is None:
+        return [], [((0.0, 0.0), (xhi, 0.0)), ((xhi, 0.0), (xhi, yhi)),
+                     ((xhi, yhi), (0.0, yhi)), ((0.0, yhi), (0.0, 0.0))]
+    cx, cy, r = circle
+    tau = 2.0 * math.pi
+    cross = []
+    for b in (0.0, xhi):                                  # metrics.py:58-62
+        c = (b - cx) / r
+        if -1.0 <= c <= 1.0:
+            t = math.acos(c)
+            cross += [t, tau - t]
+    for b in (0.0, yhi):                                  # metrics.py:63-67
+        s = (b - cy) / r
+        if -1.0 <= s <= 1.0:
+            t = math.asin(s)
+            cross += [t % tau, (math.pi - t) % tau]
+
+    def inside(t):
+        x, y = cx + r * math.cos(t), cy + r * math.sin(t)
+        return 0.0 <= x <= xhi and 0.0 <= y <= yhi
+
+    arcs = []
+    if not cross:
+        if inside(0.0):
+            arcs = [(0.0, tau)]
+    else:
+        ts = sorted(set(cross))
+        for k, t0 in enumerate(ts):
+            t1 = ts[k + 1] if k + 1 < len(ts) else ts[0] + tau
+            if t1 - t0 > 1e-12 and inside((t0 + t1) / 2.0):
+                arcs.append((t0, t1))
+    runs = []
+    for fixed, hi, horiz in ((0.0, xhi, True), (yhi, xhi, True), (0.0, yhi, False), (xhi, yhi, False)):
+        rad2 = r * r - ((fixed - cy) ** 2 if horiz else (fixed - cx) ** 2)   # metrics.py:104
+        if rad2 < 0.0:
+            continue
+        half = math.sqrt(rad2)
+        mid = cx if horiz else cy
+        a, b = max(0.0, mid - half), min(hi, mid + half)
+        if b <= a:
+            continue
+        runs.append(((a, fixed), (b, fixed)) if horiz else ((fixed, a), (fixed, b)))
+    return arcs, runs
+
+
+def boundary_points(circle, width: int, height: int, spacing: float = 1.0) -> np.ndarray:
+    """metrics.py:148-176 (samples: _sample_segment :133-138, _sample_arc :141-146)."""
+    arcs, runs = boundary_pieces(circle, width, height)
+    chunks = []
+    for t0, t1 in arcs:
+        cx, cy, r = circle
+        n = max(1, math.ceil(r * (t1 - t0) / spacing))
+        ts = np.linspace(t0, t1, n + 1)
+        chunks.append(np.column_stack((cx + r * np.cos(ts), cy + r * np.sin(ts))))
+    for p0, p1 in runs:
+        n = max(1, math.ceil(math.hypot(p1[0] - p0[0], p1[1] - p0[1]) / spacing))
+        chunks.append(_linspace_cols(p0[0], p1[0] - p0[0], p0[1], p1[1] - p0[1], n))
+    if not chunks:
+        return np.zeros((0, 2))
+    return np.vstack(chunks)
+
+
+def hausdorff(a: np.ndarray, b: np.ndarray, block: int = 2048) -> float:
+    """Symmetric Hausdorff distance (metrics.py:193-203) by brute force:
+    sqrt(dx*dx + dy*dy), the p=2 distance the reference's KD-tree returns."""
+    def directed(p, q):
+        best = 0.0
+        for i in range(0, len(p), block):
+            dx = p[i:i + block, None, 0] - q[None, :, 0]
+            dy = p[i:i + block, None, 1] - q[None, :, 1]
+            best = max(best, float(np.sqrt((dx * dx + dy * dy).min(axis=1)).max()))
+        return best
+    return max(directed(a, b), directed(b, a))
+
+
+def area_error_px(pred, truth, width: int, height: int, spacing: float = 1.0) -> float:
+    """metrics.py:206-223; pred / truth = (cx, cy, r) or None (full frame)."""
+    hd = hausdorff(boundary_points(pred, width, height, spacing),
+                   boundary_points(truth, width, height, spacing))
+    return REF_DIAGONAL / math.hypot(width, height) * hd

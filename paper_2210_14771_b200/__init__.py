@@ -59,4 +59,8 @@ from .stripnet import (
     save_weights_file,
 )
 
+from . import labels, metrics
+from .labels import EcaAnnotation, Source, pseudo_label
+from .metrics import area_error_px, area_errors, evaluate_dataset
+
 __version__ = "0.1.0"

@@ -60,6 +60,13 @@ SIGNATURES = {
     "eca_h2d_bands": [_p, ctypes.c_int, _i64, _i64, _I32P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                       _p, _p],
     "eca_crop_copy": [_p, ctypes.c_int, _i64, _i64, _p, _p, _p, ctypes.c_int, _p],
+    "eca_nh_workspace_bytes": [ctypes.c_int, ctypes.c_int, ctypes.c_int, _f64,
+                               ctypes.POINTER(ctypes.c_int64)],
+    "eca_area_hausdorff": [_p, _p, _p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _f64, _p, _i64, _p,
+                           _p, _p],
+    "eca_boundary_points": [_p, ctypes.c_int, ctypes.c_int, _f64, _p, ctypes.c_int, _p, _p],
+    "eca_hausdorff_workspace_bytes": [ctypes.c_int, ctypes.POINTER(ctypes.c_int64)],
+    "eca_hausdorff_points": [_p, ctypes.c_int, _p, ctypes.c_int, _p, _i64, _p, _p, _p],
 }
 
 _lib = None

@@ -123,3 +123,32 @@ def test_disk_mask_matches_scalar_contains():
             for x in range(20):
                 dx, dy = x - cx, y - cy
                 assert m[y, x] == (dx * dx + dy * dy <= r * r)
+
+
+# ---- evaluation row: metrics.py restated in the oracle
+def _circ(c):
+    return None if c is None else tuple(c)
+
+
+def test_oracle_boundary_points_match_reference():
+    g, pts = load_json("metrics.json"), load_npz("metrics_points.npz")
+    for i, c in enumerate(g["cases"]):
+        bp = orc.boundary_points(_circ(c["pred"]), c["w"], c["h"], c["spacing"])
+        bt = orc.boundary_points(_circ(c["truth"]), c["w"], c["h"], c["spacing"])
+        assert (len(bp), len(bt)) == (c["n_pred"], c["n_truth"]), (i, c)
+        if f"p{i}" in pts:
+            assert np.array_equal(bp, pts[f"p{i}"]) and np.array_equal(bt, pts[f"t{i}"]), i
+
+
+def test_oracle_hausdorff_matches_reference():
+    g, pts = load_json("metrics.json"), load_npz("metrics_points.npz")
+    for k, s in enumerate(g["sets"]):
+        assert orc.hausdorff(pts[f"ha{k}"], pts[f"hb{k}"]) == s["hd"], k
+    for i, c in enumerate(g["cases"]):
+        if c["w"] > 640:
+            continue   # the brute-force oracle is O(n^2): small frames here, all sizes on the GPU
+        bp = orc.boundary_points(_circ(c["pred"]), c["w"], c["h"], c["spacing"])
+        bt = orc.boundary_points(_circ(c["truth"]), c["w"], c["h"], c["spacing"])
+        assert orc.hausdorff(bp, bt) == c["hd"], (i, c)
+        if c["spacing"] == 1.0:
+            assert orc.area_error_px(_circ(c["pred"]), _circ(c["truth"]), c["w"], c["h"]) == c["nh"]
