@@ -332,8 +332,11 @@ def run_ours(args) -> None:
         mask = mask_leg(eb, dev, eng, pool, peaks)
         crop = crop_leg(eb, dev, eng, pool, peaks)
         uhd = uhd_leg(eb, dev, peaks)
+        evaluation = eval_leg(eb, dev, eng, pool)
         if world == 1 and not args.no_cpu:
             learned["cpu_baseline"] = learned_cpu(base)
+            evaluation["cpu_baseline"] = eval_cpu(evaluation.pop("_pairs"))
+        evaluation.pop("_pairs", None)
 
     out = None
     if rank == 0:
@@ -381,6 +384,7 @@ def run_ours(args) -> None:
             "mask": mask,
             "crop": crop,
             "uhd_4k": uhd,
+            "evaluation": evaluation,
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * eng.launches_per_run,
             "cpu_baseline": cpu,
@@ -554,6 +558,88 @@ def crop_leg(eb, dev, eng, pool, peaks) -> dict:
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(gbs / peak, 4), "kernel": "crop_bounds_kernel + crop_copy_kernel",
                          "algorithmic_bytes_per_step": nbytes}}
+
+
+def eval_leg(eb, dev, eng, pool) -> dict:
+    """§8f-3: normalised Hausdorff of one step's fitted records against the
+    renderer's truth circles (area_errors), event-timed over the kernels of
+    eca_area_hausdorff (boundary sampling + FP32-ordered exact FP64 scan)."""
+    import ctypes
+    import torch
+    from paper_2210_14771_b200 import _lib, api, metrics, synth
+    rec = eng.run(pool[:BATCH]).clone()
+    specs = synth.bench_specs(N_BASE, WIDTH, HEIGHT, seed=2024)
+    truth = [specs[i % N_BASE][1].circle for i in range(BATCH)]
+    rt = api._area_records([t for t in truth], dev)
+    dims = torch.tensor([[WIDTH, HEIGHT]] * BATCH, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    nb = ctypes.c_int64()
+    _lib.check(lib.eca_nh_workspace_bytes(BATCH, WIDTH, HEIGHT, 1.0, ctypes.byref(nb)), "nh ws")
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+    hd = torch.empty(BATCH, dtype=torch.float64, device=dev)
+    stt = torch.empty(BATCH, dtype=torch.int32, device=dev)
+    st = api._stream(dev)
+
+    def launch():
+        _lib.check(lib.eca_area_hausdorff(api._ptr(rec), api._ptr(rt), api._ptr(dims), BATCH, WIDTH, HEIGHT,
+                                          1.0, api._ptr(ws), nb.value, api._ptr(hd), api._ptr(stt), st),
+                   "eca_area_hausdorff")
+    for _ in range(3):
+        launch()
+    steps = 10
+    stream = torch.cuda.current_stream(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(steps):
+        launch()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    nh = hd.cpu().numpy() * (metrics.REF_DIAGONAL / math.hypot(WIDTH, HEIGHT))
+    fits = [None if r[5] != 0 else (float(r[0]), float(r[1]), float(r[2]))
+            for r in _records_np(rec)]
+    pairs = [(f, None if t is None else (t.cx, t.cy, t.r)) for f, t in zip(fits, truth)]
+    return {"metric": "normalised-Hausdorff evaluations/s (§8f-3: boundary sampling + exact Hausdorff, "
+                      "1080p, fitted records vs renderer truth)",
+            "value": round(BATCH / (ms * 1e-3), 1), "unit": "samples/s", "ms_per_step": round(ms, 5),
+            "samples": BATCH, "launches_per_step": 6,
+            "avg_error_px": round(float(nh.mean()), 4),
+            "miss_pct": round(100.0 * float((nh > metrics.HIT_MAX_NH_PX).mean()), 2),
+            "_pairs": pairs}
+
+
+def _records_np(rec):
+    r = rec.cpu().numpy()
+    i32 = r.view(np.int32).reshape(len(r), 10)
+    return [(row[0], row[1], row[2], row[3], int(i[8]), int(i[9])) for row, i in zip(r, i32)]
+
+
+_CPU_PAIRS = None
+
+
+def _cpu_eval(idx: int):
+    from oracle import eca_oracle as orc
+    p, t = _CPU_PAIRS[idx % len(_CPU_PAIRS)]
+    return orc.area_error_px_kdtree(p, t, WIDTH, HEIGHT)
+
+
+def eval_cpu(pairs) -> dict:
+    """The reference's evaluation algorithm on the host cores (boundary_points +
+    cKDTree Hausdorff, metrics.py:148-223), a process pool, a bounded sample."""
+    global _CPU_PAIRS
+    _CPU_PAIRS = pairs
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    import multiprocessing as mp
+    with ProcessPoolExecutor(cores, mp_context=mp.get_context("fork")) as ex:
+        list(ex.map(_cpu_eval, range(cores)))
+        n = max(len(pairs), cores * 16)
+        t0 = time.perf_counter()
+        list(ex.map(_cpu_eval, range(n), chunksize=4))
+        dt = time.perf_counter() - t0
+    return {"value": round(n / dt, 2), "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": f"{n} (fitted record, truth) pairs of the C2 1080p mix, oracle boundary_points + "
+                      f"scipy cKDTree as metrics.py, process pool of {cores}"}
 
 
 def uhd_leg(eb, dev, peaks) -> dict:
