@@ -471,19 +471,24 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
 // Streamed throughput mode as one native call per batch (ContentAreaEngine.
 // run_pipelined): bounds kernel of batch i on the caller's stream; rescore +
 // fit on the pipeline's side stream, overlapping batch i+1's bounds kernel.
-// Two buffer sets alternate inside the caller-provided scratch.
+// kPipeSets buffer sets rotate inside the caller-provided scratch: batch i's
+// bounds kernel waits only for the fit of batch i - kPipeSets.
+#ifndef ECA_PIPE_SETS
+#define ECA_PIPE_SETS 3
+#endif
+constexpr int kPipeSets = ECA_PIPE_SETS;
 struct EcaPipeline {
   int batch, n_strips;
   StripJob J;                 // template: geometry, params, tau
   const int16_t* trip;
   cudaStream_t side;
-  cudaEvent_t ev_bounds[2], ev_free[2];
-  bool used[2];
+  cudaEvent_t ev_bounds[kPipeSets], ev_free[kPipeSets];
+  bool used[kPipeSets];
   int step, last;
-  uint8_t* ws[2];
-  int32_t *xs[2], *ys[2];
-  double* sc[2];
-  EcaFitRecord* rec[2];
+  uint8_t* ws[kPipeSets];
+  int32_t *xs[kPipeSets], *ys[kPipeSets];
+  double* sc[kPipeSets];
+  EcaFitRecord* rec[kPipeSets];
 };
 
 namespace {
@@ -500,7 +505,7 @@ PipeLayout pipe_layout(int batch, int n_strips) {
   L.sc = L.ys + up(nc * 4);
   L.rec = L.sc + up(nc * 8);
   L.set = L.rec + up(int64_t(batch) * int64_t(sizeof(EcaFitRecord)));
-  L.total = 2 * L.set;
+  L.total = kPipeSets * L.set;
   return L;
 }
 }  // namespace
@@ -535,7 +540,7 @@ extern "C" int eca_pipeline_create(int batch, int height, int width, const int32
   P->step = 0;
   P->last = -1;
   uint8_t* base = reinterpret_cast<uint8_t*>(scratch);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kPipeSets; ++k) {
     uint8_t* b = base + k * L.set;
     P->ws[k] = b + L.ws;
     P->xs[k] = reinterpret_cast<int32_t*>(b + L.xs);
@@ -551,7 +556,7 @@ extern "C" int eca_pipeline_create(int batch, int height, int width, const int32
     delete P;
     return ECA_ERR_CUDA;
   }
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < kPipeSets; ++k)
     if (cudaEventCreateWithFlags(&P->ev_bounds[k], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_free[k], cudaEventDisableTiming) != cudaSuccess) {
       cudaStreamDestroy(P->side);
@@ -568,7 +573,7 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   if (!P || !frames || !out_records || row_stride < 3LL * P->J.p.width || frame_stride < 0)
     return ECA_ERR_ARG;
   if (flags & ~ECA_BOUNDS_ZERO_COPY) return ECA_ERR_ARG;
-  const int s = P->step & 1;
+  const int s = P->step % kPipeSets;
   cudaStream_t st = as_stream(stream);
   StripJob J = P->J;
   J.frames = frames;
@@ -620,7 +625,7 @@ extern "C" int eca_pipeline_side_stream(EcaPipeline* P, void** out_stream) {
 extern "C" int eca_pipeline_destroy(EcaPipeline* P) {
   if (!P) return ECA_OK;
   cudaStreamSynchronize(P->side);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kPipeSets; ++k) {
     cudaEventDestroy(P->ev_bounds[k]);
     cudaEventDestroy(P->ev_free[k]);
   }

@@ -175,17 +175,28 @@ struct FitScratchW {
   double ps[2 * ECA_MAX_STRIPS];
 };
 
-// Inlier mask of candidate k against lane's circle, warp-uniform control flow:
-// the d^2 screen decides almost every point; the exact hypot test runs only
-// when some lane of the warp has a point inside the screen's band.
-ECA_DEV bool inlier_w(const FitPt& P, const Circ& c, const Ring& g, double tol) {
-  const double dx = P.x - c.cx, dy = P.y - c.cy;
-  const double d2 = fma(dx, dx, dy * dy);
-  bool in = d2 <= g.in_hi && d2 >= g.in_lo;
-  const bool amb = !in && !(d2 > g.out_hi || d2 < g.out_lo);
-  if (__any_sync(kFull, amb))
-    if (amb) in = is_inlier(P.x, P.y, c, tol);
-  return in;
+// Inlier bits of candidates k0 .. k0+kn-1 (kn <= 32) against the lane's
+// circle: the d^2 screen for every candidate first, with no vote inside the
+// loop, so consecutive candidates' FP64 chains overlap; the rare candidates in
+// the screen's band then take the exact test (the decisions of is_inlier).
+ECA_DEV uint32_t inlier_bits(const FitPt* pt, int k0, int kn, const Circ& c, const Ring& g,
+                             double tol) {
+  uint32_t in_m = 0, amb_m = 0;
+#pragma unroll 8
+  for (int j = 0; j < kn; ++j) {
+    const double dx = pt[k0 + j].x - c.cx, dy = pt[k0 + j].y - c.cy;
+    const double d2 = fma(dx, dx, dy * dy);
+    const bool in = d2 <= g.in_hi && d2 >= g.in_lo;
+    const bool amb = !in && !(d2 > g.out_hi || d2 < g.out_lo);
+    in_m |= uint32_t(in) << j;
+    amb_m |= uint32_t(amb) << j;
+  }
+  while (amb_m) {
+    const int j = __ffs(amb_m) - 1;
+    amb_m &= amb_m - 1u;
+    if (is_inlier(pt[k0 + j].x, pt[k0 + j].y, c, tol)) in_m |= 1u << j;
+  }
+  return in_m;
 }
 
 ECA_DEV Ring ring_dead() {   // matches no point (hypothesis no longer alive)
@@ -260,20 +271,24 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
     for (int it = 0; it < p.ransac_iterations && __any_sync(kFull, c.alive); ++it) {
       const Ring g = c.alive ? ring_of(c, tol) : ring_dead();
       double mo[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int k0 = 0; k0 < n; k0 += 32) {
+        const int kn = min(32, n - k0);
+        const uint32_t in_m = inlier_bits(pt, k0, kn, c, g, tol);
 #pragma unroll 4
-      for (int k = 0; k < n; ++k) {
-        const FitPt P = pt[k];
-        // w in {0, 1}: fma(1, v, s) == add_rn(s, v) and fma(0, v, s) == s
-        const double w = inlier_w(P, c, g, tol) ? 1.0 : 0.0;
-        mo[0] = __fma_rn(w, P.x, mo[0]);
-        mo[1] = __fma_rn(w, P.y, mo[1]);
-        mo[2] = __fma_rn(w, P.z, mo[2]);
-        mo[3] = __fma_rn(w, P.xx, mo[3]);
-        mo[4] = __fma_rn(w, P.xy, mo[4]);
-        mo[5] = __fma_rn(w, P.yy, mo[5]);
-        mo[6] = __fma_rn(w, P.xz, mo[6]);
-        mo[7] = __fma_rn(w, P.yz, mo[7]);
-        mo[8] = add_rn(mo[8], w);
+        for (int j = 0; j < kn; ++j) {
+          const FitPt& P = pt[k0 + j];
+          // w in {0, 1}: fma(1, v, s) == add_rn(s, v) and fma(0, v, s) == s
+          const double w = (in_m >> j) & 1u ? 1.0 : 0.0;
+          mo[0] = __fma_rn(w, P.x, mo[0]);
+          mo[1] = __fma_rn(w, P.y, mo[1]);
+          mo[2] = __fma_rn(w, P.z, mo[2]);
+          mo[3] = __fma_rn(w, P.xx, mo[3]);
+          mo[4] = __fma_rn(w, P.xy, mo[4]);
+          mo[5] = __fma_rn(w, P.yy, mo[5]);
+          mo[6] = __fma_rn(w, P.xz, mo[6]);
+          mo[7] = __fma_rn(w, P.yz, mo[7]);
+          mo[8] = add_rn(mo[8], w);
+        }
       }
       double na, nb, nr;
       if (c.alive) {
@@ -290,11 +305,12 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
     int inl = 0;
     {
       const Ring g = c.alive ? ring_of(c, tol) : ring_dead();
+      for (int k0 = 0; k0 < n; k0 += 32) {
+        const int kn = min(32, n - k0);
+        const uint32_t in_m = inlier_bits(pt, k0, kn, c, g, tol);
 #pragma unroll 4
-      for (int k = 0; k < n; ++k) {
-        const bool in = inlier_w(pt[k], c, g, tol);
-        score = __fma_rn(in ? 1.0 : 0.0, ps[k], score);
-        inl += in;
+        for (int j = 0; j < kn; ++j) score = __fma_rn((in_m >> j) & 1u ? 1.0 : 0.0, ps[k0 + j], score);
+        inl += __popc(in_m);
       }
     }
     const bool gated = (c.r < p.min_radius_frac) || (c.r > p.max_radius_frac) ||

@@ -54,6 +54,7 @@ class ContentAreaEngine:
         _lib.check(_lib.load().eca_points_workspace_bytes(batch, s, ctypes.byref(nws)),
                    "eca_points_workspace_bytes")
         self.workspace = torch.zeros(max(nws.value, 256), dtype=torch.uint8, device=d)
+        self._bounds_ws = [self.workspace]   # bounds(): extra slots made on demand
         self.rec_host = torch.empty((batch, 5), dtype=torch.float64, pin_memory=True)
         if isinstance(variant, api.Learned):
             self.probs = torch.empty((batch, s, width - 6), dtype=torch.float32, device=d)
@@ -221,15 +222,21 @@ class ContentAreaEngine:
                                                   ctypes.c_void_p(stream.cuda_stream)),
                    "eca_pipeline_fence")
 
-    def bounds(self, frames: torch.Tensor) -> None:
+    def bounds(self, frames: torch.Tensor, overlap: bool = False, slot: int = 0) -> None:
         """Only the bound-and-prune kernel (the step's dominant kernel; its
-        survivors land in the workspace): the bench's roofline timing."""
+        survivors land in workspace ``slot``): the bench's roofline timing.
+        ``overlap``: programmatic dependent launch, as the streaming pipeline
+        launches it; back-to-back overlapped launches need >= 3 rotating slots
+        (a launch may still run while the next two start)."""
         f = self._check_frames(frames)
+        while len(self._bounds_ws) <= slot:
+            self._bounds_ws.append(torch.zeros_like(self.workspace))
+        ws = self._bounds_ws[slot]
         _lib.check(_lib.load().eca_bounds_handcrafted(
             ctypes.c_void_p(f.data_ptr()), self.batch, f.stride(0), f.stride(1), self._rows, None,
             self.n_strips, ctypes.byref(self.params), api._ptr(self.xs), api._ptr(self.ys),
-            api._ptr(self.sc), api._ptr(self.workspace), 0, api._stream(self.device)),
-            "eca_bounds_handcrafted")
+            api._ptr(self.sc), api._ptr(ws), _lib.BOUNDS_OVERLAP_PREVIOUS if overlap else 0,
+            api._stream(self.device)), "eca_bounds_handcrafted")
 
     def run(self, frames: torch.Tensor) -> torch.Tensor:
         """Frames on this GPU -> device records (asynchronous)."""
