@@ -7,21 +7,21 @@
 //                   :91-118, _rect_corners :121-130), then all threads write
 //                   the numpy.linspace samples (_sample_segment :133-138,
 //                   _sample_arc :141-146): FP64 points + an FP32 copy.
-//  near32_kernel    FP32 brute force, one thread per two points of A, B
-//                   staged through shared memory in tiles: per point of A the
-//                   tile holding its (approximate) nearest neighbour in B, and
-//                   the point of A with the largest approximate distance.
-//  seed_kernel      one warp per (sample, direction): that point's exact FP64
-//                   nearest distance L, a lower bound of the directed distance.
-//  exact_kernel     per point of A, an FP64 scan of B starting at its FP32
-//                   nearest tile that stops at the first distance <= L (the
-//                   point cannot raise the maximum); points that never get
-//                   there are exact minima above L -> atomic max.
+//  box_kernel       bounding boxes of every 32-point tile of each point set
+//                   (points in boundary order, so a tile is a short curve
+//                   piece) and of every 16-tile supertile, in FP64.
+//  nn_kernel        one thread per point of A: exact FP64 nearest distance in
+//                   B by branch-and-bound -- nearest supertile / tile first,
+//                   then only the (super)tiles whose box distance does not
+//                   exceed the best so far -- and a stop as soon as the best
+//                   falls to the directed maximum found so far (the point
+//                   cannot raise it).  Directed maxima by atomic max.
 //  finish_kernel    hausdorff = max over both directions (metrics.py:193-203).
 //
-// The result is exact by construction (the FP32 pass only orders the work):
-// distances are sqrt(dx*dx + dy*dy) in FP64 without contraction, cKDTree's
-// p=2 distance; the minimum over B and the maximum over A are order-free.
+// Box distances are FP64 lower bounds of every point distance in the box
+// (each rounding step is monotone), so pruning never drops a nearer point:
+// the result is exactly max_a min_b sqrt(dx*dx + dy*dy) in FP64 without
+// contraction, cKDTree's p=2 distance, in any order.
 #include <math.h>
 
 #include "eca_common.cuh"
@@ -31,8 +31,9 @@ using namespace eca;
 namespace {
 
 constexpr int kMaxPieces = 12;   // <= 8 arcs (8 crossings) + 4 edge runs
-constexpr int kTile = 512;       // B points per shared-memory tile
-constexpr int kNearThreads = 256;
+constexpr int kTileP = 32;       // points per tile
+constexpr int kSuper = 16;       // tiles per supertile
+constexpr int kSuperP = kTileP * kSuper;
 constexpr double kTwoPi = 6.283185307179586;   // 2.0 * math.pi
 constexpr double kPi = 3.141592653589793;
 
@@ -49,12 +50,10 @@ struct EvalJob {
   int batch, cap;
   double spacing;
   double2* pts;                  // [batch][2][cap]
-  float2* pts32;                 // [batch][2][cap] (null: boundary_points only)
+  double4* tbox;                 // [batch][2][cap / 32]: (xmin, ymin, xmax, ymax) per tile
+  double4* sbox;                 // [batch][2][cap / 512] per supertile
   int32_t* count;                // [batch][2]
-  uint16_t* near_tile;           // [batch][2][cap]: FP32-nearest tile of B
-  unsigned long long* far32;     // [batch][2]: (FP32 distance bits << 32) | point index
-  double* seed;                  // [batch][2]: exact nearest distance of that point
-  unsigned long long* dmax;      // [batch][2]: exact directed maxima above seed (double bits)
+  unsigned long long* dmax;      // [batch][2]: directed maxima (non-negative double bits)
   double* out_hd;                // [batch]
   int32_t* out_status;           // [batch]: bit0 prediction empty, bit1 truth empty, bit2 overflow
 };
@@ -198,7 +197,6 @@ __global__ void __launch_bounds__(256) boundary_kernel(EvalJob E) {
   const int np = np_s, tot = start[np];
   if (tot > E.cap) return;
   double2* out = E.pts + set * E.cap;
-  float2* out32 = E.pts32 ? E.pts32 + set * E.cap : nullptr;
   for (int i = threadIdx.x; i < tot; i += blockDim.x) {
     int k = 0;
     while (k + 1 < np && start[k + 1] <= i) ++k;
@@ -216,66 +214,7 @@ __global__ void __launch_bounds__(256) boundary_kernel(EvalJob E) {
       y = add_rn(p.b, mul_rn(t, sub_rn(p.d, p.b)));
     }
     out[i] = make_double2(x, y);
-    if (out32) out32[i] = make_float2(float(x), float(y));
   }
-}
-
-// direction d: A = set d of the sample, B = the other set
-__global__ void __launch_bounds__(kNearThreads) near32_kernel(EvalJob E) {
-  const int b = blockIdx.z, d = blockIdx.y;
-  const size_t sa = size_t(b) * 2 + d, sb = size_t(b) * 2 + (d ^ 1);
-  if (E.out_status[b]) return;
-  const int na = E.count[sa], nb = E.count[sb];
-  const int i0 = blockIdx.x * 2 * kNearThreads + threadIdx.x, i1 = i0 + kNearThreads;
-  if (blockIdx.x * 2 * kNearThreads >= na || nb == 0) return;
-  __shared__ __align__(16) float2 tile[kTile];
-  const float2* A = E.pts32 + sa * E.cap;
-  const float2* B = E.pts32 + sb * E.cap;
-  const float2 a0 = i0 < na ? A[i0] : make_float2(0.f, 0.f);
-  const float2 a1 = i1 < na ? A[i1] : make_float2(0.f, 0.f);
-  float m0 = INFINITY, m1 = INFINITY;
-  int t0 = 0, t1 = 0;
-  for (int base = 0; base < nb; base += kTile) {
-    const int n = min(kTile, nb - base);
-    __syncthreads();
-    for (int k = threadIdx.x; k < kTile; k += blockDim.x)
-      tile[k] = k < n ? B[base + k] : B[base];   // pad with a duplicate point
-    __syncthreads();
-    float p0 = INFINITY, p1 = INFINITY;
-    const float4* t4 = reinterpret_cast<const float4*>(tile);
-#pragma unroll 8
-    for (int k = 0; k < kTile / 2; ++k) {
-      const float4 q = t4[k];
-      float dx = a0.x - q.x, dy = a0.y - q.y;
-      p0 = fminf(p0, fmaf(dy, dy, dx * dx));
-      dx = a0.x - q.z; dy = a0.y - q.w;
-      p0 = fminf(p0, fmaf(dy, dy, dx * dx));
-      dx = a1.x - q.x; dy = a1.y - q.y;
-      p1 = fminf(p1, fmaf(dy, dy, dx * dx));
-      dx = a1.x - q.z; dy = a1.y - q.w;
-      p1 = fminf(p1, fmaf(dy, dy, dx * dx));
-    }
-    const int tix = base / kTile;
-    if (p0 < m0) { m0 = p0; t0 = tix; }
-    if (p1 < m1) { m1 = p1; t1 = tix; }
-  }
-  uint16_t* nt = E.near_tile + sa * E.cap;
-  unsigned long long key = 0;
-  if (i0 < na) {
-    nt[i0] = uint16_t(t0);
-    key = (uint64_t(__float_as_uint(m0)) << 32) | uint32_t(i0);
-  }
-  if (i1 < na) {
-    nt[i1] = uint16_t(t1);
-    const unsigned long long k1 = (uint64_t(__float_as_uint(m1)) << 32) | uint32_t(i1);
-    key = k1 > key ? k1 : key;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const unsigned long long v = __shfl_xor_sync(kFull, key, o);
-    key = v > key ? v : key;
-  }
-  if ((threadIdx.x & 31) == 0 && key) atomicMax(E.far32 + sa, key);
 }
 
 // hausdorff() on caller point sets: side 0 = a, side 1 = b
@@ -285,13 +224,46 @@ __global__ void load_points_kernel(EvalJob E, const double2* a, int na, const do
     E.count[0] = na;
     E.count[1] = nb;
   }
-  if (i < na) {
-    E.pts[i] = a[i];
-    E.pts32[i] = make_float2(float(a[i].x), float(a[i].y));
+  if (i < na) E.pts[i] = a[i];
+  if (i < nb) E.pts[E.cap + i] = b[i];
+}
+
+ECA_DEV double4 box_merge(double4 a, double4 b) {
+  return make_double4(fmin(a.x, b.x), fmin(a.y, b.y), fmax(a.z, b.z), fmax(a.w, b.w));
+}
+
+// one CTA (16 warps) per supertile of one set: warp = tile, lane = point
+__global__ void __launch_bounds__(kSuperP) box_kernel(EvalJob E) {
+  const int set = blockIdx.y, st = blockIdx.x;
+  if (E.out_status[set >> 1]) return;
+  const int n = E.count[set];
+  if (st * kSuperP >= n) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = st * kSuperP + threadIdx.x;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double4 bx = make_double4(inf, inf, -inf, -inf);
+  if (i < n) {
+    const double2 p = E.pts[size_t(set) * E.cap + i];
+    bx = make_double4(p.x, p.y, p.x, p.y);
   }
-  if (i < nb) {
-    E.pts[E.cap + i] = b[i];
-    E.pts32[E.cap + i] = make_float2(float(b[i].x), float(b[i].y));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double4 q = make_double4(__shfl_xor_sync(kFull, bx.x, o), __shfl_xor_sync(kFull, bx.y, o),
+                                   __shfl_xor_sync(kFull, bx.z, o), __shfl_xor_sync(kFull, bx.w, o));
+    bx = box_merge(bx, q);
+  }
+  __shared__ double4 tb[kSuper];
+  const int tiles = E.cap / kTileP;
+  if (lane == 0) {
+    tb[w] = bx;
+    const int t = st * kSuper + w;
+    if (t < tiles) E.tbox[size_t(set) * tiles + t] = bx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double4 sb = tb[0];
+    for (int k = 1; k < kSuper; ++k) sb = box_merge(sb, tb[k]);
+    E.sbox[size_t(set) * (E.cap / kSuperP) + st] = sb;
   }
 }
 
@@ -300,45 +272,58 @@ ECA_DEV double dist2(double2 a, double2 b) {
   return add_rn(mul_rn(dx, dx), mul_rn(dy, dy));
 }
 
-// one warp per (sample, direction): exact nearest distance of the FP32-farthest point
-__global__ void __launch_bounds__(128) seed_kernel(EvalJob E) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= 2 * E.batch || E.out_status[w >> 1]) return;
-  const int na = E.count[w], nb = E.count[w ^ 1];
-  if (na == 0 || nb == 0) return;
-  const int ia = int(uint32_t(E.far32[w] & 0xffffffffull));
-  const double2 a = E.pts[size_t(w) * E.cap + ia];
-  const double2* B = E.pts + size_t(w ^ 1) * E.cap;
-  double m = INFINITY;
-  for (int k = lane; k < nb; k += 32) m = fmin(m, dist2(a, B[k]));
-#pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmin(m, __shfl_xor_sync(kFull, m, o));
-  if (lane == 0) E.seed[w] = __dsqrt_rn(m);
+// squared distance from a to the box: <= dist2(a, b) for every b in the box
+ECA_DEV double box_d2(double2 a, double4 b) {
+  const double dx = fmax(fmax(sub_rn(b.x, a.x), sub_rn(a.x, b.z)), 0.0);
+  const double dy = fmax(fmax(sub_rn(b.y, a.y), sub_rn(a.y, b.w)), 0.0);
+  return add_rn(mul_rn(dx, dx), mul_rn(dy, dy));
 }
 
-__global__ void __launch_bounds__(256) exact_kernel(EvalJob E) {
+ECA_DEV double tile_min(const double2* B, int t, int nb, double2 a, double best) {
+  const int k1 = min(nb, (t + 1) * kTileP);
+  for (int k = t * kTileP; k < k1; ++k) best = fmin(best, dist2(a, B[k]));
+  return best;
+}
+
+__global__ void __launch_bounds__(128) nn_kernel(EvalJob E) {
   const int b = blockIdx.z, d = blockIdx.y;
-  const size_t sa = size_t(b) * 2 + d, sb = size_t(b) * 2 + (d ^ 1);
   if (E.out_status[b]) return;
+  const size_t sa = size_t(b) * 2 + d, sb = size_t(b) * 2 + (d ^ 1);
   const int na = E.count[sa], nb = E.count[sb];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= na || nb == 0) return;
-  const double L = E.seed[sa];
   const double2 a = E.pts[sa * E.cap + i];
   const double2* B = E.pts + sb * E.cap;
-  const int first = int(E.near_tile[sa * E.cap + i]) * kTile;
-  // m <= fl_down(L*L) <= L^2 implies sqrt_rn(m) <= L: this point cannot raise the maximum
-  const double stop2 = __dmul_rd(L, L);
-  double m = INFINITY;
-  // scan B from the FP32-nearest tile, wrapping, until a distance <= L
-  for (int s = 0; s < nb; ++s) {
-    int k = first + s;
-    if (k >= nb) k -= nb;
-    m = fmin(m, dist2(a, B[k]));
-    if (m <= stop2) return;
+  const int tiles = E.cap / kTileP, supers = E.cap / kSuperP;
+  const double4* TB = E.tbox + sb * tiles;
+  const double4* SB = E.sbox + sb * supers;
+  const int nt = (nb + kTileP - 1) / kTileP, ns = (nb + kSuperP - 1) / kSuperP;
+  // nearest supertile box, then its nearest tile box: the first upper bound
+  int s0 = 0;
+  double sd = INFINITY;
+  for (int s = 0; s < ns; ++s) {
+    const double v = box_d2(a, SB[s]);
+    if (v < sd) { sd = v; s0 = s; }
   }
-  const double dm = __dsqrt_rn(m);
-  if (dm > L) atomicMax(E.dmax + sa, __double_as_longlong(dm));
+  int t0 = s0 * kSuper;
+  double td = INFINITY;
+  for (int t = s0 * kSuper; t < min(nt, (s0 + 1) * kSuper); ++t) {
+    const double v = box_d2(a, TB[t]);
+    if (v < td) { td = v; t0 = t; }
+  }
+  double best = tile_min(B, t0, nb, a, INFINITY);
+  // the directed maximum so far is a lower bound of the result: a point whose
+  // nearest distance is already below it cannot change the result
+  const double lo = __longlong_as_double(
+      static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(E.dmax + sa)));
+  const double stop2 = __dmul_rd(lo, lo);
+  if (best <= stop2) return;
+  for (int s = 0; s < ns && best > stop2; ++s) {
+    if (box_d2(a, SB[s]) > best) continue;
+    for (int t = s * kSuper; t < min(nt, (s + 1) * kSuper); ++t)
+      if (t != t0 && box_d2(a, TB[t]) <= best) best = tile_min(B, t, nb, a, best);
+  }
+  if (best > stop2) atomicMax(E.dmax + sa, static_cast<unsigned long long>(__double_as_longlong(__dsqrt_rn(best))));
 }
 
 __global__ void finish_kernel(EvalJob E) {
@@ -348,33 +333,33 @@ __global__ void finish_kernel(EvalJob E) {
     E.out_hd[b] = __longlong_as_double(0x7ff8000000000000ll);
     return;
   }
-  double h = 0.0;
-  for (int d = 0; d < 2; ++d) {
-    const size_t s = size_t(b) * 2 + d;
-    h = fmax(h, fmax(E.seed[s], __longlong_as_double(E.dmax[s])));
-  }
-  E.out_hd[b] = h;
+  E.out_hd[b] = fmax(__longlong_as_double(static_cast<long long>(E.dmax[2 * b])),
+                     __longlong_as_double(static_cast<long long>(E.dmax[2 * b + 1])));
 }
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct WsLayout {
-  size_t pts, pts32, count, near_tile, far32, seed, dmax, total;
+  size_t pts, tbox, sbox, count, dmax, total;
 };
 
+// cap: a multiple of kSuperP (so tiles and supertiles index without remainders)
 WsLayout ws_layout(int batch, int cap) {
   WsLayout L;
   const size_t sets = size_t(batch) * 2;
   size_t o = 0;
-  L.pts = o;       o = align256(o + sets * cap * sizeof(double2));
-  L.pts32 = o;     o = align256(o + sets * cap * sizeof(float2));
-  L.near_tile = o; o = align256(o + sets * cap * sizeof(uint16_t));
-  L.count = o;     o = align256(o + sets * sizeof(int32_t));
-  L.far32 = o;     o = align256(o + sets * sizeof(unsigned long long));
-  L.seed = o;      o = align256(o + sets * sizeof(double));
-  L.dmax = o;      o = align256(o + sets * sizeof(unsigned long long));
+  L.pts = o;   o = align256(o + sets * cap * sizeof(double2));
+  L.tbox = o;  o = align256(o + sets * (cap / kTileP) * sizeof(double4));
+  L.sbox = o;  o = align256(o + sets * (cap / kSuperP) * sizeof(double4));
+  L.count = o; o = align256(o + sets * sizeof(int32_t));
+  L.dmax = o;  o = align256(o + sets * sizeof(unsigned long long));
   L.total = o;
   return L;
+}
+
+int round_cap(int64_t n) {
+  const int64_t c = (n + kSuperP - 1) / kSuperP * kSuperP;
+  return c > (int64_t(1) << 30) ? -1 : int(c);
 }
 
 // metrics.boundary_points sample bound: the boundary of a convex subset of
@@ -383,14 +368,14 @@ WsLayout ws_layout(int batch, int cap) {
 int boundary_cap(int width, int height, double spacing) {
   const double per = 2.0 * (double(width - 1) + double(height - 1));
   const double c = ceil(per / spacing) + 2.0 * kMaxPieces + 64.0;
-  return c > 2.0e9 ? -1 : int(c);
+  return c > 1.0e9 ? -1 : round_cap(int64_t(c));
 }
 
 EvalJob make_job(const EcaFitRecord* pred, const EcaFitRecord* truth, const int32_t* dims,
                  int batch, int cap, double spacing, void* ws, double* out_hd, int32_t* out_status) {
   const WsLayout L = ws_layout(batch, cap);
   uint8_t* w = static_cast<uint8_t*>(ws);
-  EvalJob E;
+  EvalJob E{};
   E.area[0] = pred;
   E.area[1] = truth;
   E.dims = dims;
@@ -398,11 +383,9 @@ EvalJob make_job(const EcaFitRecord* pred, const EcaFitRecord* truth, const int3
   E.cap = cap;
   E.spacing = spacing;
   E.pts = reinterpret_cast<double2*>(w + L.pts);
-  E.pts32 = reinterpret_cast<float2*>(w + L.pts32);
+  E.tbox = reinterpret_cast<double4*>(w + L.tbox);
+  E.sbox = reinterpret_cast<double4*>(w + L.sbox);
   E.count = reinterpret_cast<int32_t*>(w + L.count);
-  E.near_tile = reinterpret_cast<uint16_t*>(w + L.near_tile);
-  E.far32 = reinterpret_cast<unsigned long long*>(w + L.far32);
-  E.seed = reinterpret_cast<double*>(w + L.seed);
   E.dmax = reinterpret_cast<unsigned long long*>(w + L.dmax);
   E.out_hd = out_hd;
   E.out_status = out_status;
@@ -411,12 +394,9 @@ EvalJob make_job(const EcaFitRecord* pred, const EcaFitRecord* truth, const int3
 
 int run_distance(const EvalJob& E, const WsLayout& L, void* ws, cudaStream_t st) {
   uint8_t* w = static_cast<uint8_t*>(ws);
-  // far32, seed and dmax are contiguous: one memset clears the reduction state
-  cudaMemsetAsync(w + L.far32, 0, L.total - L.far32, st);
-  const int blocks_a = (E.cap + 2 * kNearThreads - 1) / (2 * kNearThreads);
-  near32_kernel<<<dim3(blocks_a, 2, E.batch), kNearThreads, 0, st>>>(E);
-  seed_kernel<<<(2 * E.batch * 32 + 127) / 128, 128, 0, st>>>(E);
-  exact_kernel<<<dim3((E.cap + 255) / 256, 2, E.batch), 256, 0, st>>>(E);
+  cudaMemsetAsync(w + L.dmax, 0, L.total - L.dmax, st);
+  box_kernel<<<dim3(E.cap / kSuperP, 2 * E.batch), kSuperP, 0, st>>>(E);
+  nn_kernel<<<dim3((E.cap + 127) / 128, 2, E.batch), 128, 0, st>>>(E);
   finish_kernel<<<(E.batch + 127) / 128, 128, 0, st>>>(E);
   return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
 }
@@ -429,7 +409,7 @@ int eca_nh_workspace_bytes(int batch, int max_width, int max_height, double spac
                            int64_t* bytes) {
   if (batch < 0 || max_width < 2 || max_height < 2 || !(spacing > 0.0) || !bytes) return ECA_ERR_ARG;
   const int cap = boundary_cap(max_width, max_height, spacing);
-  if (cap < 0 || cap > 65535 * kTile) return ECA_ERR_UNSUPPORTED;
+  if (cap < 0) return ECA_ERR_UNSUPPORTED;
   *bytes = int64_t(ws_layout(batch, cap).total);
   return ECA_OK;
 }
@@ -441,7 +421,7 @@ int eca_area_hausdorff(const EcaFitRecord* pred, const EcaFitRecord* truth, cons
   if (batch == 0) return ECA_OK;
   if (!pred || !truth || !dims || !workspace || !out_hd || !out_status) return ECA_ERR_ARG;
   const int cap = boundary_cap(max_width, max_height, spacing);
-  if (cap < 0 || cap > 65535 * kTile) return ECA_ERR_UNSUPPORTED;
+  if (cap < 0) return ECA_ERR_UNSUPPORTED;
   const WsLayout L = ws_layout(batch, cap);
   if (workspace_bytes < int64_t(L.total)) return ECA_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -470,8 +450,9 @@ int eca_boundary_points(const EcaFitRecord* area, int width, int height, double 
 }
 
 int eca_hausdorff_workspace_bytes(int max_points, int64_t* bytes) {
-  if (max_points < 1 || max_points > 65535 * kTile || !bytes) return ECA_ERR_ARG;
-  *bytes = int64_t(ws_layout(1, max_points).total);
+  const int cap = round_cap(max_points);
+  if (max_points < 1 || cap < 0 || !bytes) return ECA_ERR_ARG;
+  *bytes = int64_t(ws_layout(1, cap).total);
   return ECA_OK;
 }
 
@@ -479,8 +460,8 @@ int eca_hausdorff_points(const double* a, int na, const double* b, int nb, void*
                          int64_t workspace_bytes, double* out_hd, int32_t* out_status,
                          void* stream) {
   if (na < 1 || nb < 1 || !a || !b || !workspace || !out_hd || !out_status) return ECA_ERR_ARG;
-  const int cap = na > nb ? na : nb;
-  if (cap > 65535 * kTile) return ECA_ERR_UNSUPPORTED;
+  const int cap = round_cap(na > nb ? na : nb);
+  if (cap < 0) return ECA_ERR_UNSUPPORTED;
   const WsLayout L = ws_layout(1, cap);
   if (workspace_bytes < int64_t(L.total)) return ECA_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
