@@ -343,7 +343,9 @@ def run_ours(args) -> None:
         crop = crop_leg(eb, dev, eng, pool, peaks)
         uhd = uhd_leg(eb, dev, peaks)
         evaluation = eval_leg(eb, dev, eng, pool)
+        training = train_leg(eb, dev)
         if world == 1 and not args.no_cpu:
+            training["cpu_baseline"] = train_cpu()
             learned["cpu_baseline"] = learned_cpu(base)
             evaluation["cpu_baseline"] = eval_cpu(evaluation.pop("_pairs"))
         evaluation.pop("_pairs", None)
@@ -401,6 +403,7 @@ def run_ours(args) -> None:
             "crop": crop,
             "uhd_4k": uhd,
             "evaluation": evaluation,
+            "training": training,
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * eng.launches_per_run,
             "cpu_baseline": cpu,
@@ -623,6 +626,75 @@ def eval_leg(eb, dev, eng, pool) -> dict:
             "avg_error_px": round(float(nh.mean()), 4),
             "miss_pct": round(100.0 * float((nh > metrics.HIT_MAX_NH_PX).mean()), 2),
             "_pairs": pairs}
+
+
+TRAIN_M, TRAIN_BATCH = 2048, 8
+
+
+def _train_data(m: int):
+    rng = np.random.default_rng(77)
+    x = rng.normal(0.0, 1.0, (m, 5, 7, WIDTH)).astype(np.float32)
+    t = rng.uniform(0.0, 1.0, (m, 1, 1, WIDTH - 6)).astype(np.float32)
+    return x, t
+
+
+def train_leg(eb, dev) -> dict:
+    """§8f-4: one epoch of EdgeNet SGD training (edgenet.train) over 2048
+    synthetic RGBXY strips (5 x 7 x 1920, the learned variant's input) in
+    batches of 8, forward + BCE + backward + update on the GPU; wall clock
+    with the strips resident in HBM, synchronised."""
+    import torch
+    from paper_2210_14771_b200 import training as tr
+    x, t = _train_data(TRAIN_M)
+    xd, td = torch.from_numpy(x).to(dev), torch.from_numpy(t).to(dev)
+    cfg = tr.TrainConfig(learning_rate=0.001, batch_size=TRAIN_BATCH, max_epochs=1)
+    net = eb.EdgeNet(eb.ChannelStats((100.0,) * 3, (50.0,) * 3), seed=0)
+    tr.train(net, (xd[:64], td[:64]), None, cfg)   # warm-up
+    torch.cuda.synchronize()
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        tr.train(eb.EdgeNet(eb.ChannelStats((100.0,) * 3, (50.0,) * 3), seed=0), (xd, td), None, cfg)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    steps = TRAIN_M // TRAIN_BATCH
+    return {"metric": "EdgeNet training samples/s (§8f-4: SGD epoch, batch 8 strips of 5x7x1920, "
+                      "forward + BCE + backward + update)",
+            "value": round(TRAIN_M / dt, 1), "unit": "samples/s", "ms_per_step": round(1e3 * dt / steps, 4),
+            "steps": steps, "launches_per_step": 16, "dtype": "f32", "data": "synthetic normal strips"}
+
+
+_CPU_TRAIN = None
+
+
+def _cpu_train(k: int):
+    from oracle import eca_oracle as orc
+    x, t, layers = _CPU_TRAIN
+    s = (k * TRAIN_BATCH) % (len(x) - TRAIN_BATCH)
+    return orc.train_step(x[s:s + TRAIN_BATCH], t[s:s + TRAIN_BATCH], layers, 0.001)[0]
+
+
+def train_cpu() -> dict:
+    """The reference's training step (numpy im2col forward/backward, edgenet.py
+    :100-130, 306-328) restated in the oracle, a process pool over the host
+    cores, a bounded sample of steps."""
+    global _CPU_TRAIN
+    from oracle import eca_oracle as orc
+    x, t = _train_data(64)
+    _CPU_TRAIN = (x, t, orc.glorot_layers(0))
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    import multiprocessing as mp
+    with ProcessPoolExecutor(cores, mp_context=mp.get_context("fork")) as ex:
+        list(ex.map(_cpu_train, range(cores)))
+        n = cores * 2
+        t0 = time.perf_counter()
+        list(ex.map(_cpu_train, range(n)))
+        dt = time.perf_counter() - t0
+    return {"value": round(n * TRAIN_BATCH / dt, 2), "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": f"{n} SGD steps of 8 strips (5x7x1920) through the numpy oracle port of "
+                      f"edgenet.train, process pool of {cores}, 1 BLAS thread each (independent steps)"}
 
 
 def _records_np(rec):

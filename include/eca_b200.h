@@ -268,6 +268,26 @@ int eca_hausdorff_points(const double* a, int na, const double* b, int nb, void*
                          int64_t workspace_bytes, double* out_hd, int32_t* out_status,
                          void* stream);
 
+/* ------------------------------------------- learned training */
+
+/* EdgeNet training pieces (edgenet.py:100-130, 182-211, 213-225, 236-241,
+ * 277-344), FP32.  x: [*][5][h][w] float32 RGBXY samples (NCHW, the
+ * reference's training inputs), targets: [*][1][h-6][w-6]; index: the m
+ * sample indices of this batch (null: samples 0..m-1).  net: ECA_NET_FLOATS
+ * packed weights (kernel0, bias0, ..., kernel3, bias3 in reference order).
+ * forward keeps the activations in the workspace (the reference's caches);
+ * backward (after forward on the same batch) writes the mean stable BCE loss
+ * (FP64), the packed gradients (out_grads null: the loss only), and sets
+ * *diverged = 1 on a non-finite loss (diverged may be null).
+ * eca_sgd_step: net -= fl32(lr) * grads, skipped while *diverged != 0. */
+int eca_train_workspace_bytes(int m, int h, int w, int64_t* bytes);
+int eca_edgenet_forward(const float* x, const int32_t* index, int m, int h, int w, const float* net,
+                        void* workspace, int64_t workspace_bytes, float* out_logits, void* stream);
+int eca_edgenet_backward(const float* x, const float* targets, const int32_t* index, int m, int h,
+                         int w, const float* net, void* workspace, int64_t workspace_bytes,
+                         float* out_grads, double* out_loss, int32_t* diverged, void* stream);
+int eca_sgd_step(float* net, const float* grads, float lr, const int32_t* diverged, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

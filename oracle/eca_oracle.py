@@ -438,3 +438,116 @@ def hausdorff_kdtree(a: np.ndarray, b: np.ndarray) -> float:
 def area_error_px_kdtree(pred, truth, width: int, height: int) -> float:
     hd = hausdorff_kdtree(boundary_points(pred, width, height), boundary_points(truth, width, height))
     return REF_DIAGONAL / math.hypot(width, height) * hd
+
+
+# ----------------------------------------------------------------------------
+# learned-variant training                     edgenet.py:100-130, 182-225, 236-344
+# ----------------------------------------------------------------------------
+def _im2col(x: np.ndarray, kh: int, kw: int) -> np.ndarray:
+    w = np.lib.stride_tricks.sliding_window_view(x, (kh, kw), axis=(2, 3))
+    return np.ascontiguousarray(w.transpose(0, 2, 3, 1, 4, 5)).reshape(-1, x.shape[1] * kh * kw)
+
+
+def forward_logits(x: np.ndarray, layers):
+    """(B,5,h,W) -> logits (B,1,h-6,W-6) and the per-layer caches
+    (input, im2col, ReLU mask) of edgenet.py:182-205."""
+    x = np.asarray(x, dtype=np.float32)
+    caches = []
+    for i, (kern, bias) in enumerate(layers):
+        y = _valid_conv(x, kern, bias)
+        mask = (y > 0) if i < 3 else None
+        caches.append((x.shape, _im2col(x, kern.shape[2], kern.shape[3]), mask))
+        x = y * mask if i < 3 else y
+    return x, caches
+
+
+def backward(dlogits: np.ndarray, caches, layers):
+    """Per-layer (dkernel, dbias), edgenet.py:119-130 + 213-224."""
+    grads = [None] * 4
+    dy = dlogits.astype(np.float32)
+    for k in range(3, -1, -1):
+        x_shape, cols, _ = caches[k]
+        kern = layers[k][0]
+        oc, ic, kh, kw = kern.shape
+        dy_mat = np.ascontiguousarray(dy.transpose(0, 2, 3, 1)).reshape(-1, oc)
+        grads[k] = ((dy_mat.T @ cols).reshape(kern.shape), dy_mat.sum(axis=0))
+        padded = np.pad(dy, ((0, 0), (0, 0), (kh - 1, kh - 1), (kw - 1, kw - 1)))
+        flipped = np.ascontiguousarray(kern[:, :, ::-1, ::-1].transpose(1, 0, 2, 3))
+        dy = _valid_conv(padded, flipped, np.zeros(ic, dtype=np.float32))
+        if k > 0:
+            dy = dy * caches[k - 1][2]
+    return grads
+
+
+def sigmoid32(z: np.ndarray) -> np.ndarray:
+    out = np.empty_like(z)
+    pos = z >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-z[pos]))
+    e = np.exp(z[~pos])
+    out[~pos] = e / (1.0 + e)
+    return out
+
+
+def bce_with_logits(logits: np.ndarray, targets: np.ndarray) -> float:
+    """edgenet.py:236-241: mean stable BCE in float64."""
+    z = logits.astype(np.float64)
+    t = targets.astype(np.float64)
+    return float((np.maximum(z, 0.0) - z * t + np.log1p(np.exp(-np.abs(z)))).mean())
+
+
+def train_step(x, t, layers, lr: float):
+    """One SGD step of edgenet.train (:306-328); returns (loss, grads, new layers)."""
+    logits, caches = forward_logits(x, layers)
+    loss = bce_with_logits(logits, t)
+    dlog = (sigmoid32(logits) - t.astype(np.float32)) / logits.size
+    grads = backward(dlog, caches, layers)
+    new = [(k - np.float32(lr) * dk, b - np.float32(lr) * db) for (k, b), (dk, db) in zip(layers, grads)]
+    return loss, grads, new
+
+
+def train(layers, train_x, train_t, val_x, val_t, lr=0.001, batch=8, patience=5, epochs=50,
+          shuffle=True, seed=0):
+    """edgenet.train (:277-344): SGD, per-epoch permutation, early stopping on
+    the validation loss; returns (layers of the best epoch, train losses, val
+    losses, best epoch).  Raises FloatingPointError on a non-finite loss."""
+    rng = np.random.default_rng(seed)
+    layers = [(k.copy(), b.copy()) for k, b in layers]
+    best, best_val, stale, best_epoch = [(k.copy(), b.copy()) for k, b in layers], np.inf, 0, -1
+    tl, vl = [], []
+    for epoch in range(epochs):
+        order = rng.permutation(len(train_x)) if shuffle else np.arange(len(train_x))
+        tot, cnt = 0.0, 0
+        for s in range(0, len(order), batch):
+            idx = order[s:s + batch]
+            x, t = train_x[idx], train_t[idx]
+            logits, caches = forward_logits(x, layers)
+            loss = bce_with_logits(logits, t)
+            if not np.isfinite(loss):
+                raise FloatingPointError(f"non-finite loss at epoch {epoch}, sample offset {s}")
+            tot += loss * logits.size
+            cnt += logits.size
+            dlog = (sigmoid32(logits) - t.astype(np.float32)) / logits.size
+            grads = backward(dlog, caches, layers)
+            if lr != 0.0:
+                for (k, b), (dk, db) in zip(layers, grads):
+                    k -= lr * dk
+                    b -= lr * db
+        tl.append(tot / cnt)
+        if val_x is not None:
+            vt, vc = 0.0, 0
+            vb = max(batch, 32)
+            for s in range(0, len(val_x), vb):
+                lg, _ = forward_logits(val_x[s:s + vb], layers)
+                vt += bce_with_logits(lg, val_t[s:s + vb]) * lg.size
+                vc += lg.size
+            v = vt / max(vc, 1)
+            vl.append(v)
+            if v < best_val:
+                best_val, best, best_epoch, stale = v, [(k.copy(), b.copy()) for k, b in layers], epoch, 0
+            else:
+                stale += 1
+                if stale >= patience:
+                    break
+        else:
+            best, best_epoch = [(k.copy(), b.copy()) for k, b in layers], epoch
+    return best, tl, vl, best_epoch

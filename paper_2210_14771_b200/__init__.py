@@ -59,7 +59,7 @@ from .stripnet import (
     save_weights_file,
 )
 
-from . import labels, metrics
+from . import labels, metrics, training
 from .labels import EcaAnnotation, Source, pseudo_label
 from .metrics import area_error_px, area_errors, evaluate_dataset
 

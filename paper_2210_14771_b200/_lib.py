@@ -67,6 +67,11 @@ SIGNATURES = {
     "eca_boundary_points": [_p, ctypes.c_int, ctypes.c_int, _f64, _p, ctypes.c_int, _p, _p],
     "eca_hausdorff_workspace_bytes": [ctypes.c_int, ctypes.POINTER(ctypes.c_int64)],
     "eca_hausdorff_points": [_p, ctypes.c_int, _p, ctypes.c_int, _p, _i64, _p, _p, _p],
+    "eca_train_workspace_bytes": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)],
+    "eca_edgenet_forward": [_p, _p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _p, _i64, _p, _p],
+    "eca_edgenet_backward": [_p, _p, _p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _p, _i64, _p, _p,
+                             _p, _p],
+    "eca_sgd_step": [_p, _p, ctypes.c_float, _p, _p],
 }
 
 _lib = None

@@ -1,0 +1,363 @@
+// §8f-4: EdgeNet training on the GPU (edgenet.py:100-130, 213-344), FP32 like
+// the reference.
+//
+// Inputs are the reference's training tensors: x [*][5][h][W] (NCHW float32,
+// RGBXY rows), targets [*][1][h-6][W-6]; a batch is a list of sample indices
+// into them (the epoch permutation), gathered inside the first kernels.
+//
+//  forward    conv3_fwd (3x3 valid conv + bias + ReLU, one thread per output
+//             position, all output channels in registers, weights in shared
+//             memory) x3, head_fwd (1x1 conv) -> logits; activations stay in
+//             the workspace (the reference's caches; ReLU masks are y > 0).
+//  backward   loss_kernel: stable BCE terms in FP64 (edgenet.py:236-241) and
+//             dlogits = (sigmoid(z) - t) / N in FP32 (:315); head_dgrad; per 3x3
+//             layer conv3_dgrad (dx = full correlation with the flipped
+//             kernel, times the previous layer's ReLU mask) and conv_wgrad
+//             (per-row-segment partial dW / db in shared memory, then a
+//             fixed-order reduction: deterministic, no float atomics).
+//  sgd        w = w - fl32(lr) * g without contraction (:327-328), skipped
+//             once a non-finite loss was seen (the reference raises before
+//             that update), so an epoch runs without host round trips.
+// Accumulations are sequential FMA; the reference's sgemm reassociates, so
+// logits / gradients agree to FP32 rounding, not bitwise.
+#include <math.h>
+
+#include "eca_common.cuh"
+
+using namespace eca;
+
+namespace {
+
+constexpr int kOffW0 = 0, kOffB0 = 360, kOffW1 = 368, kOffB1 = 1520, kOffW2 = 1536, kOffB2 = 6144,
+              kOffW3 = 6176, kOffB3 = 6208, kNetN = 6209;
+static_assert(kNetN == ECA_NET_FLOATS, "weight layout");
+constexpr int kSeg = 128;   // output columns per weight-gradient segment
+
+struct TrainWs {   // workspace layout (floats unless noted)
+  size_t a1, a2, a3, logit, d3, d2, d1, dlog, wpart, lpart, total;
+  int nseg3, nseg2, nseg1, nseg0, nlblk;
+};
+
+size_t up256(size_t v) { return (v + 255) & ~size_t(255); }
+
+constexpr int kLossThreads = 256;
+
+TrainWs train_ws(int m, int h, int w) {
+  TrainWs L;
+  const size_t p1 = size_t(m) * (h - 2) * (w - 2), p2 = size_t(m) * (h - 4) * (w - 4),
+               p3 = size_t(m) * (h - 6) * (w - 6);
+  size_t o = 0;
+  L.a1 = o;    o = up256(o + 4 * 8 * p1);
+  L.a2 = o;    o = up256(o + 4 * 16 * p2);
+  L.a3 = o;    o = up256(o + 4 * 32 * p3);
+  L.logit = o; o = up256(o + 4 * p3);
+  L.d3 = o;    o = up256(o + 4 * 32 * p3);
+  L.d2 = o;    o = up256(o + 4 * 16 * p2);
+  L.d1 = o;    o = up256(o + 4 * 8 * p1);
+  L.dlog = o;  o = up256(o + 4 * p3);
+  // weight-gradient segments: (sample, output row, kSeg columns) per layer
+  L.nseg3 = int(size_t(m) * (h - 6) * ((w - 6 + kSeg - 1) / kSeg));
+  L.nseg2 = L.nseg3;   // layer 2's output grid is the head's
+  L.nseg1 = int(size_t(m) * (h - 4) * ((w - 4 + kSeg - 1) / kSeg));
+  L.nseg0 = int(size_t(m) * (h - 2) * ((w - 2 + kSeg - 1) / kSeg));
+  const size_t parts = size_t(L.nseg3) * (32 + 1) + size_t(L.nseg2) * (4608 + 32) +
+                       size_t(L.nseg1) * (1152 + 16) + size_t(L.nseg0) * (360 + 8);
+  L.wpart = o; o = up256(o + 4 * parts);
+  L.nlblk = int((p3 + kLossThreads - 1) / kLossThreads);
+  L.lpart = o; o = up256(o + 8 * size_t(L.nlblk));
+  L.total = o;
+  return L;
+}
+
+// ---------------------------------------------------------------- forward ---
+// x: [*][CI][hi][wi] (sample idx[b] when idx, else b) -> y: [m][CO][hi-2][wi-2]
+template <int CI, int CO>
+__global__ void __launch_bounds__(128) conv3_fwd(const float* x, const int32_t* idx, int m, int hi,
+                                                 int wi, const float* wk, const float* bias, float* y) {
+  __shared__ float sw[CO * CI * 9], sb[CO];
+  for (int i = threadIdx.x; i < CO * CI * 9; i += blockDim.x) sw[i] = wk[i];
+  for (int i = threadIdx.x; i < CO; i += blockDim.x) sb[i] = bias[i];
+  __syncthreads();
+  const int ho = hi - 2, wo = wi - 2;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= int64_t(m) * ho * wo) return;
+  const int ox = int(p % wo), oy = int((p / wo) % ho), b = int(p / (int64_t(wo) * ho));
+  const int s = idx ? idx[b] : b;
+  const float* xs = x + int64_t(s) * CI * hi * wi;
+  float acc[CO];
+#pragma unroll
+  for (int o = 0; o < CO; ++o) acc[o] = 0.f;
+  for (int c = 0; c < CI; ++c)
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const float v = xs[(int64_t(c) * hi + oy + k / 3) * wi + ox + k % 3];
+#pragma unroll
+      for (int o = 0; o < CO; ++o) acc[o] = fmaf(sw[(o * CI + c) * 9 + k], v, acc[o]);
+    }
+  float* ys = y + int64_t(b) * CO * ho * wo + int64_t(oy) * wo + ox;
+#pragma unroll
+  for (int o = 0; o < CO; ++o) {
+    const float v = acc[o] + sb[o];
+    ys[int64_t(o) * ho * wo] = v * float(v > 0.f);   // y * (y > 0): -inf and NaN give NaN, as numpy
+  }
+}
+
+// 1x1 head: logit = sum_c w3[c] * a3[c] + b3
+__global__ void __launch_bounds__(128) head_fwd(const float* a3, int64_t plane, int m,
+                                                const float* net, float* logit) {
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= int64_t(m) * plane) return;
+  const int64_t b = p / plane, q = p % plane;
+  const float* a = a3 + b * 32 * plane + q;
+  float z = 0.f;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) z = fmaf(net[kOffW3 + c], a[c * plane], z);
+  logit[p] = z + net[kOffB3];
+}
+
+// --------------------------------------------------------------- backward ---
+// stable BCE terms (FP64) + dlogits (FP32); block partial sums of the terms
+__global__ void __launch_bounds__(kLossThreads) loss_kernel(const float* logit, const float* tgt,
+                                                            const int32_t* idx, int m, int64_t plane,
+                                                            float* dlog, double* lpart) {
+  const int64_t n = int64_t(m) * plane;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  double term = 0.0;
+  if (p < n) {
+    const int64_t b = p / plane, q = p % plane;
+    const float t = tgt[(idx ? int64_t(idx[b]) : b) * plane + q];
+    const float z = logit[p];
+    const double zd = double(z), td = double(t);
+    term = add_rn(sub_rn(fmax(zd, 0.0), mul_rn(zd, td)), log1p(exp(-fabs(zd))));
+    float sg;   // _sigmoid (edgenet.py:227-233), FP32
+    if (z >= 0.f) {
+      sg = 1.0f / (1.0f + expf(-z));
+    } else {
+      const float e = expf(z);
+      sg = e / (1.0f + e);
+    }
+    dlog[p] = __fdiv_rn(__fsub_rn(sg, t), float(n));
+  }
+  __shared__ double red[kLossThreads];
+  red[threadIdx.x] = term;
+  __syncthreads();
+  for (int o = kLossThreads / 2; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) lpart[blockIdx.x] = red[0];
+}
+
+// mean loss (fixed order over blocks); flags a non-finite loss
+__global__ void loss_final(const double* lpart, int nblk, int64_t n, double* out_loss, int32_t* flag) {
+  __shared__ double red[256];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += 256) v += lpart[i];
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 128; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double loss = red[0] / double(n);
+    *out_loss = loss;
+    if (!isfinite(loss) && flag) *flag = 1;
+  }
+}
+
+// head backward: da3 = g * w3 * (a3 > 0)
+__global__ void __launch_bounds__(128) head_dgrad(const float* dlog, const float* a3, int64_t plane,
+                                                  int m, const float* net, float* d3) {
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= int64_t(m) * plane) return;
+  const int64_t b = p / plane, q = p % plane;
+  const float g = dlog[p];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const int64_t o = b * 32 * plane + c * plane + q;
+    d3[o] = (g * net[kOffW3 + c]) * float(a3[o] > 0.f);   // dx * mask (inf * 0 = NaN, as numpy)
+  }
+}
+
+// Weight / bias gradient partials of one segment (sample, output row, kSeg
+// output columns) for a KxK valid correlation: part[seg][(o*CI + c)*K*K + k]
+// and part[seg][CO*CI*K*K + o].  x: the layer input (sample idx[b] when idx).
+template <int CI, int CO, int K>
+__global__ void __launch_bounds__(256) conv_wgrad(const float* dy, const float* x, const int32_t* idx,
+                                                  int m, int hi, int wi, float* part) {
+  constexpr int NW = CO * CI * K * K;
+  const int ho = hi - K + 1, wo = wi - K + 1;
+  const int segs_x = (wo + kSeg - 1) / kSeg;
+  const int seg = blockIdx.x;
+  const int sx = seg % segs_x, oy = (seg / segs_x) % ho, b = seg / (segs_x * ho);
+  const int x0 = sx * kSeg, len = min(kSeg, wo - x0);
+  __shared__ float sdy[CO][kSeg];
+  __shared__ float sx_[CI][K][kSeg + K - 1];
+  const int s = idx ? idx[b] : b;
+  for (int i = threadIdx.x; i < CO * kSeg; i += blockDim.x) {
+    const int o = i / kSeg, j = i % kSeg;
+    sdy[o][j] = j < len ? dy[((int64_t(b) * CO + o) * ho + oy) * wo + x0 + j] : 0.f;
+  }
+  for (int i = threadIdx.x; i < CI * K * (kSeg + K - 1); i += blockDim.x) {
+    const int c = i / (K * (kSeg + K - 1)), r = (i / (kSeg + K - 1)) % K, j = i % (kSeg + K - 1);
+    sx_[c][r][j] = j < len + K - 1 ? x[((int64_t(s) * CI + c) * hi + oy + r) * wi + x0 + j] : 0.f;
+  }
+  __syncthreads();
+  float* out = part + size_t(seg) * (NW + CO);
+  for (int wi_ = threadIdx.x; wi_ < NW + CO; wi_ += blockDim.x) {
+    float acc = 0.f;
+    if (wi_ < NW) {
+      const int o = wi_ / (CI * K * K), c = (wi_ / (K * K)) % CI, k = wi_ % (K * K);
+      const int ky = k / K, kx = k % K;
+      for (int j = 0; j < len; ++j) acc = fmaf(sdy[o][j], sx_[c][ky][j + kx], acc);
+    } else {
+      const int o = wi_ - NW;
+      for (int j = 0; j < len; ++j) acc += sdy[o][j];
+    }
+    out[wi_] = acc;
+  }
+}
+
+// grads[off + i] = sum over segments (fixed order) of part[seg][i]
+__global__ void wgrad_reduce(const float* part, int nseg, int nw, float* gw, float* gb, int nb) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nw + nb) return;
+  float acc = 0.f;
+  for (int s = 0; s < nseg; ++s) acc += part[size_t(s) * (nw + nb) + i];
+  if (i < nw) gw[i] = acc;
+  else gb[i - nw] = acc;
+}
+
+// dx[c][y][x] = sum_{o,ky,kx} dy[o][y-ky][x-kx] * w[o][c][ky][kx], times the
+// ReLU mask of the input (x_in > 0)
+template <int CI, int CO>
+__global__ void __launch_bounds__(128) conv3_dgrad(const float* dy, const float* xin, int m, int hi,
+                                                   int wi, const float* wk, float* dx) {
+  __shared__ float sw[CO * CI * 9];
+  for (int i = threadIdx.x; i < CO * CI * 9; i += blockDim.x) sw[i] = wk[i];
+  __syncthreads();
+  const int ho = hi - 2, wo = wi - 2;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= int64_t(m) * hi * wi) return;
+  const int x = int(p % wi), y = int((p / wi) % hi), b = int(p / (int64_t(wi) * hi));
+  float acc[CI];
+#pragma unroll
+  for (int c = 0; c < CI; ++c) acc[c] = 0.f;
+  for (int o = 0; o < CO; ++o)
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int yy = y - k / 3, xx = x - k % 3;
+      if (yy < 0 || yy >= ho || xx < 0 || xx >= wo) continue;
+      const float g = dy[((int64_t(b) * CO + o) * ho + yy) * wo + xx];
+#pragma unroll
+      for (int c = 0; c < CI; ++c) acc[c] = fmaf(g, sw[(o * CI + c) * 9 + k], acc[c]);
+    }
+#pragma unroll
+  for (int c = 0; c < CI; ++c) {
+    const int64_t q = ((int64_t(b) * CI + c) * hi + y) * wi + x;
+    dx[q] = acc[c] * float(xin[q] > 0.f);
+  }
+}
+
+__global__ void sgd_kernel(float* w, const float* g, int n, float lr, const int32_t* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || (flag && *flag)) return;
+  w[i] = __fsub_rn(w[i], __fmul_rn(lr, g[i]));
+}
+
+unsigned blocks(int64_t n, int t) { return unsigned((n + t - 1) / t); }
+
+int check_dims(int m, int h, int w) {
+  if (m < 1 || h < 7 || w < 7) return ECA_ERR_ARG;
+  if (int64_t(m) * h * w > (int64_t(1) << 31) / 32) return ECA_ERR_UNSUPPORTED;
+  return ECA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int eca_train_workspace_bytes(int m, int h, int w, int64_t* bytes) {
+  if (!bytes) return ECA_ERR_ARG;
+  if (const int rc = check_dims(m, h, w)) return rc;
+  *bytes = int64_t(train_ws(m, h, w).total);
+  return ECA_OK;
+}
+
+int eca_edgenet_forward(const float* x, const int32_t* index, int m, int h, int w, const float* net,
+                        void* workspace, int64_t workspace_bytes, float* out_logits, void* stream) {
+  if (const int rc = check_dims(m, h, w)) return rc;
+  if (!x || !net || !workspace) return ECA_ERR_ARG;
+  const TrainWs L = train_ws(m, h, w);
+  if (workspace_bytes < int64_t(L.total)) return ECA_ERR_ARG;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  float* a1 = reinterpret_cast<float*>(ws + L.a1);
+  float* a2 = reinterpret_cast<float*>(ws + L.a2);
+  float* a3 = reinterpret_cast<float*>(ws + L.a3);
+  float* logit = reinterpret_cast<float*>(ws + L.logit);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  conv3_fwd<5, 8><<<blocks(int64_t(m) * (h - 2) * (w - 2), 128), 128, 0, st>>>(
+      x, index, m, h, w, net + kOffW0, net + kOffB0, a1);
+  conv3_fwd<8, 16><<<blocks(int64_t(m) * (h - 4) * (w - 4), 128), 128, 0, st>>>(
+      a1, nullptr, m, h - 2, w - 2, net + kOffW1, net + kOffB1, a2);
+  conv3_fwd<16, 32><<<blocks(int64_t(m) * (h - 6) * (w - 6), 128), 128, 0, st>>>(
+      a2, nullptr, m, h - 4, w - 4, net + kOffW2, net + kOffB2, a3);
+  const int64_t plane = int64_t(h - 6) * (w - 6);
+  head_fwd<<<blocks(m * plane, 128), 128, 0, st>>>(a3, plane, m, net, logit);
+  if (out_logits)
+    cudaMemcpyAsync(out_logits, logit, sizeof(float) * size_t(m * plane), cudaMemcpyDeviceToDevice, st);
+  return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
+}
+
+int eca_edgenet_backward(const float* x, const float* targets, const int32_t* index, int m, int h,
+                         int w, const float* net, void* workspace, int64_t workspace_bytes,
+                         float* out_grads, double* out_loss, int32_t* diverged, void* stream) {
+  if (const int rc = check_dims(m, h, w)) return rc;
+  if (!x || !targets || !net || !workspace || !out_loss) return ECA_ERR_ARG;
+  const TrainWs L = train_ws(m, h, w);
+  if (workspace_bytes < int64_t(L.total)) return ECA_ERR_ARG;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  auto f = [&](size_t o) { return reinterpret_cast<float*>(ws + o); };
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t plane = int64_t(h - 6) * (w - 6), n = int64_t(m) * plane;
+  double* lpart = reinterpret_cast<double*>(ws + L.lpart);
+  loss_kernel<<<L.nlblk, kLossThreads, 0, st>>>(f(L.logit), targets, index, m, plane, f(L.dlog), lpart);
+  loss_final<<<1, 256, 0, st>>>(lpart, L.nlblk, n, out_loss, diverged);
+  if (!out_grads) return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;   // loss only
+  // head (1x1, 32 -> 1)
+  float* part = f(L.wpart);
+  float* p3 = part;
+  float* p2 = p3 + size_t(L.nseg3) * 33;
+  float* p1 = p2 + size_t(L.nseg2) * (4608 + 32);
+  float* p0 = p1 + size_t(L.nseg1) * (1152 + 16);
+  conv_wgrad<32, 1, 1><<<L.nseg3, 256, 0, st>>>(f(L.dlog), f(L.a3), nullptr, m, h - 6, w - 6, p3);
+  wgrad_reduce<<<1, 64, 0, st>>>(p3, L.nseg3, 32, out_grads + kOffW3, out_grads + kOffB3, 1);
+  head_dgrad<<<blocks(n, 128), 128, 0, st>>>(f(L.dlog), f(L.a3), plane, m, net, f(L.d3));
+  // layer 2 (16 -> 32)
+  conv_wgrad<16, 32, 3><<<L.nseg2, 256, 0, st>>>(f(L.d3), f(L.a2), nullptr, m, h - 4, w - 4, p2);
+  wgrad_reduce<<<blocks(4608 + 32, 256), 256, 0, st>>>(p2, L.nseg2, 4608, out_grads + kOffW2,
+                                                       out_grads + kOffB2, 32);
+  conv3_dgrad<16, 32><<<blocks(int64_t(m) * (h - 4) * (w - 4), 128), 128, 0, st>>>(
+      f(L.d3), f(L.a2), m, h - 4, w - 4, net + kOffW2, f(L.d2));
+  // layer 1 (8 -> 16)
+  conv_wgrad<8, 16, 3><<<L.nseg1, 256, 0, st>>>(f(L.d2), f(L.a1), nullptr, m, h - 2, w - 2, p1);
+  wgrad_reduce<<<blocks(1152 + 16, 256), 256, 0, st>>>(p1, L.nseg1, 1152, out_grads + kOffW1,
+                                                       out_grads + kOffB1, 16);
+  conv3_dgrad<8, 16><<<blocks(int64_t(m) * (h - 2) * (w - 2), 128), 128, 0, st>>>(
+      f(L.d2), f(L.a1), m, h - 2, w - 2, net + kOffW1, f(L.d1));
+  // layer 0 (5 -> 8): weights only (the input gradient is not needed)
+  conv_wgrad<5, 8, 3><<<L.nseg0, 256, 0, st>>>(f(L.d1), x, index, m, h, w, p0);
+  wgrad_reduce<<<blocks(360 + 8, 256), 256, 0, st>>>(p0, L.nseg0, 360, out_grads + kOffW0,
+                                                     out_grads + kOffB0, 8);
+  return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
+}
+
+int eca_sgd_step(float* net, const float* grads, float lr, const int32_t* diverged, void* stream) {
+  if (!net || !grads) return ECA_ERR_ARG;
+  sgd_kernel<<<blocks(kNetN, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(net, grads, kNetN, lr,
+                                                                              diverged);
+  return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
+}
+
+}  // extern "C"

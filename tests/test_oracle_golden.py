@@ -152,3 +152,43 @@ def test_oracle_hausdorff_matches_reference():
         assert orc.hausdorff(bp, bt) == c["hd"], (i, c)
         if c["spacing"] == 1.0:
             assert orc.area_error_px(_circ(c["pred"]), _circ(c["truth"]), c["w"], c["h"]) == c["nh"]
+
+
+# ---- learned training row: edgenet.py training restated in the oracle
+def train_inputs(m=24, h=7, w=64, seed=5):
+    """Same recipe as tests/golden/make_golden_train.py."""
+    rng = np.random.default_rng(seed)
+    x = rng.normal(0.0, 1.0, (m, 5, h, w)).astype(np.float32)
+    t = rng.uniform(0.0, 1.0, (m, 1, h - 6, w - 6)).astype(np.float32)
+    return x, t
+
+
+def _pack(layers):
+    return np.concatenate([np.concatenate([k.ravel(), b.ravel()]) for k, b in layers]).astype(np.float32)
+
+
+def test_oracle_training_step_matches_reference():
+    g = load_npz("train.npz")
+    layers = orc.glorot_layers(0)
+    assert np.array_equal(_pack(layers), g["w0"])
+    x, t = train_inputs()
+    logits, _ = orc.forward_logits(x[:8], layers)
+    assert np.array_equal(logits, g["logits"])
+    loss, grads, _ = orc.train_step(x[:8], t[:8], layers, 0.0)
+    assert loss == g["loss"][0]
+    assert np.array_equal(_pack(grads), g["grads"])
+
+
+def test_oracle_train_loop_matches_reference():
+    g = load_npz("train.npz")
+    x, t = train_inputs()
+    xv, tv = train_inputs(m=10, seed=6)
+    best, tl, vl, be = orc.train(orc.glorot_layers(0), x, t, xv, tv, lr=0.05, batch=4, patience=2,
+                                 epochs=6, seed=3)
+    assert tl == g["train_losses"].tolist() and vl == g["val_losses"].tolist()
+    assert be == g["best_epoch"][0]
+    assert np.array_equal(_pack(best), g["w_trained"])
+    best, tl, _, _ = orc.train(orc.glorot_layers(0), x, t, None, None, lr=0.02, batch=5, epochs=2,
+                               shuffle=False)
+    assert tl == g["train_losses_noval"].tolist()
+    assert np.array_equal(_pack(best), g["w_noval"])
