@@ -233,50 +233,44 @@ __global__ void __launch_bounds__(256, 2) cnn_kernel(const __grid_constant__ Cnn
 
 
 // ---------------------------------------------------------------------------
-// Tensor-core variant (ECA_LEARNED_TCGEN05): the same network with layer 2 on
-// tcgen05.  Measured on B200, 256 x 1080p: 7.5 ms against 6.2 ms for the SIMT
-// kernel above -- building the im2col operand and waiting for the per-piece
-// MMAs costs more than layer 2's FMAs, and layers 0-1 stay SIMT at one
-// 512-thread CTA per SM.  Kept as a parity-tested option; chaining all three
-// layers through TMEM is the step that would make it pay.
-// Layer 2 (16 -> 32 channels, K = 16*3*3 = 144) runs on the tensor cores:
-// per tile D[128 columns][32 channels] = im2col(o2)[128][144] . W2^T, tcgen05
-// kind::tf32 with a 3xTF32 split (hi*hi + hi*lo + lo*hi, FP32-level error
-// ~2e-6, tools/umma_test.cu), FP32 accumulators in TMEM.  Operands sit in
-// shared memory in the K-major no-swizzle canonical layout: 8-row x 16-byte
-// core matrices, LBO = 128 B between K chunks, SBO between 8-row groups.
-// The im2col operand is built in K-ninths (16 K each), double-buffered so one
-// ninth is written while the tensor core consumes the other, in shared memory
-// aliased over the input / layer-0 buffers (dead during layer 2): the CTA stays
-// under 113 KB, two CTAs per SM.
-#ifndef ECA_CNN_NO_MMA   // diagnostic: skip the MMAs (wrong results), time the rest
-#define ECA_CNN_NO_MMA 0
-#endif
-constexpr int kK2 = 144, kK2p = 16;             // layer-2 K, per built piece
-constexpr int kSboA = (kK2p / 4) * 128;         // 512 B
-constexpr int kSboB = (kK2 / 4) * 128;          // 4608 B
-constexpr int kAPiece = kTX * kK2p * 4;         // 8 KB (hi or lo)
+// Tensor-core variant (ECA_LEARNED_TCGEN05): layers 1 and 2 (8->16 and
+// 16->32 channels, 81 % of the network's FLOPs) on tcgen05, layer 0 (5->8)
+// and the head on the CUDA cores, one 512-thread CTA per SM, one tile of
+// kTP = 128 positions of one strip at a time.
+//
+// No im2col.  A 3x3 valid conv is 9 shifted GEMMs; the vertical shift (ky)
+// selects an input ROW (each row is its own K-major operand), and the
+// horizontal shift (kx) is moved to the output: accumulator D[kx][m] =
+// sum_ky sum_c in[row + ky][m][c] * W[ky][kx][c] over the UNshifted positions
+// m, and out[m] = D[0][m] + D[1][m + 1] + D[2][m + 2], combined in the
+// epilogue with warp shuffles (lanes 30/31 take their neighbours from the next
+// warp through shared memory).  Each layer input is written once, by the
+// previous layer's epilogue, straight into the canonical K-major operand
+// layout (8-row x 16-byte core matrices), split hi/lo for 3xTF32
+// (hi*hi + hi*lo + lo*hi: FP32-level error, tools/umma_test.cu).  128 MMA
+// positions give 124 valid outputs per tile (the 3x3 halo of two layers).
+//   layer 1: 3 output rows x 3 kx accumulators (N = 16), 3 ky x 3 terms each
+//   layer 2: 3 kx accumulators (N = 32), 3 ky x 2 K-steps x 3 terms each
+// TMEM: layer 1 columns [0, 144), layer 2 columns [160, 256).
+constexpr int kTP = 128, kTOut = kTP - 4;
+constexpr int kSbo1 = 2 * 128, kSbo2 = 4 * 128;       // K = 8 / 16 channels
+constexpr int kA1 = 16 * kSbo1, kA2 = 16 * kSbo2;     // one row operand (128 positions)
+constexpr int kWt1 = 2 * kSbo1, kWt2 = 4 * kSbo2;     // one (ky, kx) weight operand
 
 struct CnnSmemTc {
-  union {   // 1024-byte aligned (kernel smem base): descriptor addresses are 16-byte units
-    struct {                      // layers 0-1
-      float in[5][7][kTX + 8];
-      float o1[8][5][kTX + 4];
-    } l01;
-    uint8_t a[2][2][kAPiece];     // layer 2: [buffer][hi, lo] im2col piece
-  } u;
-  uint8_t b_hi[32 * kK2 * 4];     // layer-2 weights [out][k] (reference order = K-major)
-  uint8_t b_lo[32 * kK2 * 4];
-  // layers 0-1: weights transposed to [in][ky][kx][out] so one position reads out-vectors
-  float4 w0[5 * 9 * 2];
-  float4 w1[8 * 9 * 4];
-  int koff[kK2];                  // layer-2 k -> offset of o2[ci][ky][kx] (column 0)
-  uint64_t bar[2];                // MMA completion per A buffer
-  uint32_t tmem;                  // TMEM base address (32 columns)
-  float b0[8], b1[16], b2[32], w3[32], b3;
-  float o2[16][3][kTX + 2];
-  float lut[3][256];             // float((v - mean_c) / std_c), computed in FP64
-  float ybuf[32][kTX];           // layer-2 outputs after bias + ReLU
+  uint8_t a1[5][2][kA1];          // layer-1 input rows (layer-0 output), hi / lo
+  uint8_t a2[3][2][kA2];          // layer-2 input rows (layer-1 output), hi / lo
+  uint8_t b1[9][2][kWt1];         // layer-1 weights [ky*3+kx][out 16][in 8]
+  uint8_t b2[9][2][kWt2];         // layer-2 weights [ky*3+kx][out 32][in 16]
+  float in[5][7][kTP + 8];        // RGBXY window, columns 0 .. kTP+1 used
+  float4 w0[5 * 9 * 2];           // layer-0 weights [in][ky][kx][out]
+  float b0[8], b1v[16], b2v[32], w3[32], b3;
+  float lut[3][256];              // float((v - mean_c) / std_c), computed in FP64
+  float xch1[3][4][2][2][16];     // [row][lane quarter][lane 0/1][kx-1][channel]
+  float xch2[4][2][2][32];
+  float zpart[4][kTP];            // head partial sums per channel group
+  uint64_t bar;                   // MMA completion
+  uint32_t tmem;
 };
 
 ECA_DEV float tf32_rna(float x) {
@@ -292,61 +286,99 @@ ECA_DEV uint64_t umma_desc(uint32_t saddr, int sbo) {
   return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) |
          (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);   // version 1, no swizzle
 }
-// kind::tf32, D F32, A/B TF32 K-major, M = 128, N = 32
-constexpr uint32_t kIdescL2 = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(32 >> 3) << 17) |
-                              (uint32_t(128 >> 4) << 24);
+// kind::tf32, D F32, A/B TF32 K-major, M = 128
+constexpr uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+ECA_DEV void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+// 3xTF32 product accumulated into tmem: hi*hi, hi*lo, lo*hi
+ECA_DEV void mma3(uint32_t tmem, uint32_t a_hi, uint32_t a_lo, int sboa, uint32_t b_hi, uint32_t b_lo,
+                  int sbob, uint32_t idesc, bool first) {
+  mma_tf32(tmem, umma_desc(a_hi, sboa), umma_desc(b_hi, sbob), idesc, first ? 0u : 1u);
+  mma_tf32(tmem, umma_desc(a_hi, sboa), umma_desc(b_lo, sbob), idesc, 1u);
+  mma_tf32(tmem, umma_desc(a_lo, sboa), umma_desc(b_hi, sbob), idesc, 1u);
+}
+ECA_DEV void st_hilo(uint8_t* hi, uint8_t* lo, int off, float4 v) {
+  float4 h, l;
+  h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
+  h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
+  h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
+  h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
+  *reinterpret_cast<float4*>(hi + off) = h;
+  *reinterpret_cast<float4*>(lo + off) = l;
+}
+template <int N>
+ECA_DEV void tmem_ld(uint32_t addr, float* v);
+template <>
+ECA_DEV void tmem_ld<4>(uint32_t addr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <>
+ECA_DEV void tmem_ld<8>(uint32_t addr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(addr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+ECA_DEV void bar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nECA_MW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra ECA_MW;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// st.shared by all threads -> visible to the tensor core; all threads past the barrier
+ECA_DEV void publish_operands() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
 
-// 512 threads, one CTA per SM (the occupancy API grants this kernel one)
 __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ CnnJob J) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   CnnSmemTc& s = *reinterpret_cast<CnnSmemTc*>(smem_raw);
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int W = J.W, H = J.H;
   const float* wg = J.weights;
 
-  // ---- weights -> smem (transposed) ----
+  // ---- weights -> smem: layer 0 transposed for the CUDA cores, layers 1-2
+  // as K-major hi/lo operands [ky*3+kx][out][in] ----
   float* w0f = reinterpret_cast<float*>(s.w0);
-  float* w1f = reinterpret_cast<float*>(s.w1);
   for (int i = tid; i < kW0; i += nt) {  // i = ((o*5 + c)*3 + ky)*3 + kx
     const int o = i / 45, r = i % 45;
     w0f[r * 8 + o] = wg[i];
   }
-  for (int i = tid; i < kW1; i += nt) {
-    const int o = i / 72, r = i % 72;
-    w1f[r * 16 + o] = wg[kOffW1 + i];
+  for (int i = tid; i < kW1; i += nt) {   // i = ((o*8 + c)*3 + ky)*3 + kx
+    const int o = i / 72, c = (i / 9) % 8, q = i % 9;
+    const float v = wg[kOffW1 + i], hi = tf32_rna(v);
+    *reinterpret_cast<float*>(s.b1[q][0] + kmaj_off(o, c, kSbo1)) = hi;
+    *reinterpret_cast<float*>(s.b1[q][1] + kmaj_off(o, c, kSbo1)) = tf32_rna(v - hi);
   }
-  for (int i = tid; i < kW2; i += nt) {   // i = o*144 + k: already K-major
-    const int o = i / kK2, k = i % kK2;
+  for (int i = tid; i < kW2; i += nt) {   // i = ((o*16 + c)*3 + ky)*3 + kx
+    const int o = i / 144, c = (i / 9) % 16, q = i % 9;
     const float v = wg[kOffW2 + i], hi = tf32_rna(v);
-    *reinterpret_cast<float*>(s.b_hi + kmaj_off(o, k, kSboB)) = hi;
-    *reinterpret_cast<float*>(s.b_lo + kmaj_off(o, k, kSboB)) = tf32_rna(v - hi);
+    *reinterpret_cast<float*>(s.b2[q][0] + kmaj_off(o, c, kSbo2)) = hi;
+    *reinterpret_cast<float*>(s.b2[q][1] + kmaj_off(o, c, kSbo2)) = tf32_rna(v - hi);
   }
-  for (int k = tid; k < kK2; k += nt) {
-    const int ci = k / 9, ky = (k % 9) / 3, kx = k % 3;
-    s.koff[k] = (ci * 3 + ky) * (kTX + 2) + kx;
-  }
-  const int warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    for (int q = 0; q < 2; ++q)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-          static_cast<uint32_t>(__cvta_generic_to_shared(&s.bar[q]))));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
-        static_cast<uint32_t>(__cvta_generic_to_shared(&s.tmem))));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = s.tmem;
-  const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&s.bar[0]));
-  uint32_t mma_phase = 0;   // bit q: parity of buffer q's next completion
   if (tid < 8) s.b0[tid] = wg[kOffB0 + tid];
-  if (tid < 16) s.b1[tid] = wg[kOffB1 + tid];
+  if (tid < 16) s.b1v[tid] = wg[kOffB1 + tid];
   if (tid < 32) {
-    s.b2[tid] = wg[kOffB2 + tid];
+    s.b2v[tid] = wg[kOffB2 + tid];
     s.w3[tid] = wg[kOffW3 + tid];
   }
   if (tid == 0) s.b3 = wg[kOffB3];
@@ -354,33 +386,51 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     const int ch = i >> 8, v = i & 255;
     s.lut[ch][v] = float(div_rn(sub_rn(double(v), J.mean[ch]), J.stdv[ch]));
   }
+  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&s.bar));
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        static_cast<uint32_t>(__cvta_generic_to_shared(&s.tmem))));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  publish_operands();
+  const uint32_t tmem = s.tmem;
+  uint32_t phase = 0;
+  const auto saddr = [](const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); };
+  const int q = warp & 3, g = warp >> 2;          // TMEM lane quarter, channel group
+  const int m = 32 * q + lane;                    // this thread's MMA position
+  const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
+
   const double xden = double(W - 1 > 1 ? W - 1 : 1), yden = double(H - 1 > 1 ? H - 1 : 1);
   const double xc = div_rn(double(W - 1), 2.0), yc = div_rn(double(H - 1), 2.0);
-  const int tiles_x = (W - 6 + kTX - 1) / kTX;
+  const int tiles_x = (W - 6 + kTOut - 1) / kTOut;
   const int n_tiles = tiles_x * J.S * J.batch;
 
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
   const int tx = t % tiles_x, fs = t / tiles_x;
   const int strip = fs % J.S, b = fs / J.S;
-  const int j0 = tx * kTX;               // first output column (frame x = j0 + 3)
-  __syncthreads();                       // previous tile's buffers are free; tables ready
+  const int j0 = tx * kTOut;              // first output column (frame x = j0 + 3)
+  __syncthreads();                        // previous tile's buffers are free
 
-  // ---- RGBXY window (edgenet.py:75-82), rows h-3..h+3, columns j0..j0+kTX+5 ----
+  // ---- RGBXY window (edgenet.py:75-82), rows h-3..h+3, columns j0..j0+kTP+1 ----
   const int h = J.rows[strip];
   const int band = J.band[strip];
   const uint8_t* fb = J.frames + int64_t(b) * J.fstride;
-  for (int c = tid; c < kTX + 6; c += nt) {   // X channel: one FP64 division per column
+  for (int c = tid; c < kTP + 2; c += nt) {
     const int x = j0 + c;
     const float fx = x < W ? float(div_rn(sub_rn(double(x), xc), xden)) : 0.f;
 #pragma unroll
-    for (int r = 0; r < 7; ++r) s.u.l01.in[3][r][c] = fx;
+    for (int r = 0; r < 7; ++r) s.in[3][r][c] = fx;
   }
   if (tid < 7) {
     const float fy = float(div_rn(sub_rn(double(h - 3 + tid), yc), yden));
-    for (int c = 0; c < kTX + 6; ++c) s.u.l01.in[4][tid][c] = j0 + c < W ? fy : 0.f;
+    for (int c = 0; c < kTP + 2; ++c) s.in[4][tid][c] = j0 + c < W ? fy : 0.f;
   }
-  for (int i = tid; i < 7 * (kTX + 6); i += nt) {
-    const int r = i / (kTX + 6), c = i % (kTX + 6);
+  for (int i = tid; i < 7 * (kTP + 2); i += nt) {
+    const int r = i / (kTP + 2), c = i % (kTP + 2);
     const int x = j0 + c;
     float f0 = 0.f, f1 = 0.f, f2 = 0.f;
     if (x < W) {
@@ -389,148 +439,138 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
       f1 = s.lut[1][px[1]];
       f2 = s.lut[2][px[2]];
     }
-    s.u.l01.in[0][r][c] = f0;
-    s.u.l01.in[1][r][c] = f1;
-    s.u.l01.in[2][r][c] = f2;
+    s.in[0][r][c] = f0;
+    s.in[1][r][c] = f1;
+    s.in[2][r][c] = f2;
   }
   __syncthreads();
 
-  // ---- layer 0: 5 -> 8, rows 7 -> 5 ----
-  for (int i = tid; i < 5 * (kTX + 4); i += nt) {
-    const int r = i / (kTX + 4), c = i % (kTX + 4);
+  // ---- layer 0 (CUDA cores): 5 -> 8, rows 7 -> 5, positions 0..127, written
+  // as the layer-1 operand rows ----
+  for (int i = tid; i < 5 * kTP; i += nt) {
+    const int r = i / kTP, c = i % kTP;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int ci = 0; ci < 5; ++ci)
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
-        const float v = s.u.l01.in[ci][r + k / 3][c + k % 3];
+        const float v = s.in[ci][r + k / 3][c + k % 3];
         const float4 wa = s.w0[(ci * 9 + k) * 2], wb = s.w0[(ci * 9 + k) * 2 + 1];
         acc[0] = fmaf(wa.x, v, acc[0]); acc[1] = fmaf(wa.y, v, acc[1]);
         acc[2] = fmaf(wa.z, v, acc[2]); acc[3] = fmaf(wa.w, v, acc[3]);
         acc[4] = fmaf(wb.x, v, acc[4]); acc[5] = fmaf(wb.y, v, acc[5]);
         acc[6] = fmaf(wb.z, v, acc[6]); acc[7] = fmaf(wb.w, v, acc[7]);
       }
+    float y[8];
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
-      const float y = acc[o] + s.b0[o];
-      s.u.l01.o1[o][r][c] = y > 0.f ? y : 0.f;
+      const float v = acc[o] + s.b0[o];
+      y[o] = v > 0.f ? v : 0.f;
     }
+    st_hilo(s.a1[r][0], s.a1[r][1], kmaj_off(c, 0, kSbo1), make_float4(y[0], y[1], y[2], y[3]));
+    st_hilo(s.a1[r][0], s.a1[r][1], kmaj_off(c, 4, kSbo1), make_float4(y[4], y[5], y[6], y[7]));
   }
-  __syncthreads();
+  publish_operands();
 
-  // ---- layer 1: 8 -> 16, rows 5 -> 3 ----
-  for (int i = tid; i < 3 * (kTX + 2); i += nt) {
-    const int r = i / (kTX + 2), c = i % (kTX + 2);
-    float acc[16];
-#pragma unroll
-    for (int o = 0; o < 16; ++o) acc[o] = 0.f;
-    for (int ci = 0; ci < 8; ++ci)
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const float v = s.u.l01.o1[ci][r + k / 3][c + k % 3];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 w = s.w1[(ci * 9 + k) * 4 + q];
-          acc[4 * q + 0] = fmaf(w.x, v, acc[4 * q + 0]);
-          acc[4 * q + 1] = fmaf(w.y, v, acc[4 * q + 1]);
-          acc[4 * q + 2] = fmaf(w.z, v, acc[4 * q + 2]);
-          acc[4 * q + 3] = fmaf(w.w, v, acc[4 * q + 3]);
-        }
-      }
-#pragma unroll
-    for (int o = 0; o < 16; ++o) {
-      const float y = acc[o] + s.b1[o];
-      s.o2[o][r][c] = y > 0.f ? y : 0.f;
-    }
+  // ---- layer 1 (tensor cores): D1[r][kx] = sum_ky a1[r + ky] . b1[ky][kx] ----
+  if (tid == 0) {
+    constexpr uint32_t id1 = idesc_tf32(16);
+    for (int r = 0; r < 3; ++r)
+      for (int kx = 0; kx < 3; ++kx)
+        for (int ky = 0; ky < 3; ++ky)
+          mma3(tmem + uint32_t((r * 3 + kx) * 16), saddr(s.a1[r + ky][0]), saddr(s.a1[r + ky][1]), kSbo1,
+               saddr(s.b1[ky * 3 + kx][0]), saddr(s.b1[ky * 3 + kx][1]), kSbo1, id1, ky == 0);
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
   }
-  __syncthreads();
-
-  // ---- layer 2 on the tensor cores: 9 pieces of im2col(o2), 6 MMAs each ----
-  auto wait_buf = [&](int q) {
-    asm volatile(
-        "{\n.reg .pred P1;\nECA_MW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra ECA_MW;\n}\n" ::"r"(bar0 + 8u * uint32_t(q)),
-        "r"((mma_phase >> q) & 1u)
-        : "memory");
-    mma_phase ^= 1u << q;
-  };
-  for (int piece = 0; piece < kK2 / kK2p; ++piece) {
-    const int q = piece & 1;
-    if (piece >= 2) wait_buf(q);         // the MMAs of piece - 2 have read this buffer
-    // one warp per 8x4 core matrix: lane = (row & 7) * 4 + (k & 3), so a warp
-    // writes 128 contiguous bytes
-    const int r8 = lane >> 2, c4 = lane & 3;
-    uint8_t* ahi = s.u.a[q][0];
-    uint8_t* alo = s.u.a[q][1];
-    for (int cm = warp; cm < (kTX / 8) * (kK2p / 4); cm += nt >> 5) {
-      const int mi = cm / (kK2p / 4), kc = cm % (kK2p / 4);
-      const int m = mi * 8 + r8, kk = kc * 4 + c4;
-      const float v = (&s.o2[0][0][0])[s.koff[piece * kK2p + kk] + m];
-      const float hi = tf32_rna(v);
-      const int off = mi * kSboA + kc * 128 + lane * 4;
-      *reinterpret_cast<float*>(ahi + off) = hi;
-      *reinterpret_cast<float*>(alo + off) = tf32_rna(v - hi);
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // st.shared -> tensor core
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (tid == 0) {
-      const uint32_t ah = static_cast<uint32_t>(__cvta_generic_to_shared(ahi));
-      const uint32_t al = static_cast<uint32_t>(__cvta_generic_to_shared(alo));
-      const uint32_t bh = static_cast<uint32_t>(__cvta_generic_to_shared(s.b_hi));
-      const uint32_t bl = static_cast<uint32_t>(__cvta_generic_to_shared(s.b_lo));
-#pragma unroll
-      for (int j = 0; j < kK2p / 8; ++j) {   // 8 tf32 (32 bytes) of K per instruction
-        const uint32_t oa = uint32_t(j) * 256u;
-        const uint32_t ob = uint32_t(piece * (kK2p / 8) + j) * 256u;
-        const uint64_t da[3] = {umma_desc(ah + oa, kSboA), umma_desc(ah + oa, kSboA),
-                                umma_desc(al + oa, kSboA)};
-        const uint64_t db[3] = {umma_desc(bh + ob, kSboB), umma_desc(bl + ob, kSboB),
-                                umma_desc(bh + ob, kSboB)};
-#pragma unroll
-        for (int t3 = 0; t3 < (ECA_CNN_NO_MMA ? 0 : 3); ++t3) {
-          const uint32_t accum = (piece > 0 || j > 0 || t3 > 0) ? 1u : 0u;
-          asm volatile(
-              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-              "l"(da[t3]), "l"(db[t3]), "r"(kIdescL2), "r"(accum));
-        }
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       bar0 + 8u * uint32_t(q))
-                   : "memory");
-    }
-  }
-  // the last two pieces (buffers 1 and 0) have completed: accumulators final,
-  // the aliased input buffers free again
-  wait_buf(1);
-  wait_buf(0);
+  bar_wait(bar, phase);
+  phase ^= 1u;
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // accumulators -> registers: warp w reads TMEM lanes 32*(w%4).. (output
-  // columns) and channels 8*(w/4) .. 8*(w/4)+7; bias + ReLU into ybuf, then the
-  // 1x1 head sums the 32 channels in order
+
+  // ---- layer-1 epilogue: o2[r][m] = D[0][m] + D[1][m+1] + D[2][m+2] + b1,
+  // ReLU, as the layer-2 operand rows; warp (q, g): positions 32q.., channels 4g.. ----
   {
-    const int g = warp >> 2, c = (warp & 3) * 32 + lane;
-    uint32_t v[8];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7])
-        : "r"(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(8 * g)));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float d[3][3][4];
 #pragma unroll
-    for (int o = 0; o < 8; ++o) {
-      const float y = __uint_as_float(v[o]) + s.b2[8 * g + o];
-      s.ybuf[8 * g + o][c] = y > 0.f ? y : 0.f;
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) tmem_ld<4>(lane_base + uint32_t((r * 3 + kx) * 16 + 4 * g), d[r][kx]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (lane < 2) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) s.xch1[r][q][lane][k][4 * g + c] = d[r][k + 1][c];
     }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      float y[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float v1 = __shfl_down_sync(kFull, d[r][1][c], 1);
+        float v2 = __shfl_down_sync(kFull, d[r][2][c], 2);
+        if (q < 3) {
+          if (lane == 31) v1 = s.xch1[r][q + 1][0][0][4 * g + c];
+          if (lane >= 30) v2 = s.xch1[r][q + 1][lane - 30][1][4 * g + c];
+        }
+        const float v = (d[r][0][c] + v1) + v2 + s.b1v[4 * g + c];
+        y[c] = v > 0.f ? v : 0.f;
+      }
+      st_hilo(s.a2[r][0], s.a2[r][1], kmaj_off(m, 4 * g, kSbo2), make_float4(y[0], y[1], y[2], y[3]));
+    }
+  }
+  publish_operands();
+
+  // ---- layer 2 (tensor cores): D2[kx] = sum_ky a2[ky] . b2[ky][kx], K = 16 ----
+  if (tid == 0) {
+    constexpr uint32_t id2 = idesc_tf32(32);
+    for (int kx = 0; kx < 3; ++kx)
+      for (int ky = 0; ky < 3; ++ky)
+        for (int j = 0; j < 2; ++j)   // 8 channels (32 bytes of K) per instruction
+          mma3(tmem + uint32_t(160 + kx * 32), saddr(s.a2[ky][0]) + 256u * j, saddr(s.a2[ky][1]) + 256u * j,
+               kSbo2, saddr(s.b2[ky * 3 + kx][0]) + 256u * j, saddr(s.b2[ky * 3 + kx][1]) + 256u * j,
+               kSbo2, id2, ky == 0 && j == 0);
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+  }
+  bar_wait(bar, phase);
+  phase ^= 1u;
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  // ---- layer-2 epilogue + head: channels 8g..8g+7 per warp, partial head
+  // sums per channel group, then the sigmoid ----
+  {
+    float d[3][8];
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) tmem_ld<8>(lane_base + uint32_t(160 + kx * 32 + 8 * g), d[kx]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (lane < 2) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) s.xch2[q][lane][k][8 * g + c] = d[k + 1][c];
+    }
+    __syncthreads();
+    float z = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float v1 = __shfl_down_sync(kFull, d[1][c], 1);
+      float v2 = __shfl_down_sync(kFull, d[2][c], 2);
+      if (q < 3) {
+        if (lane == 31) v1 = s.xch2[q + 1][0][0][8 * g + c];
+        if (lane >= 30) v2 = s.xch2[q + 1][lane - 30][1][8 * g + c];
+      }
+      const float v = (d[0][c] + v1) + v2 + s.b2v[8 * g + c];
+      z = fmaf(s.w3[8 * g + c], v > 0.f ? v : 0.f, z);
+    }
+    s.zpart[g][m] = z;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (tid < kTX) {
-    float z = 0.f;
-#pragma unroll
-    for (int o = 0; o < 32; ++o) z = fmaf(s.w3[o], s.ybuf[o][tid], z);
-    z += s.b3;
+  if (tid < kTOut) {
+    const float z = ((s.zpart[0][tid] + s.zpart[1][tid]) + (s.zpart[2][tid] + s.zpart[3][tid])) + s.b3;
     const int j = j0 + tid;
     if (j < W - 6) {
       float p;
@@ -546,7 +586,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
 // half-row winners of the zero-padded probability row (edgenet.py:363-369)
