@@ -249,8 +249,9 @@ __global__ void __launch_bounds__(256, 2) cnn_kernel(const __grid_constant__ Cnn
 // layout (8-row x 16-byte core matrices), split hi/lo for 3xTF32
 // (hi*hi + hi*lo + lo*hi: FP32-level error, tools/umma_test.cu).  128 MMA
 // positions give 124 valid outputs per tile (the 3x3 halo of two layers).
-//   layer 1: 3 output rows x 3 kx accumulators (N = 16), 3 ky x 3 terms each
-//   layer 2: 3 kx accumulators (N = 32), 3 ky x 2 K-steps x 3 terms each
+//   layer 1: per output row one N = 48 MMA chain (the 3 kx weight blocks
+//            stacked as rows of B): 3 ky x 3 split terms, 27 MMAs
+//   layer 2: one N = 96 chain: 3 ky x 2 K-steps x 3 terms, 18 MMAs
 // TMEM: layer 1 columns [0, 144), layer 2 columns [160, 256).
 constexpr int kTP = 128, kTOut = kTP - 4;
 constexpr int kSbo1 = 2 * 128, kSbo2 = 4 * 128;       // K = 8 / 16 channels
@@ -260,8 +261,8 @@ constexpr int kWt1 = 2 * kSbo1, kWt2 = 4 * kSbo2;     // one (ky, kx) weight ope
 struct CnnSmemTc {
   uint8_t a1[5][2][kA1];          // layer-1 input rows (layer-0 output), hi / lo
   uint8_t a2[3][2][kA2];          // layer-2 input rows (layer-1 output), hi / lo
-  uint8_t b1[9][2][kWt1];         // layer-1 weights [ky*3+kx][out 16][in 8]
-  uint8_t b2[9][2][kWt2];         // layer-2 weights [ky*3+kx][out 32][in 16]
+  uint8_t b1[2][3][3][kWt1];      // layer-1 weights [hi/lo][ky][kx][out 16][in 8]
+  uint8_t b2[2][3][3][kWt2];      // layer-2 weights [hi/lo][ky][kx][out 32][in 16]
   float in[5][7][kTP + 8];        // RGBXY window, columns 0 .. kTP+1 used
   float4 w0[5 * 9 * 2];           // layer-0 weights [in][ky][kx][out]
   float b0[8], b1v[16], b2v[32], w3[32], b3;
@@ -364,16 +365,16 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     w0f[r * 8 + o] = wg[i];
   }
   for (int i = tid; i < kW1; i += nt) {   // i = ((o*8 + c)*3 + ky)*3 + kx
-    const int o = i / 72, c = (i / 9) % 8, q = i % 9;
+    const int o = i / 72, c = (i / 9) % 8, ky = (i % 9) / 3, kx = i % 3;
     const float v = wg[kOffW1 + i], hi = tf32_rna(v);
-    *reinterpret_cast<float*>(s.b1[q][0] + kmaj_off(o, c, kSbo1)) = hi;
-    *reinterpret_cast<float*>(s.b1[q][1] + kmaj_off(o, c, kSbo1)) = tf32_rna(v - hi);
+    *reinterpret_cast<float*>(s.b1[0][ky][kx] + kmaj_off(o, c, kSbo1)) = hi;
+    *reinterpret_cast<float*>(s.b1[1][ky][kx] + kmaj_off(o, c, kSbo1)) = tf32_rna(v - hi);
   }
   for (int i = tid; i < kW2; i += nt) {   // i = ((o*16 + c)*3 + ky)*3 + kx
-    const int o = i / 144, c = (i / 9) % 16, q = i % 9;
+    const int o = i / 144, c = (i / 9) % 16, ky = (i % 9) / 3, kx = i % 3;
     const float v = wg[kOffW2 + i], hi = tf32_rna(v);
-    *reinterpret_cast<float*>(s.b2[q][0] + kmaj_off(o, c, kSbo2)) = hi;
-    *reinterpret_cast<float*>(s.b2[q][1] + kmaj_off(o, c, kSbo2)) = tf32_rna(v - hi);
+    *reinterpret_cast<float*>(s.b2[0][ky][kx] + kmaj_off(o, c, kSbo2)) = hi;
+    *reinterpret_cast<float*>(s.b2[1][ky][kx] + kmaj_off(o, c, kSbo2)) = tf32_rna(v - hi);
   }
   if (tid < 8) s.b0[tid] = wg[kOffB0 + tid];
   if (tid < 16) s.b1v[tid] = wg[kOffB1 + tid];
@@ -409,6 +410,32 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   const int tiles_x = (W - 6 + kTOut - 1) / kTOut;
   const int n_tiles = tiles_x * J.S * J.batch;
 
+  // the RGB bytes of a tile's window, 2 pixels per thread, loaded one tile
+  // ahead (issued under the previous tile's tensor-core work)
+  constexpr int kWinPx = 7 * (kTP + 2);
+  static_assert(kWinPx <= 2 * 512, "two window pixels per thread");
+  uint32_t px_next[2] = {0u, 0u};
+  auto load_window = [&](int t) {
+    if (t >= n_tiles) return;
+    const int tx = t % tiles_x, fs = t / tiles_x;
+    const int strip = fs % J.S, b = fs / J.S;
+    const uint8_t* fb = J.frames + int64_t(b) * J.fstride;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = tid + k * nt;
+      uint32_t v = 0u;
+      if (i < kWinPx) {
+        const int r = i / (kTP + 2), c = i % (kTP + 2), x = tx * kTOut + c;
+        if (x < W) {
+          const uint8_t* px = fb + int64_t(J.band[strip] + r) * J.rstride + 3 * x;
+          v = uint32_t(__ldg(px)) | (uint32_t(__ldg(px + 1)) << 8) | (uint32_t(__ldg(px + 2)) << 16);
+        }
+      }
+      px_next[k] = v;
+    }
+  };
+  load_window(blockIdx.x);
+
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
   const int tx = t % tiles_x, fs = t / tiles_x;
   const int strip = fs % J.S, b = fs / J.S;
@@ -417,8 +444,18 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
 
   // ---- RGBXY window (edgenet.py:75-82), rows h-3..h+3, columns j0..j0+kTP+1 ----
   const int h = J.rows[strip];
-  const int band = J.band[strip];
-  const uint8_t* fb = J.frames + int64_t(b) * J.fstride;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = tid + k * nt;
+    if (i < kWinPx) {
+      const int r = i / (kTP + 2), c = i % (kTP + 2);
+      const uint32_t v = px_next[k];
+      const bool in_frame = j0 + c < W;
+      s.in[0][r][c] = in_frame ? s.lut[0][v & 255u] : 0.f;
+      s.in[1][r][c] = in_frame ? s.lut[1][(v >> 8) & 255u] : 0.f;
+      s.in[2][r][c] = in_frame ? s.lut[2][(v >> 16) & 255u] : 0.f;
+    }
+  }
   for (int c = tid; c < kTP + 2; c += nt) {
     const int x = j0 + c;
     const float fx = x < W ? float(div_rn(sub_rn(double(x), xc), xden)) : 0.f;
@@ -428,20 +465,6 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   if (tid < 7) {
     const float fy = float(div_rn(sub_rn(double(h - 3 + tid), yc), yden));
     for (int c = 0; c < kTP + 2; ++c) s.in[4][tid][c] = j0 + c < W ? fy : 0.f;
-  }
-  for (int i = tid; i < 7 * (kTP + 2); i += nt) {
-    const int r = i / (kTP + 2), c = i % (kTP + 2);
-    const int x = j0 + c;
-    float f0 = 0.f, f1 = 0.f, f2 = 0.f;
-    if (x < W) {
-      const uint8_t* px = fb + int64_t(band + r) * J.rstride + 3 * x;
-      f0 = s.lut[0][px[0]];
-      f1 = s.lut[1][px[1]];
-      f2 = s.lut[2][px[2]];
-    }
-    s.in[0][r][c] = f0;
-    s.in[1][r][c] = f1;
-    s.in[2][r][c] = f2;
   }
   __syncthreads();
 
@@ -471,17 +494,19 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   }
   publish_operands();
 
-  // ---- layer 1 (tensor cores): D1[r][kx] = sum_ky a1[r + ky] . b1[ky][kx] ----
+  // ---- layer 1 (tensor cores): D1[r][kx] = sum_ky a1[r + ky] . b1[ky][kx];
+  // the three kx weight blocks are adjacent rows of one N = 48 operand, so one
+  // MMA per (row, ky, split term) fills all three kx accumulators ----
   if (tid == 0) {
-    constexpr uint32_t id1 = idesc_tf32(16);
+    constexpr uint32_t id1 = idesc_tf32(48);
     for (int r = 0; r < 3; ++r)
-      for (int kx = 0; kx < 3; ++kx)
-        for (int ky = 0; ky < 3; ++ky)
-          mma3(tmem + uint32_t((r * 3 + kx) * 16), saddr(s.a1[r + ky][0]), saddr(s.a1[r + ky][1]), kSbo1,
-               saddr(s.b1[ky * 3 + kx][0]), saddr(s.b1[ky * 3 + kx][1]), kSbo1, id1, ky == 0);
+      for (int ky = 0; ky < 3; ++ky)
+        mma3(tmem + uint32_t(r * 48), saddr(s.a1[r + ky][0]), saddr(s.a1[r + ky][1]), kSbo1,
+             saddr(s.b1[0][ky][0]), saddr(s.b1[1][ky][0]), kSbo1, id1, ky == 0);
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
   }
+  load_window(t + gridDim.x);   // the next tile's bytes arrive under this tile's MMAs
   bar_wait(bar, phase);
   phase ^= 1u;
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -523,15 +548,15 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   }
   publish_operands();
 
-  // ---- layer 2 (tensor cores): D2[kx] = sum_ky a2[ky] . b2[ky][kx], K = 16 ----
+  // ---- layer 2 (tensor cores): D2[kx] = sum_ky a2[ky] . b2[ky][kx], K = 16,
+  // the three kx blocks as one N = 96 operand ----
   if (tid == 0) {
-    constexpr uint32_t id2 = idesc_tf32(32);
-    for (int kx = 0; kx < 3; ++kx)
-      for (int ky = 0; ky < 3; ++ky)
-        for (int j = 0; j < 2; ++j)   // 8 channels (32 bytes of K) per instruction
-          mma3(tmem + uint32_t(160 + kx * 32), saddr(s.a2[ky][0]) + 256u * j, saddr(s.a2[ky][1]) + 256u * j,
-               kSbo2, saddr(s.b2[ky * 3 + kx][0]) + 256u * j, saddr(s.b2[ky * 3 + kx][1]) + 256u * j,
-               kSbo2, id2, ky == 0 && j == 0);
+    constexpr uint32_t id2 = idesc_tf32(96);
+    for (int ky = 0; ky < 3; ++ky)
+      for (int j = 0; j < 2; ++j)   // 8 channels (32 bytes of K) per instruction
+        mma3(tmem + 160u, saddr(s.a2[ky][0]) + 256u * j, saddr(s.a2[ky][1]) + 256u * j, kSbo2,
+             saddr(s.b2[0][ky][0]) + 256u * j, saddr(s.b2[1][ky][0]) + 256u * j, kSbo2, id2,
+             ky == 0 && j == 0);
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
   }
