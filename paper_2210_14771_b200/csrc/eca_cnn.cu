@@ -233,10 +233,10 @@ __global__ void __launch_bounds__(256, 2) cnn_kernel(const __grid_constant__ Cnn
 
 
 // ---------------------------------------------------------------------------
-// Tensor-core variant (ECA_LEARNED_TCGEN05): layers 1 and 2 (8->16 and
-// 16->32 channels, 81 % of the network's FLOPs) on tcgen05, layer 0 (5->8)
-// and the head on the CUDA cores, one 512-thread CTA per SM, one tile of
-// kTP = 128 positions of one strip at a time.
+// Tensor-core variant (ECA_LEARNED_TCGEN05): the three 3x3 layers on tcgen05
+// (layer 0 with its 5 input / 8 output channels zero-padded to 8 / 16), the
+// epilogues, 1x1 head and sigmoid on the CUDA cores; one 512-thread CTA per
+// SM, one tile of kTP = 128 positions of one strip at a time.
 //
 // No im2col.  A 3x3 valid conv is 9 shifted GEMMs; the vertical shift (ky)
 // selects an input ROW (each row is its own K-major operand), and the
@@ -248,26 +248,30 @@ __global__ void __launch_bounds__(256, 2) cnn_kernel(const __grid_constant__ Cnn
 // previous layer's epilogue, straight into the canonical K-major operand
 // layout (8-row x 16-byte core matrices), split hi/lo for 3xTF32
 // (hi*hi + hi*lo + lo*hi: FP32-level error, tools/umma_test.cu).  128 MMA
-// positions give 124 valid outputs per tile (the 3x3 halo of two layers).
+// positions give 122 valid outputs per tile (the 3x3 halo of three layers).
+//   layer 0: per output row one N = 48 chain: 3 ky x 3 split terms, 45 MMAs
 //   layer 1: per output row one N = 48 MMA chain (the 3 kx weight blocks
 //            stacked as rows of B): 3 ky x 3 split terms, 27 MMAs
 //   layer 2: one N = 96 chain: 3 ky x 2 K-steps x 3 terms, 18 MMAs
-// TMEM: layer 1 columns [0, 144), layer 2 columns [160, 256).
-constexpr int kTP = 128, kTOut = kTP - 4;
+// TMEM: layer 0 columns [0, 240), layer 1 [240, 384), layer 2 [384, 480).
+constexpr int kTP = 128, kTOut = kTP - 6;   // 3 layers x 2 columns of halo
 constexpr int kSbo1 = 2 * 128, kSbo2 = 4 * 128;       // K = 8 / 16 channels
 constexpr int kA1 = 16 * kSbo1, kA2 = 16 * kSbo2;     // one row operand (128 positions)
 constexpr int kWt1 = 2 * kSbo1, kWt2 = 4 * kSbo2;     // one (ky, kx) weight operand
 
 struct CnnSmemTc {
+  union {                         // a0 is dead once layer 0's MMAs completed
+    uint8_t a0[7][2][kA1];        // layer-0 input rows (RGBXY, 5 of 8 K lanes), hi / lo
+    uint8_t a2[3][2][kA2];        // layer-2 input rows (layer-1 output), hi / lo
+  } u;
   uint8_t a1[5][2][kA1];          // layer-1 input rows (layer-0 output), hi / lo
-  uint8_t a2[3][2][kA2];          // layer-2 input rows (layer-1 output), hi / lo
+  uint8_t b0[2][3][3][kWt1];      // layer-0 weights [hi/lo][ky][kx][out 8 + 8 zero][in 5 + 3 zero]
   uint8_t b1[2][3][3][kWt1];      // layer-1 weights [hi/lo][ky][kx][out 16][in 8]
   uint8_t b2[2][3][3][kWt2];      // layer-2 weights [hi/lo][ky][kx][out 32][in 16]
-  float in[5][7][kTP + 8];        // RGBXY window, columns 0 .. kTP+1 used
-  float4 w0[5 * 9 * 2];           // layer-0 weights [in][ky][kx][out]
-  float b0[8], b1v[16], b2v[32], w3[32], b3;
+  float b0v[8], b1v[16], b2v[32], w3[32], b3;
   float lut[3][256];              // float((v - mean_c) / std_c), computed in FP64
-  float xch1[3][4][2][2][16];     // [row][lane quarter][lane 0/1][kx-1][channel]
+  float xch0[5][4][2][2][8];      // [row][lane quarter][lane 0/1][kx-1][channel]
+  float xch1[3][4][2][2][16];
   float xch2[4][2][2][32];
   float zpart[4][kTP];            // head partial sums per channel group
   uint64_t bar;                   // MMA completion
@@ -316,6 +320,13 @@ ECA_DEV void st_hilo(uint8_t* hi, uint8_t* lo, int off, float4 v) {
 template <int N>
 ECA_DEV void tmem_ld(uint32_t addr, float* v);
 template <>
+ECA_DEV void tmem_ld<2>(uint32_t addr, float* v) {
+  uint32_t r[2];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+  v[0] = __uint_as_float(r[0]);
+  v[1] = __uint_as_float(r[1]);
+}
+template <>
 ECA_DEV void tmem_ld<4>(uint32_t addr, float* v) {
   uint32_t r[4];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
@@ -357,12 +368,15 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   const int W = J.W, H = J.H;
   const float* wg = J.weights;
 
-  // ---- weights -> smem: layer 0 transposed for the CUDA cores, layers 1-2
-  // as K-major hi/lo operands [ky*3+kx][out][in] ----
-  float* w0f = reinterpret_cast<float*>(s.w0);
-  for (int i = tid; i < kW0; i += nt) {  // i = ((o*5 + c)*3 + ky)*3 + kx
-    const int o = i / 45, r = i % 45;
-    w0f[r * 8 + o] = wg[i];
+  // ---- weights -> smem as K-major hi/lo operands [hi/lo][ky][kx][out][in];
+  // layer 0's 8 x 5 blocks zero-padded to 16 x 8 ----
+  for (int i = tid; i < 2 * 9 * kWt1 / 4; i += nt) reinterpret_cast<float*>(&s.b0[0][0][0][0])[i] = 0.f;
+  __syncthreads();
+  for (int i = tid; i < kW0; i += nt) {   // i = ((o*5 + c)*3 + ky)*3 + kx
+    const int o = i / 45, c = (i / 9) % 5, ky = (i % 9) / 3, kx = i % 3;
+    const float v = wg[i], hi = tf32_rna(v);
+    *reinterpret_cast<float*>(s.b0[0][ky][kx] + kmaj_off(o, c, kSbo1)) = hi;
+    *reinterpret_cast<float*>(s.b0[1][ky][kx] + kmaj_off(o, c, kSbo1)) = tf32_rna(v - hi);
   }
   for (int i = tid; i < kW1; i += nt) {   // i = ((o*8 + c)*3 + ky)*3 + kx
     const int o = i / 72, c = (i / 9) % 8, ky = (i % 9) / 3, kx = i % 3;
@@ -376,7 +390,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     *reinterpret_cast<float*>(s.b2[0][ky][kx] + kmaj_off(o, c, kSbo2)) = hi;
     *reinterpret_cast<float*>(s.b2[1][ky][kx] + kmaj_off(o, c, kSbo2)) = tf32_rna(v - hi);
   }
-  if (tid < 8) s.b0[tid] = wg[kOffB0 + tid];
+  if (tid < 8) s.b0v[tid] = wg[kOffB0 + tid];
   if (tid < 16) s.b1v[tid] = wg[kOffB1 + tid];
   if (tid < 32) {
     s.b2v[tid] = wg[kOffB2 + tid];
@@ -393,7 +407,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         static_cast<uint32_t>(__cvta_generic_to_shared(&s.tmem))));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -412,7 +426,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
 
   // the RGB bytes of a tile's window, 2 pixels per thread, loaded one tile
   // ahead (issued under the previous tile's tensor-core work)
-  constexpr int kWinPx = 7 * (kTP + 2);
+  constexpr int kWinPx = 7 * kTP;
   static_assert(kWinPx <= 2 * 512, "two window pixels per thread");
   uint32_t px_next[2] = {0u, 0u};
   auto load_window = [&](int t) {
@@ -425,7 +439,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
       const int i = tid + k * nt;
       uint32_t v = 0u;
       if (i < kWinPx) {
-        const int r = i / (kTP + 2), c = i % (kTP + 2), x = tx * kTOut + c;
+        const int r = i / kTP, c = i % kTP, x = tx * kTOut + c;
         if (x < W) {
           const uint8_t* px = fb + int64_t(J.band[strip] + r) * J.rstride + 3 * x;
           v = uint32_t(__ldg(px)) | (uint32_t(__ldg(px + 1)) << 8) | (uint32_t(__ldg(px + 2)) << 16);
@@ -442,55 +456,83 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   const int j0 = tx * kTOut;              // first output column (frame x = j0 + 3)
   __syncthreads();                        // previous tile's buffers are free
 
-  // ---- RGBXY window (edgenet.py:75-82), rows h-3..h+3, columns j0..j0+kTP+1 ----
+  // ---- RGBXY window (edgenet.py:75-82), rows h-3..h+3, positions j0..j0+127,
+  // written as the layer-0 operand rows (K lanes: R, G, B, X, Y, 0, 0, 0) ----
   const int h = J.rows[strip];
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int i = tid + k * nt;
     if (i < kWinPx) {
-      const int r = i / (kTP + 2), c = i % (kTP + 2);
+      const int r = i / kTP, c = i % kTP, x = j0 + c;
       const uint32_t v = px_next[k];
-      const bool in_frame = j0 + c < W;
-      s.in[0][r][c] = in_frame ? s.lut[0][v & 255u] : 0.f;
-      s.in[1][r][c] = in_frame ? s.lut[1][(v >> 8) & 255u] : 0.f;
-      s.in[2][r][c] = in_frame ? s.lut[2][(v >> 16) & 255u] : 0.f;
-    }
-  }
-  for (int c = tid; c < kTP + 2; c += nt) {
-    const int x = j0 + c;
-    const float fx = x < W ? float(div_rn(sub_rn(double(x), xc), xden)) : 0.f;
-#pragma unroll
-    for (int r = 0; r < 7; ++r) s.in[3][r][c] = fx;
-  }
-  if (tid < 7) {
-    const float fy = float(div_rn(sub_rn(double(h - 3 + tid), yc), yden));
-    for (int c = 0; c < kTP + 2; ++c) s.in[4][tid][c] = j0 + c < W ? fy : 0.f;
-  }
-  __syncthreads();
-
-  // ---- layer 0 (CUDA cores): 5 -> 8, rows 7 -> 5, positions 0..127, written
-  // as the layer-1 operand rows ----
-  for (int i = tid; i < 5 * kTP; i += nt) {
-    const int r = i / kTP, c = i % kTP;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int ci = 0; ci < 5; ++ci)
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const float v = s.in[ci][r + k / 3][c + k % 3];
-        const float4 wa = s.w0[(ci * 9 + k) * 2], wb = s.w0[(ci * 9 + k) * 2 + 1];
-        acc[0] = fmaf(wa.x, v, acc[0]); acc[1] = fmaf(wa.y, v, acc[1]);
-        acc[2] = fmaf(wa.z, v, acc[2]); acc[3] = fmaf(wa.w, v, acc[3]);
-        acc[4] = fmaf(wb.x, v, acc[4]); acc[5] = fmaf(wb.y, v, acc[5]);
-        acc[6] = fmaf(wb.z, v, acc[6]); acc[7] = fmaf(wb.w, v, acc[7]);
+      float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+      float fy = 0.f;
+      if (x < W) {
+        f.x = s.lut[0][v & 255u];
+        f.y = s.lut[1][(v >> 8) & 255u];
+        f.z = s.lut[2][(v >> 16) & 255u];
+        f.w = float(div_rn(sub_rn(double(x), xc), xden));
+        fy = float(div_rn(sub_rn(double(h - 3 + r), yc), yden));
       }
-    float y[8];
-#pragma unroll
-    for (int o = 0; o < 8; ++o) {
-      const float v = acc[o] + s.b0[o];
-      y[o] = v > 0.f ? v : 0.f;
+      st_hilo(s.u.a0[r][0], s.u.a0[r][1], kmaj_off(c, 0, kSbo1), f);
+      st_hilo(s.u.a0[r][0], s.u.a0[r][1], kmaj_off(c, 4, kSbo1), make_float4(fy, 0.f, 0.f, 0.f));
     }
-    st_hilo(s.a1[r][0], s.a1[r][1], kmaj_off(c, 0, kSbo1), make_float4(y[0], y[1], y[2], y[3]));
-    st_hilo(s.a1[r][0], s.a1[r][1], kmaj_off(c, 4, kSbo1), make_float4(y[4], y[5], y[6], y[7]));
+  }
+  publish_operands();
+
+  // ---- layer 0 (tensor cores): D0[r][kx] = sum_ky a0[r + ky] . b0[ky][kx],
+  // N = 48 (three zero-padded 16-row kx blocks) ----
+  if (tid == 0) {
+    constexpr uint32_t id0 = idesc_tf32(48);
+    for (int r = 0; r < 5; ++r)
+      for (int ky = 0; ky < 3; ++ky)
+        mma3(tmem + uint32_t(r * 48), saddr(s.u.a0[r + ky][0]), saddr(s.u.a0[r + ky][1]), kSbo1,
+             saddr(s.b0[0][ky][0]), saddr(s.b0[1][ky][0]), kSbo1, id0, ky == 0);
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+  }
+  load_window(t + gridDim.x);   // the next tile's bytes arrive under this tile's MMAs
+  bar_wait(bar, phase);
+  phase ^= 1u;
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  // ---- layer-0 epilogue: o1[r][m] = D[0][m] + D[1][m+1] + D[2][m+2] + b0, ReLU,
+  // as the layer-1 operand rows; warp (q, g): positions 32q.., channels 2g, 2g+1 ----
+  {
+    float d[5][3][2];
+#pragma unroll
+    for (int r = 0; r < 5; ++r)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) tmem_ld<2>(lane_base + uint32_t(r * 48 + kx * 16 + 2 * g), d[r][kx]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (lane < 2) {
+#pragma unroll
+      for (int r = 0; r < 5; ++r)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) s.xch0[r][q][lane][k][2 * g + c] = d[r][k + 1][c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      float y[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v1 = __shfl_down_sync(kFull, d[r][1][c], 1);
+        float v2 = __shfl_down_sync(kFull, d[r][2][c], 2);
+        if (q < 3) {
+          if (lane == 31) v1 = s.xch0[r][q + 1][0][0][2 * g + c];
+          if (lane >= 30) v2 = s.xch0[r][q + 1][lane - 30][1][2 * g + c];
+        }
+        const float v = (d[r][0][c] + v1) + v2 + s.b0v[2 * g + c];
+        y[c] = v > 0.f ? v : 0.f;
+      }
+      const int off = kmaj_off(m, 2 * g, kSbo1);
+      const float h0 = tf32_rna(y[0]), h1 = tf32_rna(y[1]);
+      *reinterpret_cast<float2*>(s.a1[r][0] + off) = make_float2(h0, h1);
+      *reinterpret_cast<float2*>(s.a1[r][1] + off) = make_float2(tf32_rna(y[0] - h0), tf32_rna(y[1] - h1));
+    }
   }
   publish_operands();
 
@@ -501,12 +543,11 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     constexpr uint32_t id1 = idesc_tf32(48);
     for (int r = 0; r < 3; ++r)
       for (int ky = 0; ky < 3; ++ky)
-        mma3(tmem + uint32_t(r * 48), saddr(s.a1[r + ky][0]), saddr(s.a1[r + ky][1]), kSbo1,
+        mma3(tmem + uint32_t(240 + r * 48), saddr(s.a1[r + ky][0]), saddr(s.a1[r + ky][1]), kSbo1,
              saddr(s.b1[0][ky][0]), saddr(s.b1[1][ky][0]), kSbo1, id1, ky == 0);
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
   }
-  load_window(t + gridDim.x);   // the next tile's bytes arrive under this tile's MMAs
   bar_wait(bar, phase);
   phase ^= 1u;
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -518,7 +559,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int kx = 0; kx < 3; ++kx) tmem_ld<4>(lane_base + uint32_t((r * 3 + kx) * 16 + 4 * g), d[r][kx]);
+      for (int kx = 0; kx < 3; ++kx) tmem_ld<4>(lane_base + uint32_t(240 + (r * 3 + kx) * 16 + 4 * g), d[r][kx]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     if (lane < 2) {
 #pragma unroll
@@ -543,7 +584,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
         const float v = (d[r][0][c] + v1) + v2 + s.b1v[4 * g + c];
         y[c] = v > 0.f ? v : 0.f;
       }
-      st_hilo(s.a2[r][0], s.a2[r][1], kmaj_off(m, 4 * g, kSbo2), make_float4(y[0], y[1], y[2], y[3]));
+      st_hilo(s.u.a2[r][0], s.u.a2[r][1], kmaj_off(m, 4 * g, kSbo2), make_float4(y[0], y[1], y[2], y[3]));
     }
   }
   publish_operands();
@@ -554,7 +595,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     constexpr uint32_t id2 = idesc_tf32(96);
     for (int ky = 0; ky < 3; ++ky)
       for (int j = 0; j < 2; ++j)   // 8 channels (32 bytes of K) per instruction
-        mma3(tmem + 160u, saddr(s.a2[ky][0]) + 256u * j, saddr(s.a2[ky][1]) + 256u * j, kSbo2,
+        mma3(tmem + 384u, saddr(s.u.a2[ky][0]) + 256u * j, saddr(s.u.a2[ky][1]) + 256u * j, kSbo2,
              saddr(s.b2[0][ky][0]) + 256u * j, saddr(s.b2[1][ky][0]) + 256u * j, kSbo2, id2,
              ky == 0 && j == 0);
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -569,7 +610,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   {
     float d[3][8];
 #pragma unroll
-    for (int kx = 0; kx < 3; ++kx) tmem_ld<8>(lane_base + uint32_t(160 + kx * 32 + 8 * g), d[kx]);
+    for (int kx = 0; kx < 3; ++kx) tmem_ld<8>(lane_base + uint32_t(384 + kx * 32 + 8 * g), d[kx]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     if (lane < 2) {
 #pragma unroll
@@ -611,7 +652,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // half-row winners of the zero-padded probability row (edgenet.py:363-369)
