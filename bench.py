@@ -445,22 +445,23 @@ def learned_leg(eb, dev, pool, n_slots, peaks) -> dict:
 
     eng = ContentAreaEngine(HEIGHT, WIDTH, BATCH, variant=eb.Learned(net), device=dev)
     ms = step_ms(eng)
-    ms_tc = step_ms(ContentAreaEngine(HEIGHT, WIDTH, BATCH, variant=eb.Learned(net), device=dev,
-                                      tensor_cores=True))
+    ms_simt = step_ms(ContentAreaEngine(HEIGHT, WIDTH, BATCH, variant=eb.Learned(net), device=dev,
+                                        tensor_cores=False))
     tflops = CNN_FLOP_PER_FRAME * BATCH / (ms * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops", 2250.0)
     return {"metric": "learned-variant frames/s (C3: EdgeNet strip CNN + select + fit)",
             "value": round(BATCH / (ms * 1e-3), 1), "unit": "frames/s", "ms_per_step": round(ms, 4),
-            "steps": steps, "dtype": "f32", "launches_per_step": eng.launches_per_run,
+            "steps": steps, "dtype": "f32 (3xTF32 on tcgen05)", "launches_per_step": eng.launches_per_run,
             "roofline": {"bound": "tensor", "achieved": round(tflops, 2), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(tflops / peak, 4),
-                         "kernel": "cnn_kernel (SIMT FP32; step time incl. select + fit)",
+                         "kernel": "cnn_kernel_tc: the three 3x3 layers as tcgen05 kind::tf32 MMA chains "
+                                   "(3xTF32), no im2col; algorithmic FP32 FLOPs (not the 3x split) over the "
+                                   "step time incl. select + fit",
                          "algorithmic_flop_per_frame": CNN_FLOP_PER_FRAME,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (measured)"},
-            "tcgen05_variant": {"value": round(BATCH / (ms_tc * 1e-3), 1), "unit": "frames/s",
-                                "ms_per_step": round(ms_tc, 4),
-                                "kernel": "cnn_kernel_tc: 16->32 conv on tcgen05 kind::tf32 (3xTF32), "
-                                          "layers 0-1 SIMT (ECA_LEARNED_TCGEN05)"}}
+            "simt_variant": {"value": round(BATCH / (ms_simt * 1e-3), 1), "unit": "frames/s",
+                             "ms_per_step": round(ms_simt, 4),
+                             "kernel": "cnn_kernel: FP32 FMA on the CUDA cores (ECA_LEARNED_SIMT)"}}
 
 
 def mask_leg(eb, dev, eng, pool, peaks) -> dict:

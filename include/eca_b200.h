@@ -210,10 +210,11 @@ int eca_points_learned(const uint8_t* frames, int batch, int64_t frame_stride,
                        float* out_probs /* [batch][n_strips][width-6] */,
                        int32_t* out_x, int32_t* out_y, double* out_score, void* stream);
 
-/* Same with flags: ECA_LEARNED_TCGEN05 runs the 16->32-channel layer on the
- * tensor cores (tcgen05 kind::tf32, 3xTF32 split: FP32-level error).  Default
- * (0) is the SIMT kernel, faster at this network size (K3). */
+/* Same with flags.  Default (0) / ECA_LEARNED_TCGEN05: the three 3x3 layers
+ * on the tensor cores (tcgen05 kind::tf32, 3xTF32 split: FP32-level error,
+ * DESIGN.md K3); ECA_LEARNED_SIMT: the CUDA-core kernel (FP32 FMA). */
 #define ECA_LEARNED_TCGEN05 1
+#define ECA_LEARNED_SIMT 2
 int eca_points_learned_ex(const uint8_t* frames, int batch, int64_t frame_stride,
                           int64_t row_stride, const int32_t* strip_rows,
                           const int32_t* band_rows, int n_strips, int height, int width,

@@ -20,7 +20,7 @@ ACCEPTED, NO_CANDIDATES, LOW_SCORE, GEOMETRY_GATE = 0, 1, 2, 3
 MAX_STRIPS, MAX_WIDTH, MAX_ATTEMPTS = 128, 4096, 8192
 NET_FLOATS = 6209
 BOUNDS_OVERLAP_PREVIOUS, BOUNDS_SHARE_SMS, BOUNDS_ZERO_COPY = 1, 2, 4
-LEARNED_TCGEN05 = 1
+LEARNED_TCGEN05, LEARNED_SIMT = 1, 2
 
 _p = ctypes.c_void_p
 _i32, _i64, _u64, _f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double

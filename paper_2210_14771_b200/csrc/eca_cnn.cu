@@ -702,7 +702,9 @@ extern "C" int eca_points_learned_ex(const uint8_t* frames, int batch, int64_t f
                                      const float* weights, const double* norm, int flags,
                                      float* out_probs, int32_t* out_x, int32_t* out_y,
                                      double* out_score, void* stream) {
-  if (flags & ~ECA_LEARNED_TCGEN05) return ECA_ERR_ARG;
+  if ((flags & ~(ECA_LEARNED_TCGEN05 | ECA_LEARNED_SIMT)) ||
+      (flags & (ECA_LEARNED_TCGEN05 | ECA_LEARNED_SIMT)) == (ECA_LEARNED_TCGEN05 | ECA_LEARNED_SIMT))
+    return ECA_ERR_ARG;
   if (batch < 0 || !strip_rows || !norm) return ECA_ERR_ARG;
   if (width < 8 || height < 14 || row_stride < 3LL * width) return ECA_ERR_ARG;
   if (height > 32767) return ECA_ERR_UNSUPPORTED;
@@ -731,7 +733,7 @@ extern "C" int eca_points_learned_ex(const uint8_t* frames, int batch, int64_t f
   J.weights = weights;
   J.probs = out_probs;
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  const bool tc = (flags & ECA_LEARNED_TCGEN05) != 0;
+  const bool tc = (flags & ECA_LEARNED_SIMT) == 0;   // tcgen05 unless the SIMT kernel is asked for
   static std::once_flag once;
   static int per_sm = 1, per_sm_tc = 1, sms = 148;
   std::call_once(once, [] {

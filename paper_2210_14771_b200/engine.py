@@ -26,14 +26,14 @@ class ContentAreaEngine:
 
     def __init__(self, height: int, width: int, batch: int, cfg: EcaConfig | None = None,
                  seed: int = 0, variant: api.EstimatorVariant = api.HANDCRAFTED, device=None,
-                 tensor_cores: bool = False):
+                 tensor_cores: bool = True):
         self.cfg = cfg or config_default()
         self.height, self.width, self.batch = height, width, batch
         self.device = api._device(device)
         self.variant = variant
         self.seed = seed
-        # learned variant: ECA_LEARNED_TCGEN05 puts the 16->32 conv on tcgen05
-        self.cnn_flags = _lib.LEARNED_TCGEN05 if tensor_cores else 0
+        # learned variant: the 3x3 layers on tcgen05 (default) or the SIMT kernel
+        self.cnn_flags = 0 if tensor_cores else _lib.LEARNED_SIMT
         self.rows = api.strip_heights(height, self.cfg.strip_count, self.cfg.strip_weighting)
         s = self.n_strips = len(self.rows)
         self.half = api.HALF_WINDOW if isinstance(variant, api.Learned) else 1

@@ -347,7 +347,7 @@ def test_native_api_argument_errors():
     net = eb.EdgeNet(eb.ChannelStats([100.0] * 3, [50.0] * 3), seed=0)
     el = eb.ContentAreaEngine(480, 640, 2, variant=eb.Learned(net))
     assert lib.eca_points_learned_ex(ctypes.c_void_p(f.data_ptr()), 2, f.stride(0), f.stride(1), el._rows,
-                                     None, el.n_strips, 480, 640, api._ptr(el.w_dev), el.norm, 2,
+                                     None, el.n_strips, 480, 640, api._ptr(el.w_dev), el.norm, 4,
                                      api._ptr(el.probs), api._ptr(el.xs), api._ptr(el.ys),
                                      api._ptr(el.sc), st) == _lib.ECA_ERR_ARG
 
@@ -403,10 +403,10 @@ def test_learned_matches_reference():
     assert agree / total >= 0.9
 
 
-def test_learned_tensor_cores_match_reference():
-    """ECA_LEARNED_TCGEN05 (layer 2 on tcgen05, 3xTF32): probabilities within
-    1e-5 of the reference, candidates equal to the SIMT kernel's except at
-    near-ties."""
+def test_learned_simt_and_tensor_cores_match_reference():
+    """Both CNN kernels -- tcgen05 (default, 3xTF32) and SIMT (ECA_LEARNED_SIMT)
+    -- give probabilities within 1e-5 of the reference; their candidates agree
+    except at near-ties."""
     npz = load_npz("learned.npz")
     net = eb.EdgeNet(eb.ChannelStats([100.0] * 3, [50.0] * 3), seed=0)
     for c in load_json("learned.json"):
@@ -414,13 +414,14 @@ def test_learned_tensor_cores_match_reference():
         h, w = frame.shape[:2]
         t = torch.from_numpy(frame).cuda().unsqueeze(0)
         e_tc = eb.ContentAreaEngine(h, w, 1, variant=eb.Learned(net), tensor_cores=True)
-        e_ref = eb.ContentAreaEngine(h, w, 1, variant=eb.Learned(net))
+        e_ref = eb.ContentAreaEngine(h, w, 1, variant=eb.Learned(net), tensor_cores=False)
         e_tc.run(t)
         e_ref.run(t)
         torch.cuda.synchronize()
         got = e_tc.probs[0].cpu().numpy()
         want = npz[c["name"]][:, 3:w - 3]
         assert np.abs(got - want).max() <= 1e-5, c["name"]
+        assert np.abs(e_ref.probs[0].cpu().numpy() - want).max() <= 1e-5, c["name"]
         assert np.abs(got - e_ref.probs[0].cpu().numpy()).max() <= 1e-5
         xt, xr = e_tc.xs[0].cpu().tolist(), e_ref.xs[0].cpu().tolist()
         full = npz[c["name"]]
@@ -464,3 +465,24 @@ def test_crop_area_copies_pixels():
     assert np.array_equal(crop.cpu().numpy(), frame[y0:y1 + 1, x0:x1 + 1])
     with pytest.raises(ValueError):
         eb.crop_area(frame, eb.FULL_FRAME)
+
+
+@pytest.mark.parametrize("w,h", [(40, 30), (128, 64), (134, 40), (250, 97), (517, 300), (1920, 60)])
+@pytest.mark.parametrize("tc", [True, False])
+def test_learned_tile_edges_match_oracle(w, h, tc):
+    """CNN tiles: widths below one tile, at and around the tcgen05 tile's 122
+    valid outputs, ragged last tiles; probabilities against the oracle's FP32
+    network within 1e-5, batch of 3 frames."""
+    rng = np.random.default_rng(w * 7 + h)
+    frames = rng.integers(0, 256, (3, h, w, 3), dtype=np.uint8)
+    net = eb.EdgeNet(eb.ChannelStats([90.0, 100.0, 110.0], [40.0, 50.0, 60.0]), seed=w)
+    layers = [(l.kernel, l.bias) for l in net.layers]
+    eng = eb.ContentAreaEngine(h, w, 3, variant=eb.Learned(net), tensor_cores=tc)
+    eng.run(torch.from_numpy(frames).cuda())
+    torch.cuda.synchronize()
+    rows = eb.strip_heights(h, 16, 8.0)
+    for k in range(3):
+        want = orc.cnn_probs(orc.rgbxy_windows(frames[k], rows, [90.0, 100.0, 110.0], [40.0, 50.0, 60.0]),
+                             layers)
+        got = eng.probs[k].cpu().numpy()[:len(rows)]
+        assert np.abs(got - want).max() <= 1e-5, (k, np.abs(got - want).max())
