@@ -253,28 +253,32 @@ __global__ void __launch_bounds__(256, 2) cnn_kernel(const __grid_constant__ Cnn
 //   layer 1: per output row one N = 48 MMA chain (the 3 kx weight blocks
 //            stacked as rows of B): 3 ky x 3 split terms, 27 MMAs
 //   layer 2: one N = 96 chain: 3 ky x 2 K-steps x 3 terms, 18 MMAs
-// TMEM: layer 0 columns [0, 240), layer 1 [240, 384), layer 2 [384, 480).
+// TMEM: 256 columns per group, reused by the three layers in turn (layer 0
+// [0, 240), layer 1 [0, 144), layer 2 [0, 96)).
 constexpr int kTP = 128, kTOut = kTP - 6;   // 3 layers x 2 columns of halo
 constexpr int kSbo1 = 2 * 128, kSbo2 = 4 * 128;       // K = 8 / 16 channels
 constexpr int kA1 = 16 * kSbo1, kA2 = 16 * kSbo2;     // one row operand (128 positions)
 constexpr int kWt1 = 2 * kSbo1, kWt2 = 4 * kSbo2;     // one (ky, kx) weight operand
 
+constexpr int kGroups = 2, kGThreads = 256;          // tiles in flight per CTA, threads per tile
+constexpr int kAct = 7 * 2 * kA1;                     // a0 (7 x 2 x 4 KB) >= a2 (3 x 2 x 8 KB) >= a1
+static_assert(kAct >= 3 * 2 * kA2 && kAct >= 5 * 2 * kA1, "activation region");
+
+struct CnnGroupTc {               // one tile in flight
+  // a0 -> a1 -> a2 in turn: each is dead once the MMAs reading it completed
+  alignas(1024) uint8_t act[kAct];
+  float xch[768];                 // epilogue neighbour exchange (lanes 0/1 of each warp)
+  float zpart[2][kTP];            // head partial sums per channel half
+  uint64_t bar;                   // MMA completion
+};
+
 struct CnnSmemTc {
-  union {                         // a0 is dead once layer 0's MMAs completed
-    uint8_t a0[7][2][kA1];        // layer-0 input rows (RGBXY, 5 of 8 K lanes), hi / lo
-    uint8_t a2[3][2][kA2];        // layer-2 input rows (layer-1 output), hi / lo
-  } u;
-  uint8_t a1[5][2][kA1];          // layer-1 input rows (layer-0 output), hi / lo
+  CnnGroupTc grp[kGroups];
   uint8_t b0[2][3][3][kWt1];      // layer-0 weights [hi/lo][ky][kx][out 8 + 8 zero][in 5 + 3 zero]
   uint8_t b1[2][3][3][kWt1];      // layer-1 weights [hi/lo][ky][kx][out 16][in 8]
   uint8_t b2[2][3][3][kWt2];      // layer-2 weights [hi/lo][ky][kx][out 32][in 16]
   float b0v[8], b1v[16], b2v[32], w3[32], b3;
   float lut[3][256];              // float((v - mean_c) / std_c), computed in FP64
-  float xch0[5][4][2][2][8];      // [row][lane quarter][lane 0/1][kx-1][channel]
-  float xch1[3][4][2][2][16];
-  float xch2[4][2][2][32];
-  float zpart[4][kTP];            // head partial sums per channel group
-  uint64_t bar;                   // MMA completion
   uint32_t tmem;
 };
 
@@ -345,6 +349,17 @@ ECA_DEV void tmem_ld<8>(uint32_t addr, float* v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+template <>
+ECA_DEV void tmem_ld<16>(uint32_t addr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
 ECA_DEV void bar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred P1;\nECA_MW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
@@ -357,6 +372,16 @@ ECA_DEV void publish_operands() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// the same within one tile group (named barrier 1 + group, its 256 threads)
+ECA_DEV void group_sync(int grp) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGThreads) : "memory");
+}
+ECA_DEV void publish_group(int grp) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  group_sync(grp);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
@@ -401,8 +426,10 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     const int ch = i >> 8, v = i & 255;
     s.lut[ch][v] = float(div_rn(sub_rn(double(v), J.mean[ch]), J.stdv[ch]));
   }
-  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&s.bar));
-  if (tid == 0) {
+  const int grp = warp >> 3, gtid = tid & (kGThreads - 1);
+  CnnGroupTc& G = s.grp[grp];
+  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&G.bar));
+  if (gtid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -412,31 +439,36 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   publish_operands();
-  const uint32_t tmem = s.tmem;
+  const uint32_t tmem = s.tmem + uint32_t(grp * 256);   // this group's 256 TMEM columns
   uint32_t phase = 0;
   const auto saddr = [](const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); };
-  const int q = warp & 3, g = warp >> 2;          // TMEM lane quarter, channel group
+  const int q = warp & 3, ch = (warp >> 2) & 1;   // TMEM lane quarter, channel half
   const int m = 32 * q + lane;                    // this thread's MMA position
   const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
+  uint8_t* act = G.act;
+  auto a0 = [&](int r, int part) { return act + (r * 2 + part) * kA1; };
+  auto a1 = [&](int r, int part) { return act + (r * 2 + part) * kA1; };
+  auto a2 = [&](int r, int part) { return act + (r * 2 + part) * kA2; };
 
   const double xden = double(W - 1 > 1 ? W - 1 : 1), yden = double(H - 1 > 1 ? H - 1 : 1);
   const double xc = div_rn(double(W - 1), 2.0), yc = div_rn(double(H - 1), 2.0);
   const int tiles_x = (W - 6 + kTOut - 1) / kTOut;
   const int n_tiles = tiles_x * J.S * J.batch;
+  const int t_step = kGroups * gridDim.x;
 
-  // the RGB bytes of a tile's window, 2 pixels per thread, loaded one tile
-  // ahead (issued under the previous tile's tensor-core work)
+  // the RGB bytes of a tile's window, 4 pixels per thread, loaded one tile
+  // ahead (issued under the current tile's tensor-core work)
   constexpr int kWinPx = 7 * kTP;
-  static_assert(kWinPx <= 2 * 512, "two window pixels per thread");
-  uint32_t px_next[2] = {0u, 0u};
+  constexpr int kPxPer = (kWinPx + kGThreads - 1) / kGThreads;
+  uint32_t px_next[kPxPer];
   auto load_window = [&](int t) {
     if (t >= n_tiles) return;
     const int tx = t % tiles_x, fs = t / tiles_x;
     const int strip = fs % J.S, b = fs / J.S;
     const uint8_t* fb = J.frames + int64_t(b) * J.fstride;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int i = tid + k * nt;
+    for (int k = 0; k < kPxPer; ++k) {
+      const int i = gtid + k * kGThreads;
       uint32_t v = 0u;
       if (i < kWinPx) {
         const int r = i / kTP, c = i % kTP, x = tx * kTOut + c;
@@ -448,20 +480,22 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
       px_next[k] = v;
     }
   };
-  load_window(blockIdx.x);
+  load_window(blockIdx.x + grp * gridDim.x);
 
-  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+  // group g runs this CTA's tiles g, g + 2, ...: while one group's MMAs run,
+  // the other group's CUDA-core work (window, epilogues) proceeds
+  for (int t = blockIdx.x + grp * gridDim.x; t < n_tiles; t += t_step) {
   const int tx = t % tiles_x, fs = t / tiles_x;
   const int strip = fs % J.S, b = fs / J.S;
   const int j0 = tx * kTOut;              // first output column (frame x = j0 + 3)
-  __syncthreads();                        // previous tile's buffers are free
+  group_sync(grp);                        // the previous tile's epilogue is done
 
   // ---- RGBXY window (edgenet.py:75-82), rows h-3..h+3, positions j0..j0+127,
   // written as the layer-0 operand rows (K lanes: R, G, B, X, Y, 0, 0, 0) ----
   const int h = J.rows[strip];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int i = tid + k * nt;
+  for (int k = 0; k < kPxPer; ++k) {
+    const int i = gtid + k * kGThreads;
     if (i < kWinPx) {
       const int r = i / kTP, c = i % kTP, x = j0 + c;
       const uint32_t v = px_next[k];
@@ -474,76 +508,75 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
         f.w = float(div_rn(sub_rn(double(x), xc), xden));
         fy = float(div_rn(sub_rn(double(h - 3 + r), yc), yden));
       }
-      st_hilo(s.u.a0[r][0], s.u.a0[r][1], kmaj_off(c, 0, kSbo1), f);
-      st_hilo(s.u.a0[r][0], s.u.a0[r][1], kmaj_off(c, 4, kSbo1), make_float4(fy, 0.f, 0.f, 0.f));
+      st_hilo(a0(r, 0), a0(r, 1), kmaj_off(c, 0, kSbo1), f);
+      st_hilo(a0(r, 0), a0(r, 1), kmaj_off(c, 4, kSbo1), make_float4(fy, 0.f, 0.f, 0.f));
     }
   }
-  publish_operands();
+  publish_group(grp);
 
   // ---- layer 0 (tensor cores): D0[r][kx] = sum_ky a0[r + ky] . b0[ky][kx],
   // N = 48 (three zero-padded 16-row kx blocks) ----
-  if (tid == 0) {
+  if (gtid == 0) {
     constexpr uint32_t id0 = idesc_tf32(48);
     for (int r = 0; r < 5; ++r)
       for (int ky = 0; ky < 3; ++ky)
-        mma3(tmem + uint32_t(r * 48), saddr(s.u.a0[r + ky][0]), saddr(s.u.a0[r + ky][1]), kSbo1,
+        mma3(tmem + uint32_t(r * 48), saddr(a0(r + ky, 0)), saddr(a0(r + ky, 1)), kSbo1,
              saddr(s.b0[0][ky][0]), saddr(s.b0[1][ky][0]), kSbo1, id0, ky == 0);
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
   }
-  load_window(t + gridDim.x);   // the next tile's bytes arrive under this tile's MMAs
+  load_window(t + t_step);   // the next tile's bytes arrive under this tile's MMAs
   bar_wait(bar, phase);
   phase ^= 1u;
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   // ---- layer-0 epilogue: o1[r][m] = D[0][m] + D[1][m+1] + D[2][m+2] + b0, ReLU,
-  // as the layer-1 operand rows; warp (q, g): positions 32q.., channels 2g, 2g+1 ----
+  // as the layer-1 operand rows (over a0: its MMAs completed); warp (q, ch):
+  // positions 32q.., channels 4ch.. ----
   {
-    float d[5][3][2];
+    float d[5][3][4];
 #pragma unroll
     for (int r = 0; r < 5; ++r)
 #pragma unroll
-      for (int kx = 0; kx < 3; ++kx) tmem_ld<2>(lane_base + uint32_t(r * 48 + kx * 16 + 2 * g), d[r][kx]);
+      for (int kx = 0; kx < 3; ++kx) tmem_ld<4>(lane_base + uint32_t(r * 48 + kx * 16 + 4 * ch), d[r][kx]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float* xch = G.xch;   // [r][q][lane][kx-1][8]
     if (lane < 2) {
 #pragma unroll
       for (int r = 0; r < 5; ++r)
 #pragma unroll
         for (int k = 0; k < 2; ++k)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) s.xch0[r][q][lane][k][2 * g + c] = d[r][k + 1][c];
+          for (int c = 0; c < 4; ++c) xch[(((r * 4 + q) * 2 + lane) * 2 + k) * 8 + 4 * ch + c] = d[r][k + 1][c];
     }
-    __syncthreads();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    group_sync(grp);   // also: every a0 read of this tile's MMAs is long complete
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-      float y[2];
+      float y[4];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < 4; ++c) {
         float v1 = __shfl_down_sync(kFull, d[r][1][c], 1);
         float v2 = __shfl_down_sync(kFull, d[r][2][c], 2);
         if (q < 3) {
-          if (lane == 31) v1 = s.xch0[r][q + 1][0][0][2 * g + c];
-          if (lane >= 30) v2 = s.xch0[r][q + 1][lane - 30][1][2 * g + c];
+          if (lane == 31) v1 = xch[(((r * 4 + q + 1) * 2 + 0) * 2 + 0) * 8 + 4 * ch + c];
+          if (lane >= 30) v2 = xch[(((r * 4 + q + 1) * 2 + (lane - 30)) * 2 + 1) * 8 + 4 * ch + c];
         }
-        const float v = (d[r][0][c] + v1) + v2 + s.b0v[2 * g + c];
+        const float v = (d[r][0][c] + v1) + v2 + s.b0v[4 * ch + c];
         y[c] = v > 0.f ? v : 0.f;
       }
-      const int off = kmaj_off(m, 2 * g, kSbo1);
-      const float h0 = tf32_rna(y[0]), h1 = tf32_rna(y[1]);
-      *reinterpret_cast<float2*>(s.a1[r][0] + off) = make_float2(h0, h1);
-      *reinterpret_cast<float2*>(s.a1[r][1] + off) = make_float2(tf32_rna(y[0] - h0), tf32_rna(y[1] - h1));
+      st_hilo(a1(r, 0), a1(r, 1), kmaj_off(m, 4 * ch, kSbo1), make_float4(y[0], y[1], y[2], y[3]));
     }
   }
-  publish_operands();
+  publish_group(grp);
 
   // ---- layer 1 (tensor cores): D1[r][kx] = sum_ky a1[r + ky] . b1[ky][kx];
-  // the three kx weight blocks are adjacent rows of one N = 48 operand, so one
-  // MMA per (row, ky, split term) fills all three kx accumulators ----
-  if (tid == 0) {
+  // the three kx weight blocks are adjacent rows of one N = 48 operand ----
+  if (gtid == 0) {
     constexpr uint32_t id1 = idesc_tf32(48);
     for (int r = 0; r < 3; ++r)
       for (int ky = 0; ky < 3; ++ky)
-        mma3(tmem + uint32_t(240 + r * 48), saddr(s.a1[r + ky][0]), saddr(s.a1[r + ky][1]), kSbo1,
+        mma3(tmem + uint32_t(r * 48), saddr(a1(r + ky, 0)), saddr(a1(r + ky, 1)), kSbo1,
              saddr(s.b1[0][ky][0]), saddr(s.b1[1][ky][0]), kSbo1, id1, ky == 0);
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
@@ -552,50 +585,53 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   phase ^= 1u;
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  // ---- layer-1 epilogue: o2[r][m] = D[0][m] + D[1][m+1] + D[2][m+2] + b1,
-  // ReLU, as the layer-2 operand rows; warp (q, g): positions 32q.., channels 4g.. ----
+  // ---- layer-1 epilogue -> layer-2 operand rows (over a1: its MMAs completed);
+  // warp (q, ch): channels 8ch.. ----
   {
-    float d[3][3][4];
+    float d[3][3][8];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int kx = 0; kx < 3; ++kx) tmem_ld<4>(lane_base + uint32_t(240 + (r * 3 + kx) * 16 + 4 * g), d[r][kx]);
+      for (int kx = 0; kx < 3; ++kx) tmem_ld<8>(lane_base + uint32_t(r * 48 + kx * 16 + 8 * ch), d[r][kx]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float* xch = G.xch;   // [r][q][lane][kx-1][16]
     if (lane < 2) {
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int k = 0; k < 2; ++k)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) s.xch1[r][q][lane][k][4 * g + c] = d[r][k + 1][c];
+          for (int c = 0; c < 8; ++c) xch[(((r * 4 + q) * 2 + lane) * 2 + k) * 16 + 8 * ch + c] = d[r][k + 1][c];
     }
-    __syncthreads();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    group_sync(grp);
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      float y[4];
+      float y[8];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 8; ++c) {
         float v1 = __shfl_down_sync(kFull, d[r][1][c], 1);
         float v2 = __shfl_down_sync(kFull, d[r][2][c], 2);
         if (q < 3) {
-          if (lane == 31) v1 = s.xch1[r][q + 1][0][0][4 * g + c];
-          if (lane >= 30) v2 = s.xch1[r][q + 1][lane - 30][1][4 * g + c];
+          if (lane == 31) v1 = xch[(((r * 4 + q + 1) * 2 + 0) * 2 + 0) * 16 + 8 * ch + c];
+          if (lane >= 30) v2 = xch[(((r * 4 + q + 1) * 2 + (lane - 30)) * 2 + 1) * 16 + 8 * ch + c];
         }
-        const float v = (d[r][0][c] + v1) + v2 + s.b1v[4 * g + c];
+        const float v = (d[r][0][c] + v1) + v2 + s.b1v[8 * ch + c];
         y[c] = v > 0.f ? v : 0.f;
       }
-      st_hilo(s.u.a2[r][0], s.u.a2[r][1], kmaj_off(m, 4 * g, kSbo2), make_float4(y[0], y[1], y[2], y[3]));
+      st_hilo(a2(r, 0), a2(r, 1), kmaj_off(m, 8 * ch, kSbo2), make_float4(y[0], y[1], y[2], y[3]));
+      st_hilo(a2(r, 0), a2(r, 1), kmaj_off(m, 8 * ch + 4, kSbo2), make_float4(y[4], y[5], y[6], y[7]));
     }
   }
-  publish_operands();
+  publish_group(grp);
 
   // ---- layer 2 (tensor cores): D2[kx] = sum_ky a2[ky] . b2[ky][kx], K = 16,
   // the three kx blocks as one N = 96 operand ----
-  if (tid == 0) {
+  if (gtid == 0) {
     constexpr uint32_t id2 = idesc_tf32(96);
     for (int ky = 0; ky < 3; ++ky)
       for (int j = 0; j < 2; ++j)   // 8 channels (32 bytes of K) per instruction
-        mma3(tmem + 384u, saddr(s.u.a2[ky][0]) + 256u * j, saddr(s.u.a2[ky][1]) + 256u * j, kSbo2,
+        mma3(tmem, saddr(a2(ky, 0)) + 256u * j, saddr(a2(ky, 1)) + 256u * j, kSbo2,
              saddr(s.b2[0][ky][0]) + 256u * j, saddr(s.b2[1][ky][0]) + 256u * j, kSbo2, id2,
              ky == 0 && j == 0);
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -605,39 +641,40 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   phase ^= 1u;
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  // ---- layer-2 epilogue + head: channels 8g..8g+7 per warp, partial head
-  // sums per channel group, then the sigmoid ----
+  // ---- layer-2 epilogue + head: channels 16ch..16ch+15 per warp, partial
+  // head sums per channel half, then the sigmoid ----
   {
-    float d[3][8];
+    float d[3][16];
 #pragma unroll
-    for (int kx = 0; kx < 3; ++kx) tmem_ld<8>(lane_base + uint32_t(384 + kx * 32 + 8 * g), d[kx]);
+    for (int kx = 0; kx < 3; ++kx) tmem_ld<16>(lane_base + uint32_t(kx * 32 + 16 * ch), d[kx]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float* xch = G.xch;   // [q][lane][kx-1][32]
     if (lane < 2) {
 #pragma unroll
       for (int k = 0; k < 2; ++k)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) s.xch2[q][lane][k][8 * g + c] = d[k + 1][c];
+        for (int c = 0; c < 16; ++c) xch[((q * 2 + lane) * 2 + k) * 32 + 16 * ch + c] = d[k + 1][c];
     }
-    __syncthreads();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    group_sync(grp);
     float z = 0.f;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < 16; ++c) {
       float v1 = __shfl_down_sync(kFull, d[1][c], 1);
       float v2 = __shfl_down_sync(kFull, d[2][c], 2);
       if (q < 3) {
-        if (lane == 31) v1 = s.xch2[q + 1][0][0][8 * g + c];
-        if (lane >= 30) v2 = s.xch2[q + 1][lane - 30][1][8 * g + c];
+        if (lane == 31) v1 = xch[(((q + 1) * 2 + 0) * 2 + 0) * 32 + 16 * ch + c];
+        if (lane >= 30) v2 = xch[(((q + 1) * 2 + (lane - 30)) * 2 + 1) * 32 + 16 * ch + c];
       }
-      const float v = (d[0][c] + v1) + v2 + s.b2v[8 * g + c];
-      z = fmaf(s.w3[8 * g + c], v > 0.f ? v : 0.f, z);
+      const float v = (d[0][c] + v1) + v2 + s.b2v[16 * ch + c];
+      z = fmaf(s.w3[16 * ch + c], v > 0.f ? v : 0.f, z);
     }
-    s.zpart[g][m] = z;
+    G.zpart[ch][m] = z;
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (tid < kTOut) {
-    const float z = ((s.zpart[0][tid] + s.zpart[1][tid]) + (s.zpart[2][tid] + s.zpart[3][tid])) + s.b3;
-    const int j = j0 + tid;
+  group_sync(grp);
+  if (gtid < kTOut) {
+    const float z = (G.zpart[0][gtid] + G.zpart[1][gtid]) + s.b3;
+    const int j = j0 + gtid;
     if (j < W - 6) {
       float p;
       if (z >= 0.f) {
@@ -652,7 +689,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s.tmem));
 }
 
 // half-row winners of the zero-padded probability row (edgenet.py:363-369)

@@ -20,8 +20,9 @@ def timeit(fn, n=10):
     return a.elapsed_time(b) / n
 ms = timeit(lambda i: eng.run(pool[(i % 2) * B:][:B]))
 flop = 606.6e6 * B
-print(f"learned estimate B={B}: {ms * 1e3:.1f} us/step  {B / ms * 1e3:.0f} frames/s  CNN {flop / (ms * 1e-3) / 1e12:.1f} TFLOP/s (FP32 SIMT)")
-eng_tc = eb.ContentAreaEngine(1080, 1920, B, variant=eb.Learned(net), device=dev, tensor_cores=True)
-ms = timeit(lambda i: eng_tc.run(pool[(i % 2) * B:][:B]))
-print(f"learned estimate B={B}, tcgen05 layers 1-2: {ms * 1e3:.1f} us/step  {B / ms * 1e3:.0f} frames/s  "
+print(f"learned estimate B={B}, default (tcgen05 CNN): {ms * 1e3:.1f} us/step  {B / ms * 1e3:.0f} frames/s  "
+      f"CNN {flop / (ms * 1e-3) / 1e12:.1f} TFLOP/s")
+eng_simt = eb.ContentAreaEngine(1080, 1920, B, variant=eb.Learned(net), device=dev, tensor_cores=False)
+ms = timeit(lambda i: eng_simt.run(pool[(i % 2) * B:][:B]))
+print(f"learned estimate B={B}, SIMT CNN: {ms * 1e3:.1f} us/step  {B / ms * 1e3:.0f} frames/s  "
       f"CNN {flop / (ms * 1e-3) / 1e12:.1f} TFLOP/s")
