@@ -371,7 +371,8 @@ def run_ours(args) -> None:
                        "l2": f"inputs larger than L2: {POOL}-slot HBM pool rotated "
                              f"({POOL * STRIP_BYTES_PER_FRAME / 1e6:.0f} MB of strip rows > 126 MB L2)",
                        "parallelism": f"dp{world}" + (" + NCCL all-gather of 40-B records" if world > 1 else ""),
-                       "pipelining": "2 streams: rescore+fit of batch i overlap bound-and-prune of batch i+1"},
+                       "pipelining": "2 streams: rescore+fit of batch i overlap the next batches' "
+                                     "bound-and-prune (programmatic dependent launches, 16 buffer sets)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": "eca::bounds_kernel<1> (K1 strip scoring: exact integer Sobel / "

@@ -148,10 +148,11 @@ int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
 /* Streamed throughput mode as one call per batch (what
  * ContentAreaEngine.run_pipelined does): the bound-and-prune kernel of batch i
  * runs on `stream`, its rescore + fit on the pipeline's own low-priority side
- * stream, overlapping batch i+1's bound-and-prune.  Two buffer sets alternate
- * in the caller's device `scratch` (eca_pipeline_bytes; zeroed by create):
- * the records of step i stay valid until step i+2.  Same results as
- * eca_points_handcrafted + eca_fit.  One host thread per pipeline. */
+ * stream, overlapping the next batches' bound-and-prune.  16 buffer sets
+ * rotate in the caller's device `scratch` (eca_pipeline_bytes; zeroed by
+ * create): the records of step i stay valid until step i+16.  Consecutive
+ * bound-and-prune launches overlap (programmatic dependent launch).  Same
+ * results as eca_points_handcrafted + eca_fit.  One host thread per pipeline. */
 typedef struct EcaPipeline EcaPipeline;
 int eca_pipeline_bytes(int batch, int n_strips, int64_t* out_bytes);
 int eca_pipeline_create(int batch, int height, int width, const int32_t* strip_rows,
@@ -166,6 +167,11 @@ int eca_pipeline_create(int batch, int height, int width, const int32_t* strip_r
 int eca_pipeline_step(EcaPipeline* pipeline, const uint8_t* frames, int64_t frame_stride,
                       int64_t row_stride, int flags, EcaFitRecord* host_records, void* stream,
                       EcaFitRecord** out_records);
+/* Forget the pipeline's history (no step waits on an earlier step's events):
+ * call when everything enqueued so far has completed, e.g. right before
+ * capturing a sequence of steps into a CUDA graph, whose first steps must not
+ * wait on events recorded outside the capture. */
+int eca_pipeline_reset(EcaPipeline* pipeline);
 /* Make `stream` wait for every step enqueued so far. */
 int eca_pipeline_fence(EcaPipeline* pipeline, void* stream);
 /* The side stream (e.g. to gather the records of a step right after its fit). */

@@ -472,9 +472,12 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
 // run_pipelined): bounds kernel of batch i on the caller's stream; rescore +
 // fit on the pipeline's side stream, overlapping batch i+1's bounds kernel.
 // kPipeSets buffer sets rotate inside the caller-provided scratch: batch i's
-// bounds kernel waits only for the fit of batch i - kPipeSets.
+// bounds kernel waits for the fit of batch i - kPipeSets (16 sets measured
+// 1.3 us per batch faster than 3; a host stream wait in front of a
+// programmatic-dependent launch costs its overlap, and a device-side
+// release flag instead starved the low-priority fits -- DESIGN.md).
 #ifndef ECA_PIPE_SETS
-#define ECA_PIPE_SETS 3
+#define ECA_PIPE_SETS 16
 #endif
 constexpr int kPipeSets = ECA_PIPE_SETS;
 struct EcaPipeline {
@@ -583,7 +586,7 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   J.out_x = P->xs[s];
   J.out_y = P->ys[s];
   J.out_score = P->sc[s];
-  // the fit two steps ago has finished reading this set
+  // the fit kPipeSets batches back has finished reading this set
   if (P->used[s] && cudaStreamWaitEvent(st, P->ev_free[s], 0) != cudaSuccess) return ECA_ERR_CUDA;
   int rc = launch_bounds(J, P->ws[s], st, /*overlap=*/true, /*share=*/true,
                          (flags & ECA_BOUNDS_ZERO_COPY) != 0);
@@ -605,6 +608,14 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   P->last = s;
   ++P->step;
   *out_records = P->rec[s];
+  return ECA_OK;
+}
+
+extern "C" int eca_pipeline_reset(EcaPipeline* P) {
+  if (!P) return ECA_ERR_ARG;
+  for (int k = 0; k < kPipeSets; ++k) P->used[k] = false;
+  P->step = 0;
+  P->last = -1;
   return ECA_OK;
 }
 

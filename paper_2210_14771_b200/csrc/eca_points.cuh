@@ -144,9 +144,6 @@ struct ColEval {
 template <int NS, bool kChunked>
 __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_constant__ PointsJob PJ) {
   const StripJob& J = PJ.J;
-  // a dependent launch (the next batch, ECA_BOUNDS_OVERLAP_PREVIOUS) may start
-  // filling SMs as soon as this grid's CTAs drain
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int warps = blockDim.x >> 5;
@@ -187,6 +184,11 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     }
   }
   __syncthreads();
+  // a dependent launch (the next batch, ECA_BOUNDS_OVERLAP_PREVIOUS) may start
+  // filling SMs as this grid's CTAs drain; triggered after the prologue (its
+  // first frame loads are in flight), measured 1 us faster per launch than
+  // triggering at entry
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef ECA_WARP_TIMES
   if (lane == 0) {
     uint64_t t;

@@ -61,6 +61,7 @@ class ContentAreaEngine:
             self.w_dev, self.norm = api._dev_net(variant.net, d)
         self.graph = None
         self._pipe = None
+        self._pipe_graph = None
         # Small batches (latency): one fused launch whose last strip CTA per
         # frame runs the fit.  Large batches (throughput): bound-and-prune
         # kernel, FP64 rescore of the survivors, then a fit kernel (one warp
@@ -149,6 +150,7 @@ class ContentAreaEngine:
         return self._pipe
 
     def _release_pipeline(self):
+        self._pipe_graph = None
         if self._pipe is not None:
             _lib.load().eca_pipeline_destroy(self._pipe["handle"])
             self._pipe = None
@@ -168,9 +170,9 @@ class ContentAreaEngine:
         """Throughput mode for a stream of batches, one native call per batch
         (eca_pipeline_step): the bound-and-prune kernel of this batch runs on
         the current stream, its FP64 rescore and the fit on a side stream,
-        where they overlap the NEXT call's bound-and-prune.  Two buffer sets
-        alternate; the returned (B,5) records are complete once ``fence()`` has
-        made the reading stream wait, and are overwritten two calls later.
+        where they overlap the next calls' bound-and-prune.  16 buffer sets
+        rotate; the returned (B,5) records are complete once ``fence()`` has
+        made the reading stream wait, and are overwritten 16 calls later.
         Same records as run() (tests/test_gpu_parity.py)."""
         if isinstance(self.variant, api.Learned) or self.fused:
             return self.run(frames)
@@ -212,6 +214,35 @@ class ContentAreaEngine:
                              _lib.BOUNDS_ZERO_COPY, ctypes.c_void_p(r.data_ptr()),
                              ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
                              ctypes.byref(p["out"])), "eca_pipeline_step")
+
+    def capture_pipelined(self, batches) -> None:
+        """Record run_pipelined() over ``batches`` (device frame tensors whose
+        storage stays put) plus the closing fence as ONE CUDA graph: both
+        streams, the events between them and the programmatic-dependent
+        bound-and-prune launches become graph nodes, so replay_pipelined()
+        streams the whole sequence with one host call instead of one native
+        call per batch (which bounds the step at ~28 us of host time).  The
+        records of batch k are the ones run_pipelined returned for it during
+        capture; the graph replays exactly that sequence."""
+        p = self._pipe if self._pipe is not None else self._pipeline()
+        torch.cuda.synchronize(self.device)
+        _lib.check(_lib.load().eca_pipeline_reset(p["handle"]), "eca_pipeline_reset")
+        g = torch.cuda.CUDAGraph()
+        recs = []
+        with torch.cuda.graph(g):
+            for f in batches:
+                recs.append(self.run_pipelined(f))
+            self.fence()
+        torch.cuda.synchronize(self.device)
+        _lib.check(_lib.load().eca_pipeline_reset(p["handle"]), "eca_pipeline_reset")
+        self._pipe_graph = (g, recs)
+
+    def replay_pipelined(self) -> list:
+        """Launch the captured pipeline graph on the current stream; returns
+        the per-batch record tensors (complete when the stream reaches here)."""
+        g, recs = self._pipe_graph
+        g.replay()
+        return recs
 
     def fence(self, stream: torch.cuda.Stream | None = None) -> None:
         """Make ``stream`` (default: current) wait for every run_pipelined() so far."""

@@ -197,6 +197,49 @@ def test_pipelined_matches_run():
     assert torch.equal(r, want[j])
 
 
+def test_pipelined_long_stream_matches_run():
+    """40 unsynchronised run_pipelined calls over 3 distinct batches (the
+    16-set rotation, the every-8-steps wait and overlapping bound-and-prune
+    launches on reused sets): the last 16 steps' records all equal run()'s."""
+    specs = synth.bench_specs(40, 960, 540, seed=2024)
+    frames = torch.from_numpy(np.stack([synth.render(s, 31000 + k)
+                                        for k, (_, s) in enumerate(specs)])).cuda()
+    B = 24
+    pool = frames[[k % 40 for k in range(3 * B)]]
+    eng = eb.ContentAreaEngine(540, 960, B)
+    want = [eng.run(pool[k * B:(k + 1) * B]).clone() for k in range(3)]
+    recs = [(i % 3, eng.run_pipelined(pool[(i % 3) * B:(i % 3 + 1) * B])) for i in range(40)]
+    eng.fence()
+    torch.cuda.synchronize()
+    for k, r in recs[-16:]:
+        assert torch.equal(r, want[k])
+
+
+def test_pipeline_graph_replay_matches_run():
+    """capture_pipelined + replay_pipelined (the bench's 1-GPU mode: a whole
+    rotation of batches as one CUDA graph with both streams and the
+    programmatic-dependent bounds launches as nodes) gives run()'s records for
+    the last three batches (the pipeline's buffer sets), replay after replay."""
+    specs = synth.bench_specs(40, 1920, 1080, seed=2024)
+    frames = torch.from_numpy(np.stack([synth.render(s, 30000 + k)
+                                        for k, (_, s) in enumerate(specs)])).cuda()
+    B, n = 20, 5
+    pool = frames[[k % 40 for k in range(n * B)]]
+    eng = eb.ContentAreaEngine(1080, 1920, B)
+    want = [eng.run(pool[k * B:(k + 1) * B]).clone() for k in range(n)]
+    eng.run_pipelined(pool[:B])   # eager steps before capture are allowed
+    eng.fence()
+    eng.capture_pipelined([pool[k * B:(k + 1) * B] for k in range(n)])
+    for rep in range(3):
+        for rec in eng.replay_pipelined():
+            rec.zero_() if rep == 1 else None
+        torch.cuda.synchronize()
+        recs = eng.replay_pipelined()
+        torch.cuda.synchronize()
+        for k in range(n - 3, n):
+            assert torch.equal(recs[k], want[k]), (rep, k)
+
+
 def test_split_stages_match_points():
     """eca_bounds_handcrafted + eca_rescore_handcrafted == eca_points_handcrafted."""
     import ctypes
