@@ -649,21 +649,23 @@ def train_leg(eb, dev) -> dict:
     from paper_2210_14771_b200 import training as tr
     x, t = _train_data(TRAIN_M)
     xd, td = torch.from_numpy(x).to(dev), torch.from_numpy(t).to(dev)
-    cfg = tr.TrainConfig(learning_rate=0.001, batch_size=TRAIN_BATCH, max_epochs=1)
+    epochs = 4
+    cfg = tr.TrainConfig(learning_rate=0.001, batch_size=TRAIN_BATCH, max_epochs=epochs)
     net = eb.EdgeNet(eb.ChannelStats((100.0,) * 3, (50.0,) * 3), seed=0)
     tr.train(net, (xd[:64], td[:64]), None, cfg)   # warm-up
     torch.cuda.synchronize()
-    reps = 3
     t0 = time.perf_counter()
-    for _ in range(reps):
-        tr.train(eb.EdgeNet(eb.ChannelStats((100.0,) * 3, (50.0,) * 3), seed=0), (xd, td), None, cfg)
+    tr.train(eb.EdgeNet(eb.ChannelStats((100.0,) * 3, (50.0,) * 3), seed=0), (xd, td), None, cfg)
     torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / reps
-    steps = TRAIN_M // TRAIN_BATCH
-    return {"metric": "EdgeNet training samples/s (§8f-4: SGD epoch, batch 8 strips of 5x7x1920, "
+    dt = time.perf_counter() - t0
+    steps = epochs * (TRAIN_M // TRAIN_BATCH)
+    return {"metric": "EdgeNet training samples/s (§8f-4: SGD epochs, batch 8 strips of 5x7x1920, "
                       "forward + BCE + backward + update)",
-            "value": round(TRAIN_M / dt, 1), "unit": "samples/s", "ms_per_step": round(1e3 * dt / steps, 4),
-            "steps": steps, "launches_per_step": 16, "dtype": "f32", "data": "synthetic normal strips"}
+            "value": round(epochs * TRAIN_M / dt, 1), "unit": "samples/s",
+            "ms_per_step": round(1e3 * dt / steps, 4), "steps": steps, "epochs": epochs,
+            "launches_per_step": 16, "dtype": "f32", "data": "synthetic normal strips",
+            "method": "wall clock of edgenet.train over 4 epochs of 2048 strips resident in HBM: epoch 1 "
+                      "eager, epoch 2 captured as a CUDA graph, epochs 3-4 graph replays"}
 
 
 _CPU_TRAIN = None

@@ -88,7 +88,10 @@ class _Trainer:
         self.ws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
         self.ws_bytes = nb.value
         self.diverged = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.st = _stream(dev)
+
+    @property
+    def st(self):   # the current stream at call time (a CUDA-graph capture stream inside one)
+        return _stream(self.dev)
 
     def forward(self, x: torch.Tensor, idx, m: int, logits: torch.Tensor | None = None) -> None:
         _lib.check(self.lib.eca_edgenet_forward(
@@ -167,9 +170,8 @@ def train(net: EdgeNet, train_samples, val_samples, cfg: TrainConfig | None = No
     vsteps = list(range(0, len(vx), vb)) if val_samples is not None else []
     vlosses = torch.zeros(max(1, len(vsteps)), dtype=torch.float64, device=dev)
     order_d = torch.empty(n, dtype=torch.int32, device=dev)
-    for epoch in range(cfg.max_epochs):
-        order = rng.permutation(n) if cfg.shuffle else np.arange(n)
-        order_d.copy_(torch.from_numpy(order.astype(np.int32)))
+
+    def epoch_steps():
         for k, s in enumerate(steps):
             m = min(cfg.batch_size, n - s)
             idx = ctypes.c_void_p(order_d.data_ptr() + 4 * s)
@@ -177,6 +179,25 @@ def train(net: EdgeNet, train_samples, val_samples, cfg: TrainConfig | None = No
             tr.backward(xs, ts, idx, m, losses[k:k + 1])
             if cfg.learning_rate != 0.0:
                 tr.sgd(cfg.learning_rate)
+
+    # An epoch's launch sequence depends only on (n, batch size): from the
+    # second epoch on it replays as one CUDA graph (the permutation is copied
+    # into order_d in front of it), instead of ~16 launches per step from the
+    # host.  The first epoch runs eagerly (and warms the kernels up).
+    graph = None
+    for epoch in range(cfg.max_epochs):
+        order = rng.permutation(n) if cfg.shuffle else np.arange(n)
+        order_d.copy_(torch.from_numpy(order.astype(np.int32)))
+        if graph is not None:
+            graph.replay()
+        elif epoch == 0 or len(steps) < 4:
+            epoch_steps()
+        else:
+            torch.cuda.synchronize(dev)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                epoch_steps()
+            graph.replay()
         lh = losses.cpu().numpy()
         bad = np.flatnonzero(~np.isfinite(lh))
         if len(bad):
