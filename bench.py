@@ -735,12 +735,13 @@ def eval_cpu(pairs) -> dict:
 
 
 def uhd_leg(eb, dev, peaks) -> dict:
-    """BASELINE config 4: 3840x2160 frames (the C2 mix rendered at 4K), 64 per
-    step, through the same streamed path, frames resident in HBM."""
+    """BASELINE config 4: 3840x2160 frames (the C2 mix rendered at 4K), 128 per
+    step (4096 half-row items: the GPU's 2368 bound-and-prune warps stay busy),
+    through the same streamed path, frames resident in HBM (12.7 GB pool)."""
     import torch
     from paper_2210_14771_b200 import synth
     from paper_2210_14771_b200.engine import ContentAreaEngine
-    w, h, b = 3840, 2160, 64
+    w, h, b = 3840, 2160, 128
     specs = synth.bench_specs(8, w, h, seed=2024)
     base = torch.from_numpy(np.stack([synth.render(sp, 40000 + k) for k, (_, sp) in enumerate(specs)])).to(dev)
     slots = 4
@@ -764,9 +765,12 @@ def uhd_leg(eb, dev, peaks) -> dict:
     torch.cuda.synchronize()
     ms = a.elapsed_time(e) / steps
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(4):
+        eng.bounds(pool[(i % slots) * b:(i % slots + 1) * b], overlap=True, slot=i % 4)
+    torch.cuda.synchronize()
     k0.record(stream)
-    for i in range(steps):
-        eng.bounds(pool[(i % slots) * b:(i % slots + 1) * b])
+    for i in range(steps):   # the pipeline's launch mode, as the 1080p roofline
+        eng.bounds(pool[(i % slots) * b:(i % slots + 1) * b], overlap=True, slot=i % 4)
     k1.record(stream)
     torch.cuda.synchronize()
     k_ms = k0.elapsed_time(k1) / steps
@@ -775,11 +779,12 @@ def uhd_leg(eb, dev, peaks) -> dict:
     peak = peaks.get("hbm_gbs", 6650.0)
     del pool
     torch.cuda.empty_cache()
-    return {"metric": "4K frames/s (3840x2160, C2 mix rendered at 4K, 64 per step, streamed)",
+    return {"metric": "4K frames/s (3840x2160, C2 mix rendered at 4K, 128 per step, streamed)",
             "value": round(b / (ms * 1e-3), 1), "unit": "frames/s", "ms_per_step": round(ms, 5),
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(gbs / peak, 4), "kernel": "eca::bounds_kernel<1, 0>",
-                         "kernel_ms": round(k_ms, 5), "algorithmic_bytes_per_launch": nbytes}}
+                         "kernel_ms": round(k_ms, 5), "algorithmic_bytes_per_launch": nbytes,
+                         "launch_mode": "back to back with programmatic dependent launch, 4 workspaces"}}
 
 
 def latency(eb, dev) -> dict:

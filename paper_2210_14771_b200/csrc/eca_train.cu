@@ -74,8 +74,12 @@ TrainWs train_ws(int m, int h, int w) {
 template <int CI, int CO>
 __global__ void __launch_bounds__(128) conv3_fwd(const float* x, const int32_t* idx, int m, int hi,
                                                  int wi, const float* wk, const float* bias, float* y) {
-  __shared__ float sw[CO * CI * 9], sb[CO];
-  for (int i = threadIdx.x; i < CO * CI * 9; i += blockDim.x) sw[i] = wk[i];
+  // weights transposed to [in][ky][kx][out]: a position's output-channel
+  // vector is contiguous (16-byte shared loads)
+  __shared__ __align__(16) float sw[CO * CI * 9];
+  __shared__ float sb[CO];
+  for (int j = threadIdx.x; j < CO * CI * 9; j += blockDim.x)   // contiguous shared stores
+    sw[j] = wk[(j % CO) * CI * 9 + j / CO];
   for (int i = threadIdx.x; i < CO; i += blockDim.x) sb[i] = bias[i];
   __syncthreads();
   const int ho = hi - 2, wo = wi - 2;
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(128) conv3_fwd(const float* x, const int32_t* 
     for (int k = 0; k < 9; ++k) {
       const float v = xs[(int64_t(c) * hi + oy + k / 3) * wi + ox + k % 3];
 #pragma unroll
-      for (int o = 0; o < CO; ++o) acc[o] = fmaf(sw[(o * CI + c) * 9 + k], v, acc[o]);
+      for (int o = 0; o < CO; ++o) acc[o] = fmaf(sw[(c * 9 + k) * CO + o], v, acc[o]);
     }
   float* ys = y + int64_t(b) * CO * ho * wo + int64_t(oy) * wo + ox;
 #pragma unroll
@@ -234,8 +238,12 @@ __global__ void wgrad_reduce(const float* part, int nseg, int nw, float* gw, flo
 template <int CI, int CO>
 __global__ void __launch_bounds__(128) conv3_dgrad(const float* dy, const float* xin, int m, int hi,
                                                    int wi, const float* wk, float* dx) {
-  __shared__ float sw[CO * CI * 9];
-  for (int i = threadIdx.x; i < CO * CI * 9; i += blockDim.x) sw[i] = wk[i];
+  // weights as [out][ky][kx][in]: the input-channel vector of (o, ky, kx) is contiguous
+  __shared__ __align__(16) float sw[CO * CI * 9];
+  for (int j = threadIdx.x; j < CO * CI * 9; j += blockDim.x) {   // contiguous shared stores
+    const int o = j / (9 * CI), k = (j / CI) % 9, c = j % CI;
+    sw[j] = wk[(o * CI + c) * 9 + k];
+  }
   __syncthreads();
   const int ho = hi - 2, wo = wi - 2;
   const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(128) conv3_dgrad(const float* dy, const float*
       if (yy < 0 || yy >= ho || xx < 0 || xx >= wo) continue;
       const float g = dy[((int64_t(b) * CO + o) * ho + yy) * wo + xx];
 #pragma unroll
-      for (int c = 0; c < CI; ++c) acc[c] = fmaf(g, sw[(o * CI + c) * 9 + k], acc[c]);
+      for (int c = 0; c < CI; ++c) acc[c] = fmaf(g, sw[(o * 9 + k) * CI + c], acc[c]);
     }
 #pragma unroll
   for (int c = 0; c < CI; ++c) {
