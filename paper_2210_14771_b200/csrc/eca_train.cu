@@ -223,14 +223,32 @@ __global__ void __launch_bounds__(256) conv_wgrad(const float* dy, const float* 
   }
 }
 
-// grads[off + i] = sum over segments (fixed order) of part[seg][i]
-__global__ void wgrad_reduce(const float* part, int nseg, int nw, float* gw, float* gb, int nb) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nw + nb) return;
+// grads[i] = sum over segments of part[seg][i] in a fixed order: 8 groups of
+// consecutive segments summed in parallel (threadIdx.y), then the 8 partial
+// sums in group order -- deterministic, and 8x shorter dependent chains
+constexpr int kRedGroups = 8;
+__global__ void __launch_bounds__(32 * kRedGroups) wgrad_reduce(const float* part, int nseg, int nw,
+                                                                float* gw, float* gb, int nb) {
+  __shared__ float red[kRedGroups][32];
+  const int i = blockIdx.x * 32 + threadIdx.x, g = threadIdx.y;
+  const int per = (nseg + kRedGroups - 1) / kRedGroups;
+  const int s0 = g * per, s1 = min(nseg, s0 + per);
   float acc = 0.f;
-  for (int s = 0; s < nseg; ++s) acc += part[size_t(s) * (nw + nb) + i];
-  if (i < nw) gw[i] = acc;
-  else gb[i - nw] = acc;
+  if (i < nw + nb)
+    for (int s = s0; s < s1; ++s) acc += part[size_t(s) * (nw + nb) + i];
+  red[g][threadIdx.x] = acc;
+  __syncthreads();
+  if (g == 0 && i < nw + nb) {
+    float v = red[0][threadIdx.x];
+#pragma unroll
+    for (int k = 1; k < kRedGroups; ++k) v += red[k][threadIdx.x];
+    if (i < nw) gw[i] = v;
+    else gb[i - nw] = v;
+  }
+}
+
+void reduce_grads(const float* part, int nseg, int nw, float* gw, float* gb, int nb, cudaStream_t st) {
+  wgrad_reduce<<<(nw + nb + 31) / 32, dim3(32, kRedGroups), 0, st>>>(part, nseg, nw, gw, gb, nb);
 }
 
 // dx[c][y][x] = sum_{o,ky,kx} dy[o][y-ky][x-kx] * w[o][c][ky][kx], times the
@@ -340,24 +358,21 @@ int eca_edgenet_backward(const float* x, const float* targets, const int32_t* in
   float* p1 = p2 + size_t(L.nseg2) * (4608 + 32);
   float* p0 = p1 + size_t(L.nseg1) * (1152 + 16);
   conv_wgrad<32, 1, 1><<<L.nseg3, 256, 0, st>>>(f(L.dlog), f(L.a3), nullptr, m, h - 6, w - 6, p3);
-  wgrad_reduce<<<1, 64, 0, st>>>(p3, L.nseg3, 32, out_grads + kOffW3, out_grads + kOffB3, 1);
+  reduce_grads(p3, L.nseg3, 32, out_grads + kOffW3, out_grads + kOffB3, 1, st);
   head_dgrad<<<blocks(n, 128), 128, 0, st>>>(f(L.dlog), f(L.a3), plane, m, net, f(L.d3));
   // layer 2 (16 -> 32)
   conv_wgrad<16, 32, 3><<<L.nseg2, 256, 0, st>>>(f(L.d3), f(L.a2), nullptr, m, h - 4, w - 4, p2);
-  wgrad_reduce<<<blocks(4608 + 32, 256), 256, 0, st>>>(p2, L.nseg2, 4608, out_grads + kOffW2,
-                                                       out_grads + kOffB2, 32);
+  reduce_grads(p2, L.nseg2, 4608, out_grads + kOffW2, out_grads + kOffB2, 32, st);
   conv3_dgrad<16, 32><<<blocks(int64_t(m) * (h - 4) * (w - 4), 128), 128, 0, st>>>(
       f(L.d3), f(L.a2), m, h - 4, w - 4, net + kOffW2, f(L.d2));
   // layer 1 (8 -> 16)
   conv_wgrad<8, 16, 3><<<L.nseg1, 256, 0, st>>>(f(L.d2), f(L.a1), nullptr, m, h - 2, w - 2, p1);
-  wgrad_reduce<<<blocks(1152 + 16, 256), 256, 0, st>>>(p1, L.nseg1, 1152, out_grads + kOffW1,
-                                                       out_grads + kOffB1, 16);
+  reduce_grads(p1, L.nseg1, 1152, out_grads + kOffW1, out_grads + kOffB1, 16, st);
   conv3_dgrad<8, 16><<<blocks(int64_t(m) * (h - 2) * (w - 2), 128), 128, 0, st>>>(
       f(L.d2), f(L.a1), m, h - 2, w - 2, net + kOffW1, f(L.d1));
   // layer 0 (5 -> 8): weights only (the input gradient is not needed)
   conv_wgrad<5, 8, 3><<<L.nseg0, 256, 0, st>>>(f(L.d1), x, index, m, h, w, p0);
-  wgrad_reduce<<<blocks(360 + 8, 256), 256, 0, st>>>(p0, L.nseg0, 360, out_grads + kOffW0,
-                                                     out_grads + kOffB0, 8);
+  reduce_grads(p0, L.nseg0, 360, out_grads + kOffW0, out_grads + kOffB0, 8, st);
   return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
 }
 
