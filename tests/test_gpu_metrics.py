@@ -138,3 +138,27 @@ def test_fitted_records_evaluate_against_truth():
                                  (a.circle.cx, a.circle.cy, a.circle.r),
                                  None if t is None else (t.cx, t.cy, t.r), 640, 480)
         assert abs(v - want) <= 1e-8, (a, t, v, want)
+
+
+try:
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+except ImportError:   # pragma: no cover
+    given = None
+
+if given is not None:
+    @given(data=st.data())
+    @settings(max_examples=40, deadline=None)
+    def test_hausdorff_metric_axioms(data):
+        """test_metrics.py:113-131 on the GPU distance: symmetry, identity,
+        triangle inequality, and equality with the oracle."""
+        def point_set(label):
+            n = data.draw(st.integers(1, 12), label=label)
+            return np.array(data.draw(st.lists(st.tuples(st.floats(-50, 50), st.floats(-50, 50)),
+                                               min_size=n, max_size=n), label=label + "_pts"))
+        a, b, c = point_set("a"), point_set("b"), point_set("c")
+        hab = gm.hausdorff(a, b)
+        assert hab == gm.hausdorff(b, a)
+        assert gm.hausdorff(a, a) == 0.0
+        assert gm.hausdorff(a, c) <= hab + gm.hausdorff(b, c) + 1e-9
+        assert hab == orc.hausdorff(a, b)
