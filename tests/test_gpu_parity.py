@@ -529,3 +529,40 @@ def test_learned_tile_edges_match_oracle(w, h, tc):
                              layers)
         got = eng.probs[k].cpu().numpy()[:len(rows)]
         assert np.abs(got - want).max() <= 1e-5, (k, np.abs(got - want).max())
+
+
+try:
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+except ImportError:   # pragma: no cover
+    given = None
+
+if given is not None:
+    @given(data=st.data())
+    @settings(max_examples=60, deadline=None)
+    def test_ransac_fuzz_matches_oracle(data):
+        """Random candidate sets -- points near a random circle plus outliers,
+        ragged counts, random seeds, exhaustive or seeded -- through the GPU
+        fitter against the oracle: status and inlier count exact, circle within
+        1e-3 px, score rel 1e-12 (fitting.py:159-230; cf. the reference's
+        test_accepted_fits_always_satisfy_gates)."""
+        w, h = data.draw(st.sampled_from([(640, 480), (1920, 1080), (300, 200)]))
+        cx = data.draw(st.floats(0.2 * w, 0.8 * w))
+        cy = data.draw(st.floats(0.2 * h, 0.8 * h))
+        r = data.draw(st.floats(0.12 * w, 0.75 * w))
+        n_in = data.draw(st.integers(0, 28))
+        n_out = data.draw(st.integers(0, 8))
+        seed = data.draw(st.integers(0, 2**31 - 1))
+        rng = np.random.default_rng(seed)
+        t = rng.uniform(0, 2 * np.pi, n_in)
+        pts = np.column_stack([cx + r * np.cos(t) + rng.normal(0, 1.0, n_in),
+                               cy + r * np.sin(t) + rng.normal(0, 1.0, n_in)])
+        pts = np.vstack([pts, rng.uniform([3, 3], [w - 4, h - 4], (n_out, 2))])
+        pts = np.clip(np.rint(pts), [3, 3], [w - 4, h - 4]).astype(int)
+        scores = rng.uniform(0.05, 1.0, len(pts))
+        cfg = eb.EcaConfig()
+        exhaustive = data.draw(st.booleans()) and len(pts) <= 12
+        cands = [eb.EdgeCandidate(int(x), int(y), float(s), eb.Side.LEFT) for (x, y), s in zip(pts, scores)]
+        got = eb.ransac_fit(cands, (w, h), cfg, seed % 1000, exhaustive=exhaustive)
+        want = orc.ransac(pts[:, 0], pts[:, 1], scores, w, h, cfg, seed % 1000, exhaustive=exhaustive)
+        assert_fit_equal(got, want, (w, h, cx, cy, r, n_in, n_out, seed))
