@@ -553,16 +553,23 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     group_sync(grp);   // also: every a0 read of this tile's MMAs is long complete
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-      float y[4];
+      float v1[4], v2[4], y[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        float v1 = __shfl_down_sync(kFull, d[r][1][c], 1);
-        float v2 = __shfl_down_sync(kFull, d[r][2][c], 2);
-        if (q < 3) {
-          if (lane == 31) v1 = xch[(((r * 4 + q + 1) * 2 + 0) * 2 + 0) * 8 + 4 * ch + c];
-          if (lane >= 30) v2 = xch[(((r * 4 + q + 1) * 2 + (lane - 30)) * 2 + 1) * 8 + 4 * ch + c];
+        v1[c] = __shfl_down_sync(kFull, d[r][1][c], 1);
+        v2[c] = __shfl_down_sync(kFull, d[r][2][c], 2);
+      }
+      if (q < 3 && lane >= 30) {   // two lanes: the next warp's first positions
+        const float* nx = xch + ((r * 4 + q + 1) * 2) * 2 * 8 + 4 * ch;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (lane == 31) v1[c] = nx[c];                       // lane 0, kx 1
+          v2[c] = nx[((lane - 30) * 2 + 1) * 8 + c];           // lane 0/1, kx 2
         }
-        const float v = (d[r][0][c] + v1) + v2 + s.b0v[4 * ch + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float v = (d[r][0][c] + v1[c]) + v2[c] + s.b0v[4 * ch + c];
         y[c] = v > 0.f ? v : 0.f;
       }
       st_hilo(a1(r, 0), a1(r, 1), kmaj_off(m, 4 * ch, kSbo1), make_float4(y[0], y[1], y[2], y[3]));
@@ -607,16 +614,23 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     group_sync(grp);
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      float y[8];
+      float v1[8], v2[8], y[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        float v1 = __shfl_down_sync(kFull, d[r][1][c], 1);
-        float v2 = __shfl_down_sync(kFull, d[r][2][c], 2);
-        if (q < 3) {
-          if (lane == 31) v1 = xch[(((r * 4 + q + 1) * 2 + 0) * 2 + 0) * 16 + 8 * ch + c];
-          if (lane >= 30) v2 = xch[(((r * 4 + q + 1) * 2 + (lane - 30)) * 2 + 1) * 16 + 8 * ch + c];
+        v1[c] = __shfl_down_sync(kFull, d[r][1][c], 1);
+        v2[c] = __shfl_down_sync(kFull, d[r][2][c], 2);
+      }
+      if (q < 3 && lane >= 30) {   // two lanes: the next warp's first positions
+        const float* nx = xch + ((r * 4 + q + 1) * 2) * 2 * 16 + 8 * ch;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (lane == 31) v1[c] = nx[c];
+          v2[c] = nx[((lane - 30) * 2 + 1) * 16 + c];
         }
-        const float v = (d[r][0][c] + v1) + v2 + s.b1v[8 * ch + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float v = (d[r][0][c] + v1[c]) + v2[c] + s.b1v[8 * ch + c];
         y[c] = v > 0.f ? v : 0.f;
       }
       st_hilo(a2(r, 0), a2(r, 1), kmaj_off(m, 8 * ch, kSbo2), make_float4(y[0], y[1], y[2], y[3]));
@@ -657,16 +671,24 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     group_sync(grp);
+    float v1[16], v2[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      v1[c] = __shfl_down_sync(kFull, d[1][c], 1);
+      v2[c] = __shfl_down_sync(kFull, d[2][c], 2);
+    }
+    if (q < 3 && lane >= 30) {   // two lanes: the next warp's first positions
+      const float* nx = xch + ((q + 1) * 2) * 2 * 32 + 16 * ch;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        if (lane == 31) v1[c] = nx[c];
+        v2[c] = nx[((lane - 30) * 2 + 1) * 32 + c];
+      }
+    }
     float z = 0.f;
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-      float v1 = __shfl_down_sync(kFull, d[1][c], 1);
-      float v2 = __shfl_down_sync(kFull, d[2][c], 2);
-      if (q < 3) {
-        if (lane == 31) v1 = xch[(((q + 1) * 2 + 0) * 2 + 0) * 32 + 16 * ch + c];
-        if (lane >= 30) v2 = xch[(((q + 1) * 2 + (lane - 30)) * 2 + 1) * 32 + 16 * ch + c];
-      }
-      const float v = (d[0][c] + v1) + v2 + s.b2v[16 * ch + c];
+      const float v = (d[0][c] + v1[c]) + v2[c] + s.b2v[16 * ch + c];
       z = fmaf(s.w3[16 * ch + c], v > 0.f ? v : 0.f, z);
     }
     G.zpart[ch][m] = z;
