@@ -279,6 +279,7 @@ struct CnnSmemTc {
   uint8_t b2[2][3][3][kWt2];      // layer-2 weights [hi/lo][ky][kx][out 32][in 16]
   float b0v[8], b1v[16], b2v[32], w3[32], b3;
   float lut[3][256];              // float((v - mean_c) / std_c), computed in FP64
+  float ytab[ECA_MAX_STRIPS * 7];  // Y channel of rows y-3..y+3 of every strip (edgenet.py:80-82)
   uint32_t tmem;
 };
 
@@ -426,6 +427,11 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
     const int ch = i >> 8, v = i & 255;
     s.lut[ch][v] = float(div_rn(sub_rn(double(v), J.mean[ch]), J.stdv[ch]));
   }
+  {
+    const double yden0 = double(H - 1 > 1 ? H - 1 : 1), yc0 = div_rn(double(H - 1), 2.0);
+    for (int i = tid; i < J.S * 7; i += nt)
+      s.ytab[i] = float(div_rn(sub_rn(double(J.rows[i / 7] - 3 + i % 7), yc0), yden0));
+  }
   const int grp = warp >> 3, gtid = tid & (kGThreads - 1);
   CnnGroupTc& G = s.grp[grp];
   const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&G.bar));
@@ -492,12 +498,14 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
 
   // ---- RGBXY window (edgenet.py:75-82), rows h-3..h+3, positions j0..j0+127,
   // written as the layer-0 operand rows (K lanes: R, G, B, X, Y, 0, 0, 0) ----
-  const int h = J.rows[strip];
+  static_assert(kGThreads % kTP == 0, "a thread keeps one window column");
+  const int wc = gtid % kTP;   // this thread's column for all its window pixels
+  const float fx_c = j0 + wc < W ? float(div_rn(sub_rn(double(j0 + wc), xc), xden)) : 0.f;
 #pragma unroll
   for (int k = 0; k < kPxPer; ++k) {
     const int i = gtid + k * kGThreads;
     if (i < kWinPx) {
-      const int r = i / kTP, c = i % kTP, x = j0 + c;
+      const int r = i / kTP, c = wc, x = j0 + c;
       const uint32_t v = px_next[k];
       float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
       float fy = 0.f;
@@ -505,8 +513,8 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
         f.x = s.lut[0][v & 255u];
         f.y = s.lut[1][(v >> 8) & 255u];
         f.z = s.lut[2][(v >> 16) & 255u];
-        f.w = float(div_rn(sub_rn(double(x), xc), xden));
-        fy = float(div_rn(sub_rn(double(h - 3 + r), yc), yden));
+        f.w = fx_c;
+        fy = s.ytab[strip * 7 + r];
       }
       st_hilo(a0(r, 0), a0(r, 1), kmaj_off(c, 0, kSbo1), f);
       st_hilo(a0(r, 0), a0(r, 1), kmaj_off(c, 4, kSbo1), make_float4(fy, 0.f, 0.f, 0.f));
