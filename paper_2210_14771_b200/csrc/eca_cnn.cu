@@ -269,7 +269,7 @@ struct CnnGroupTc {               // one tile in flight
   alignas(1024) uint8_t act[kAct];
   float xch[768];                 // epilogue neighbour exchange (lanes 0/1 of each warp)
   float zpart[2][kTP];            // head partial sums per channel half
-  uint64_t bar;                   // MMA completion
+  uint64_t bar[3];                // MMA completion per layer (5 / 3 / 1 issuing threads)
 };
 
 struct CnnSmemTc {
@@ -434,11 +434,18 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   }
   const int grp = warp >> 3, gtid = tid & (kGThreads - 1);
   CnnGroupTc& G = s.grp[grp];
-  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&G.bar));
+  // the MMA chains of different output rows are independent: layer 0's five
+  // rows are issued by five warps, layer 1's three by three, layer 2's one
+  // chain by one thread; each layer's mbarrier counts its issuers' commits
+  const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&G.bar[0]));
+  const uint32_t bar1 = bar0 + 8u, bar2 = bar0 + 16u;
   if (gtid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 5;" ::"r"(bar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 3;" ::"r"(bar1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar2));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  const int gw = (gtid >> 5);   // warp index within the group
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         static_cast<uint32_t>(__cvta_generic_to_shared(&s.tmem))));
@@ -524,18 +531,17 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
 
   // ---- layer 0 (tensor cores): D0[r][kx] = sum_ky a0[r + ky] . b0[ky][kx],
   // N = 48 (three zero-padded 16-row kx blocks) ----
-  if (gtid == 0) {
+  if (gw < 5 && lane == 0) {   // output row r = gw
     constexpr uint32_t id0 = idesc_tf32(48);
-    for (int r = 0; r < 5; ++r)
-      for (int ky = 0; ky < 3; ++ky)
-        mma3(tmem + uint32_t(r * 48), saddr(a0(r + ky, 0)), saddr(a0(r + ky, 1)), kSbo1,
-             saddr(s.b0[0][ky][0]), saddr(s.b0[1][ky][0]), kSbo1, id0, ky == 0);
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+    const int r = gw;
+    for (int ky = 0; ky < 3; ++ky)
+      mma3(tmem + uint32_t(r * 48), saddr(a0(r + ky, 0)), saddr(a0(r + ky, 1)), kSbo1,
+           saddr(s.b0[0][ky][0]), saddr(s.b0[1][ky][0]), kSbo1, id0, ky == 0);
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0)
                  : "memory");
   }
   load_window(t + t_step);   // the next tile's bytes arrive under this tile's MMAs
-  bar_wait(bar, phase);
-  phase ^= 1u;
+  bar_wait(bar0, phase);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   // ---- layer-0 epilogue: o1[r][m] = D[0][m] + D[1][m+1] + D[2][m+2] + b0, ReLU,
@@ -587,17 +593,16 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
 
   // ---- layer 1 (tensor cores): D1[r][kx] = sum_ky a1[r + ky] . b1[ky][kx];
   // the three kx weight blocks are adjacent rows of one N = 48 operand ----
-  if (gtid == 0) {
+  if (gw < 3 && lane == 0) {   // output row r = gw
     constexpr uint32_t id1 = idesc_tf32(48);
-    for (int r = 0; r < 3; ++r)
-      for (int ky = 0; ky < 3; ++ky)
-        mma3(tmem + uint32_t(r * 48), saddr(a1(r + ky, 0)), saddr(a1(r + ky, 1)), kSbo1,
-             saddr(s.b1[0][ky][0]), saddr(s.b1[1][ky][0]), kSbo1, id1, ky == 0);
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+    const int r = gw;
+    for (int ky = 0; ky < 3; ++ky)
+      mma3(tmem + uint32_t(r * 48), saddr(a1(r + ky, 0)), saddr(a1(r + ky, 1)), kSbo1,
+           saddr(s.b1[0][ky][0]), saddr(s.b1[1][ky][0]), kSbo1, id1, ky == 0);
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar1)
                  : "memory");
   }
-  bar_wait(bar, phase);
-  phase ^= 1u;
+  bar_wait(bar1, phase);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   // ---- layer-1 epilogue -> layer-2 operand rows (over a1: its MMAs completed);
@@ -656,11 +661,11 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
         mma3(tmem, saddr(a2(ky, 0)) + 256u * j, saddr(a2(ky, 1)) + 256u * j, kSbo2,
              saddr(s.b2[0][ky][0]) + 256u * j, saddr(s.b2[1][ky][0]) + 256u * j, kSbo2, id2,
              ky == 0 && j == 0);
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar2)
                  : "memory");
   }
-  bar_wait(bar, phase);
-  phase ^= 1u;
+  bar_wait(bar2, phase);
+  phase ^= 1u;   // each layer's barrier completes once per tile
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   // ---- layer-2 epilogue + head: channels 16ch..16ch+15 per warp, partial
