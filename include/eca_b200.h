@@ -280,7 +280,8 @@ int eca_hausdorff_points(const double* a, int na, const double* b, int nb, void*
 /* EdgeNet training pieces (edgenet.py:100-130, 182-211, 213-225, 236-241,
  * 277-344), FP32.  x: [*][5][h][w] float32 RGBXY samples (NCHW, the
  * reference's training inputs), targets: [*][1][h-6][w-6]; index: the m
- * sample indices of this batch (null: samples 0..m-1).  net: ECA_NET_FLOATS
+ * sample indices of this batch, each < the number of samples in x / targets
+ * (device int32; null: samples 0..m-1).  net: ECA_NET_FLOATS
  * packed weights (kernel0, bias0, ..., kernel3, bias3 in reference order).
  * forward keeps the activations in the workspace (the reference's caches);
  * backward (after forward on the same batch) writes the mean stable BCE loss
