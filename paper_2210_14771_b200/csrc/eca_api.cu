@@ -479,6 +479,9 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
 #ifndef ECA_PIPE_SETS
 #define ECA_PIPE_SETS 16
 #endif
+#ifndef ECA_PIPE_SHARE   // leave one bound-and-prune CTA slot per SM to the side stream
+#define ECA_PIPE_SHARE 1
+#endif
 constexpr int kPipeSets = ECA_PIPE_SETS;
 struct EcaPipeline {
   int batch, n_strips;
@@ -588,7 +591,7 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   J.out_score = P->sc[s];
   // the fit kPipeSets batches back has finished reading this set
   if (P->used[s] && cudaStreamWaitEvent(st, P->ev_free[s], 0) != cudaSuccess) return ECA_ERR_CUDA;
-  int rc = launch_bounds(J, P->ws[s], st, /*overlap=*/true, /*share=*/true,
+  int rc = launch_bounds(J, P->ws[s], st, /*overlap=*/true, /*share=*/ECA_PIPE_SHARE != 0,
                          (flags & ECA_BOUNDS_ZERO_COPY) != 0);
   if (rc) return rc;
   if (cudaEventRecord(P->ev_bounds[s], st) != cudaSuccess ||
