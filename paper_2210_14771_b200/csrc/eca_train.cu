@@ -70,10 +70,12 @@ TrainWs train_ws(int m, int h, int w) {
 }
 
 // ---------------------------------------------------------------- forward ---
-// x: [*][CI][hi][wi] (sample idx[b] when idx, else b) -> y: [m][CO][hi-2][wi-2]
-template <int CI, int CO>
+// x: [*][CI][hi][wi] (sample idx[b] when idx, else b) -> y: [m][CO][hi-2][wi-2];
+// blockIdx.y picks a group of CO / OG output channels (more threads per layer)
+template <int CI, int CO, int OG>
 __global__ void __launch_bounds__(128) conv3_fwd(const float* x, const int32_t* idx, int m, int hi,
                                                  int wi, const float* wk, const float* bias, float* y) {
+  constexpr int CPG = CO / OG;
   // weights transposed to [in][ky][kx][out]: a position's output-channel
   // vector is contiguous (16-byte shared loads)
   __shared__ __align__(16) float sw[CO * CI * 9];
@@ -82,27 +84,27 @@ __global__ void __launch_bounds__(128) conv3_fwd(const float* x, const int32_t* 
     sw[j] = wk[(j % CO) * CI * 9 + j / CO];
   for (int i = threadIdx.x; i < CO; i += blockDim.x) sb[i] = bias[i];
   __syncthreads();
-  const int ho = hi - 2, wo = wi - 2;
+  const int ho = hi - 2, wo = wi - 2, o0 = blockIdx.y * CPG;
   const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= int64_t(m) * ho * wo) return;
   const int ox = int(p % wo), oy = int((p / wo) % ho), b = int(p / (int64_t(wo) * ho));
   const int s = idx ? idx[b] : b;
   const float* xs = x + int64_t(s) * CI * hi * wi;
-  float acc[CO];
+  float acc[CPG];
 #pragma unroll
-  for (int o = 0; o < CO; ++o) acc[o] = 0.f;
+  for (int o = 0; o < CPG; ++o) acc[o] = 0.f;
   for (int c = 0; c < CI; ++c)
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
       const float v = xs[(int64_t(c) * hi + oy + k / 3) * wi + ox + k % 3];
 #pragma unroll
-      for (int o = 0; o < CO; ++o) acc[o] = fmaf(sw[(c * 9 + k) * CO + o], v, acc[o]);
+      for (int o = 0; o < CPG; ++o) acc[o] = fmaf(sw[(c * 9 + k) * CO + o0 + o], v, acc[o]);
     }
   float* ys = y + int64_t(b) * CO * ho * wo + int64_t(oy) * wo + ox;
 #pragma unroll
-  for (int o = 0; o < CO; ++o) {
-    const float v = acc[o] + sb[o];
-    ys[int64_t(o) * ho * wo] = v * float(v > 0.f);   // y * (y > 0): -inf and NaN give NaN, as numpy
+  for (int o = 0; o < CPG; ++o) {
+    const float v = acc[o] + sb[o0 + o];
+    ys[int64_t(o0 + o) * ho * wo] = v * float(v > 0.f);   // y * (y > 0): -inf and NaN give NaN, as numpy
   }
 }
 
@@ -170,18 +172,15 @@ __global__ void loss_final(const double* lpart, int nblk, int64_t n, double* out
   }
 }
 
-// head backward: da3 = g * w3 * (a3 > 0)
-__global__ void __launch_bounds__(128) head_dgrad(const float* dlog, const float* a3, int64_t plane,
+// head backward: da3 = g * w3 * (a3 > 0), one thread per (position, channel)
+__global__ void __launch_bounds__(256) head_dgrad(const float* dlog, const float* a3, int64_t plane,
                                                   int m, const float* net, float* d3) {
-  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p >= int64_t(m) * plane) return;
-  const int64_t b = p / plane, q = p % plane;
-  const float g = dlog[p];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    const int64_t o = b * 32 * plane + c * plane + q;
-    d3[o] = (g * net[kOffW3 + c]) * float(a3[o] > 0.f);   // dx * mask (inf * 0 = NaN, as numpy)
-  }
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= int64_t(m) * 32 * plane) return;
+  const int64_t q = t % plane, bc = t / plane;   // bc = b * 32 + c
+  const int c = int(bc % 32);
+  const float g = dlog[(bc / 32) * plane + q];
+  d3[t] = (g * net[kOffW3 + c]) * float(a3[t] > 0.f);   // dx * mask (inf * 0 = NaN, as numpy)
 }
 
 // Weight / bias gradient partials of one segment (sample, output row, kSeg
@@ -209,7 +208,9 @@ __global__ void __launch_bounds__(256) conv_wgrad(const float* dy, const float* 
   }
   __syncthreads();
   float* out = part + size_t(seg) * (NW + CO);
-  for (int wi_ = threadIdx.x; wi_ < NW + CO; wi_ += blockDim.x) {
+  const int per = (NW + CO + gridDim.y - 1) / gridDim.y;   // this block's share of the weights
+  const int w0 = blockIdx.y * per, w1 = min(NW + CO, w0 + per);
+  for (int wi_ = w0 + threadIdx.x; wi_ < w1; wi_ += blockDim.x) {
     float acc = 0.f;
     if (wi_ < NW) {
       const int o = wi_ / (CI * K * K), c = (wi_ / (K * K)) % CI, k = wi_ % (K * K);
@@ -252,10 +253,12 @@ void reduce_grads(const float* part, int nseg, int nw, float* gw, float* gb, int
 }
 
 // dx[c][y][x] = sum_{o,ky,kx} dy[o][y-ky][x-kx] * w[o][c][ky][kx], times the
-// ReLU mask of the input (x_in > 0)
-template <int CI, int CO>
+// ReLU mask of the input (x_in > 0); blockIdx.y picks a group of CI / IG input
+// channels
+template <int CI, int CO, int IG>
 __global__ void __launch_bounds__(128) conv3_dgrad(const float* dy, const float* xin, int m, int hi,
                                                    int wi, const float* wk, float* dx) {
+  constexpr int CPG = CI / IG;
   // weights as [out][ky][kx][in]: the input-channel vector of (o, ky, kx) is contiguous
   __shared__ __align__(16) float sw[CO * CI * 9];
   for (int j = threadIdx.x; j < CO * CI * 9; j += blockDim.x) {   // contiguous shared stores
@@ -263,13 +266,13 @@ __global__ void __launch_bounds__(128) conv3_dgrad(const float* dy, const float*
     sw[j] = wk[(o * CI + c) * 9 + k];
   }
   __syncthreads();
-  const int ho = hi - 2, wo = wi - 2;
+  const int ho = hi - 2, wo = wi - 2, c0 = blockIdx.y * CPG;
   const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= int64_t(m) * hi * wi) return;
   const int x = int(p % wi), y = int((p / wi) % hi), b = int(p / (int64_t(wi) * hi));
-  float acc[CI];
+  float acc[CPG];
 #pragma unroll
-  for (int c = 0; c < CI; ++c) acc[c] = 0.f;
+  for (int c = 0; c < CPG; ++c) acc[c] = 0.f;
   for (int o = 0; o < CO; ++o)
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
@@ -277,11 +280,11 @@ __global__ void __launch_bounds__(128) conv3_dgrad(const float* dy, const float*
       if (yy < 0 || yy >= ho || xx < 0 || xx >= wo) continue;
       const float g = dy[((int64_t(b) * CO + o) * ho + yy) * wo + xx];
 #pragma unroll
-      for (int c = 0; c < CI; ++c) acc[c] = fmaf(g, sw[(o * 9 + k) * CI + c], acc[c]);
+      for (int c = 0; c < CPG; ++c) acc[c] = fmaf(g, sw[(o * 9 + k) * CI + c0 + c], acc[c]);
     }
 #pragma unroll
-  for (int c = 0; c < CI; ++c) {
-    const int64_t q = ((int64_t(b) * CI + c) * hi + y) * wi + x;
+  for (int c = 0; c < CPG; ++c) {
+    const int64_t q = ((int64_t(b) * CI + c0 + c) * hi + y) * wi + x;
     dx[q] = acc[c] * float(xin[q] > 0.f);
   }
 }
@@ -323,11 +326,11 @@ int eca_edgenet_forward(const float* x, const int32_t* index, int m, int h, int 
   float* a3 = reinterpret_cast<float*>(ws + L.a3);
   float* logit = reinterpret_cast<float*>(ws + L.logit);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  conv3_fwd<5, 8><<<blocks(int64_t(m) * (h - 2) * (w - 2), 128), 128, 0, st>>>(
+  conv3_fwd<5, 8, 1><<<dim3(blocks(int64_t(m) * (h - 2) * (w - 2), 128), 1), 128, 0, st>>>(
       x, index, m, h, w, net + kOffW0, net + kOffB0, a1);
-  conv3_fwd<8, 16><<<blocks(int64_t(m) * (h - 4) * (w - 4), 128), 128, 0, st>>>(
+  conv3_fwd<8, 16, 2><<<dim3(blocks(int64_t(m) * (h - 4) * (w - 4), 128), 2), 128, 0, st>>>(
       a1, nullptr, m, h - 2, w - 2, net + kOffW1, net + kOffB1, a2);
-  conv3_fwd<16, 32><<<blocks(int64_t(m) * (h - 6) * (w - 6), 128), 128, 0, st>>>(
+  conv3_fwd<16, 32, 4><<<dim3(blocks(int64_t(m) * (h - 6) * (w - 6), 128), 4), 128, 0, st>>>(
       a2, nullptr, m, h - 4, w - 4, net + kOffW2, net + kOffB2, a3);
   const int64_t plane = int64_t(h - 6) * (w - 6);
   head_fwd<<<blocks(m * plane, 128), 128, 0, st>>>(a3, plane, m, net, logit);
@@ -359,16 +362,16 @@ int eca_edgenet_backward(const float* x, const float* targets, const int32_t* in
   float* p0 = p1 + size_t(L.nseg1) * (1152 + 16);
   conv_wgrad<32, 1, 1><<<L.nseg3, 256, 0, st>>>(f(L.dlog), f(L.a3), nullptr, m, h - 6, w - 6, p3);
   reduce_grads(p3, L.nseg3, 32, out_grads + kOffW3, out_grads + kOffB3, 1, st);
-  head_dgrad<<<blocks(n, 128), 128, 0, st>>>(f(L.dlog), f(L.a3), plane, m, net, f(L.d3));
+  head_dgrad<<<blocks(n * 32, 256), 256, 0, st>>>(f(L.dlog), f(L.a3), plane, m, net, f(L.d3));
   // layer 2 (16 -> 32)
-  conv_wgrad<16, 32, 3><<<L.nseg2, 256, 0, st>>>(f(L.d3), f(L.a2), nullptr, m, h - 4, w - 4, p2);
+  conv_wgrad<16, 32, 3><<<dim3(L.nseg2, 4), 256, 0, st>>>(f(L.d3), f(L.a2), nullptr, m, h - 4, w - 4, p2);
   reduce_grads(p2, L.nseg2, 4608, out_grads + kOffW2, out_grads + kOffB2, 32, st);
-  conv3_dgrad<16, 32><<<blocks(int64_t(m) * (h - 4) * (w - 4), 128), 128, 0, st>>>(
+  conv3_dgrad<16, 32, 4><<<dim3(blocks(int64_t(m) * (h - 4) * (w - 4), 128), 4), 128, 0, st>>>(
       f(L.d3), f(L.a2), m, h - 4, w - 4, net + kOffW2, f(L.d2));
   // layer 1 (8 -> 16)
-  conv_wgrad<8, 16, 3><<<L.nseg1, 256, 0, st>>>(f(L.d2), f(L.a1), nullptr, m, h - 2, w - 2, p1);
+  conv_wgrad<8, 16, 3><<<dim3(L.nseg1, 2), 256, 0, st>>>(f(L.d2), f(L.a1), nullptr, m, h - 2, w - 2, p1);
   reduce_grads(p1, L.nseg1, 1152, out_grads + kOffW1, out_grads + kOffB1, 16, st);
-  conv3_dgrad<8, 16><<<blocks(int64_t(m) * (h - 2) * (w - 2), 128), 128, 0, st>>>(
+  conv3_dgrad<8, 16, 2><<<dim3(blocks(int64_t(m) * (h - 2) * (w - 2), 128), 2), 128, 0, st>>>(
       f(L.d2), f(L.a1), m, h - 2, w - 2, net + kOffW1, f(L.d1));
   // layer 0 (5 -> 8): weights only (the input gradient is not needed)
   conv_wgrad<5, 8, 3><<<L.nseg0, 256, 0, st>>>(f(L.d1), x, index, m, h, w, p0);
