@@ -472,10 +472,9 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
 // run_pipelined): bounds kernel of batch i on the caller's stream; rescore +
 // fit on the pipeline's side stream, overlapping batch i+1's bounds kernel.
 // kPipeSets buffer sets rotate inside the caller-provided scratch: batch i's
-// bounds kernel waits for the fit of batch i - kPipeSets (16 sets measured
-// 1.3 us per batch faster than 3; a host stream wait in front of a
-// programmatic-dependent launch costs its overlap, and a device-side
-// release flag instead starved the low-priority fits -- DESIGN.md).
+// bounds kernel waits (stream event) for the fit of batch i - kPipeSets.  16
+// sets measured 1.3 us per batch faster than 3; the step is set by how the
+// bound-and-prune kernel and the side stream share the SMs.
 #ifndef ECA_PIPE_SETS
 #define ECA_PIPE_SETS 16
 #endif
