@@ -156,7 +156,30 @@ __global__ void __launch_bounds__(256) crop_copy_kernel(const uint8_t* frames, i
   for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < rows; r += gridDim.x * (blockDim.x >> 5)) {
     const uint8_t* src = frames + int64_t(b) * fstride + int64_t(bd.y + r) * rstride + 3 * bd.x;
     uint8_t* dst = out + offs[b] + int64_t(r) * rb;
-    for (int i = lane; i < rb; i += 32) dst[i] = __ldg(src + i);
+    // Row = byte head up to a 16-B aligned dst, 16-B stores whose source bytes
+    // come from aligned 32-bit loads joined by funnel shifts (the source row
+    // starts at any byte: 3·x0), then a byte tail.
+    const int head = min(rb, int((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+    if (lane < head) dst[lane] = __ldg(src + lane);
+    const uint8_t* s = src + head;
+    uint8_t* d = dst + head;
+    const int m = rb - head, nv = m >> 4;
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(s);
+    const unsigned sh = 8u * unsigned(sa & 3);
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
+    for (int v = lane; v < nv; v += 32) {
+      const uint32_t* p = sw + 4 * v;
+      const uint32_t w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2), w3 = __ldg(p + 3);
+      // p[4] holds needed bytes only when the source is unaligned (never past the row).
+      const uint32_t w4 = sh ? __ldg(p + 4) : 0u;
+      uint4 o;
+      o.x = __funnelshift_r(w0, w1, sh);
+      o.y = __funnelshift_r(w1, w2, sh);
+      o.z = __funnelshift_r(w2, w3, sh);
+      o.w = __funnelshift_r(w3, w4, sh);
+      reinterpret_cast<uint4*>(d)[v] = o;
+    }
+    for (int i = nv * 16 + lane; i < m; i += 32) d[i] = __ldg(s + i);
   }
 }
 

@@ -510,6 +510,43 @@ def test_crop_area_copies_pixels():
         eb.crop_area(frame, eb.FULL_FRAME)
 
 
+def test_crop_copy_packed_batch_every_alignment():
+    """K5 copy through the C ABI: packed crops at every source byte offset
+    (3·x0 mod 4) and every destination offset mod 16, widths below and above
+    one 16-B vector, skipped (-1) entries in between."""
+    from paper_2210_14771_b200 import _lib, api
+    rng = np.random.default_rng(7)
+    B, H, W = 96, 70, 301
+    frames = rng.integers(0, 256, (B, H, W, 3), dtype=np.uint8)
+    bounds = np.full((B, 4), -1, dtype=np.int32)
+    for b in range(B):
+        if b % 11 == 5:
+            continue
+        x0 = int(rng.integers(0, W - 1))
+        x1 = int(min(W - 1, x0 + [0, 1, 4, 5, 6, 17, 40, 150, 300][b % 9]))
+        y0 = int(rng.integers(0, H - 1))
+        y1 = int(rng.integers(y0, H))
+        bounds[b] = (x0, y0, x1, y1)
+    sizes = [0 if r[0] < 0 else (r[2] - r[0] + 1) * (r[3] - r[1] + 1) * 3 for r in bounds]
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    max_rows = int(max(r[3] - r[1] + 1 for r in bounds if r[0] >= 0))
+    dev = torch.device("cuda:0")
+    f = torch.from_numpy(frames).to(dev)
+    bd = torch.from_numpy(bounds).to(dev)
+    od = torch.from_numpy(offs).to(dev)
+    out = torch.zeros(int(sum(sizes)) + 64, dtype=torch.uint8, device=dev)
+    _lib.check(_lib.load().eca_crop_copy(api._ptr(f), B, f.stride(0), f.stride(1), api._ptr(bd),
+                                         api._ptr(od), api._ptr(out), max_rows, api._stream(dev)),
+               "eca_crop_copy")
+    got = out.cpu().numpy()
+    for b, r in enumerate(bounds):
+        if r[0] < 0:
+            continue
+        want = frames[b, r[1]:r[3] + 1, r[0]:r[2] + 1].reshape(-1)
+        assert np.array_equal(got[offs[b]:offs[b] + sizes[b]], want), (b, r)
+    assert not got[int(sum(sizes)):].any()
+
+
 @pytest.mark.parametrize("w,h", [(40, 30), (128, 64), (134, 40), (250, 97), (517, 300), (1920, 60)])
 @pytest.mark.parametrize("tc", [True, False])
 def test_learned_tile_edges_match_oracle(w, h, tc):
