@@ -12,6 +12,13 @@
 
 using namespace eca;
 
+#ifndef ECA_MASK_CS   // tuning knob: streaming (evict-first) stores for the mask body
+#define ECA_MASK_CS 0
+#endif
+#ifndef ECA_MASK_BPS  // tuning knob: resident-CTA cap per SM of the mask grid
+#define ECA_MASK_BPS 16
+#endif
+
 namespace {
 
 ECA_DEV bool inside(double x, double cx, double dy2, double r2) {
@@ -97,7 +104,11 @@ __global__ void __launch_bounds__(256) mask_kernel(const EcaFitRecord* fits, int
       if (lane < h) dst[lane] = (lane >= rlo && lane <= rhi) ? 1 : 0;
       const int n16 = (W - h) >> 4;
       uint4* body = reinterpret_cast<uint4*>(dst + h);
+#if ECA_MASK_CS
+      for (int v = lane; v < n16; v += 32) __stcs(body + v, mask16(h + v * 16, rlo, rhi));
+#else
       for (int v = lane; v < n16; v += 32) body[v] = mask16(h + v * 16, rlo, rhi);
+#endif
       for (int x = h + n16 * 16 + lane; x < W; x += 32) dst[x] = (x >= rlo && x <= rhi) ? 1 : 0;
     }
   }
@@ -193,7 +204,7 @@ extern "C" int eca_draw_mask(const EcaFitRecord* fits, int batch, int height, in
   if (!fits || !out) return ECA_ERR_ARG;
   const int64_t rows = int64_t(batch) * height;
   const int64_t blocks64 = (rows + 255) / 256;   // 8 warps x 32 rows per CTA pass
-  const int blocks = int(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
+  const int blocks = int(blocks64 < 148 * ECA_MASK_BPS ? blocks64 : 148 * ECA_MASK_BPS);
   mask_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(fits, batch, height,
                                                                           width, out,
                                                                           out_frame_stride);
