@@ -1,7 +1,12 @@
 """Time K4 draw_mask (256 x 1080p, accepted circles of varied size) against a
 torch fill of the same buffer (the write-only ceiling).  usage: python tools/time_mask.py"""
+import sys
+from pathlib import Path
+
 import numpy as np
 import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from paper_2210_14771_b200 import _lib, api
 
