@@ -58,7 +58,7 @@ def log(*a):
 
 # ------------------------------------------------------------------ frames ---
 def _render(k: int) -> np.ndarray:
-    from paper_2210_14771_b200 import synth
+    from support import synth
     specs = synth.bench_specs(k + 1, WIDTH, HEIGHT, seed=2024)
     return synth.render(specs[k][1], 30000 + k)
 
@@ -591,7 +591,8 @@ def eval_leg(eb, dev, eng, pool) -> dict:
     eca_area_hausdorff (boundary sampling + FP32-ordered exact FP64 scan)."""
     import ctypes
     import torch
-    from paper_2210_14771_b200 import _lib, api, metrics, synth
+    from paper_2210_14771_b200 import _lib, api, metrics
+    from support import synth
     rec = eng.run(pool[:BATCH]).clone()
     specs = synth.bench_specs(N_BASE, WIDTH, HEIGHT, seed=2024)
     truth = [specs[i % N_BASE][1].circle for i in range(BATCH)]
@@ -803,7 +804,7 @@ def uhd_leg(eb, dev, peaks) -> dict:
     step (4096 half-row items: the GPU's 2368 bound-and-prune warps stay busy),
     through the same streamed path, frames resident in HBM (12.7 GB pool)."""
     import torch
-    from paper_2210_14771_b200 import synth
+    from support import synth
     from paper_2210_14771_b200.engine import ContentAreaEngine
     w, h, b = 3840, 2160, 128
     specs = synth.bench_specs(8, w, h, seed=2024)
@@ -855,7 +856,7 @@ def latency(eb, dev) -> dict:
     """Single-frame (C1) latency: CUDA-graph replay of the one fused launch,
     timed per replay with CUDA events; plus host wall time of estimate()."""
     import torch
-    from paper_2210_14771_b200 import synth
+    from support import synth
     from paper_2210_14771_b200.engine import ContentAreaEngine
     frame = synth.c1_frame()
     t = torch.from_numpy(frame).to(dev).unsqueeze(0)

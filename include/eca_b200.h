@@ -83,10 +83,20 @@ int eca_triplet_table(uint64_t seed, int attempts, int max_n, int16_t* out);
 /* First `count` doubles of numpy.random.default_rng(seed).random() (test hook). */
 int eca_pcg64_doubles(uint64_t seed, int64_t count, double* out);
 
-/* FP32 prefilter tolerance the handcrafted kernels use for `params`; returns
- * 0 and writes the relative bound, or 1 when the config needs the all-FP64
- * path (FP32 range insufficient). */
+/* FP32 prefilter tolerance of the handcrafted kernels for `params`: writes the
+ * relative bound (4x the modelled FP32 error; every FP32 bound in the kernels
+ * is padded outward by exactly this, rounded up to float) and returns 0, or
+ * returns 1 when the config needs the all-FP64 path (FP32 range
+ * insufficient, or a bound >= 1e-2).  No reference counterpart: it guards the
+ * exactness of score_strips (handcrafted.py:148-205) on the GPU. */
 int eca_prefilter_bound(const EcaParams* params, double* out_rel_bound);
+
+/* Test hook: measures the FP32 bound terms against FP64 on the device for one
+ * config.  dev_out (device, 4 doubles, zeroed): [0] max relative error of the
+ * tanh term over every |3g|^2, [1] of the darkness term over every preceding
+ * sum, [2] number of fused-kernel table entries that fail to bound their bin,
+ * [3] the pad the kernels use.  Synchronises `stream`. */
+int eca_prefilter_selftest(const EcaParams* params, double* dev_out, void* stream);
 
 /* -------------------------------------------------------------- device ---- */
 

@@ -33,6 +33,7 @@ SIGNATURES = {
     "eca_triplet_table": [_u64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int16)],
     "eca_pcg64_doubles": [_u64, _i64, ctypes.POINTER(ctypes.c_double)],
     "eca_prefilter_bound": [_PARAMS, ctypes.POINTER(ctypes.c_double)],
+    "eca_prefilter_selftest": [_PARAMS, _p, _p],
     "eca_points_workspace_bytes": [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)],
     "eca_points_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
                                _p, _p, _p, _p, _p],

@@ -80,6 +80,9 @@ int prepare_strip_job(StripJob& J, const uint8_t* frames, int batch, int64_t fra
   // ~5e-14 * 20 / t_g; halves whose best lower bound is under tau are scored
   // exhaustively in FP64.  Risky configs (FP32 range) always are.
   J.tau = risky ? INFINITY : float(1e-11 * 20.0 / params->gradient_threshold);
+  // every FP32 bound is padded by the config's own modelled error bound,
+  // rounded up to float (accepted configs: bound < 1e-2)
+  J.pad = risky ? 1e-2f : std::nextafter(float(bound), INFINITY);
   return ECA_OK;
 }
 
@@ -204,15 +207,15 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share)
 }
 
 // A bounds per pseudo-angle bin (as build_tables in eca_strip.cuh), in double
-// on the host, padded kPadRel outward
-void angle_table(double angle_scale, float2* at) {
+// on the host, padded `pad` outward (StripJob::pad)
+void angle_table(double angle_scale, double pad, float2* at) {
   const double pi = 3.14159265358979323846;
   auto theta_of = [&](double ps) {
     ps = std::fmin(std::fmax(ps, 0.0), 2.0);
     return ps <= 1.0 ? std::atan2(ps, 1.0 - ps) : pi - std::atan2(2.0 - ps, ps - 1.0);
   };
   auto term = [&](double th) { return 2.0 / (1.0 + std::exp(2.0 * angle_scale * th)); };
-  const double lo_f = 1.0 - kPadRel, hi_f = 1.0 + kPadRel;
+  const double lo_f = 1.0 - pad, hi_f = 1.0 + pad;
   for (int k = 0; k < kABins; ++k) {
     const double w = 2.0 / kABins;
     const double th_lo = theta_of(k * w - 1e-5), th_hi = theta_of((k + 1) * w + 1e-5);
@@ -226,12 +229,14 @@ PointsJob points_job(const StripJob& J, void* workspace) {
   PointsJob PJ;
   PJ.J = J;
   PJ.chunked = 0;
-  {   // the table depends only on angle_scale: cached per host thread
+  {   // the table depends only on angle_scale and the pad: cached per host thread
     thread_local double cached_scale = -1.0;
+    thread_local float cached_pad = -1.0f;
     thread_local float2 cached[kABins + 1];
-    if (cached_scale != J.p.angle_scale) {
-      angle_table(J.p.angle_scale, cached);
+    if (cached_scale != J.p.angle_scale || cached_pad != J.pad) {
+      angle_table(J.p.angle_scale, double(J.pad), cached);
       cached_scale = J.p.angle_scale;
+      cached_pad = J.pad;
     }
     std::memcpy(PJ.atab, cached, sizeof(cached));
   }
@@ -652,3 +657,97 @@ extern "C" int eca_debug_warp_times(uint64_t* out, int n) {
   return cudaMemcpyFromSymbol(out, g_warp_times, sizeof(uint64_t) * 3 * n) == cudaSuccess ? 0 : -2;
 }
 #endif
+
+// ------------------------------------------------------- prefilter self-test
+// Test hook (tests/test_gpu_parity.py): measures, on the device, the FP32
+// bound terms of the handcrafted kernels against FP64 for one config.
+//   out[0] max relative error of t_term (bounds kernel) over every q in
+//          [1, (3*1020)^2 * 2] (every integer |3g|^2 a frame can produce)
+//   out[1] max relative error of d_term over every preceding sum 0..765
+//   out[2] number of fused-kernel table entries (tanh / angle / darkness,
+//          build_tables with the config's pad) that fail to bound the FP64
+//          term over their bin
+//   out[3] the pad the kernels use (StripJob::pad)
+namespace {
+constexpr int kSelfQMax = 2 * 3060 * 3060;
+
+__device__ void atomic_max_pos(double* a, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(a), __double_as_longlong(v));
+}
+
+__global__ void selftest_terms(const EcaParams p, const TermK tk, double* out) {
+  double mt = 0.0, md = 0.0;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int q = 1 + tid; q <= kSelfQMax; q += nt) {
+    const double t64 = tanh(sqrt(double(q)) / 3.0 / p.gradient_threshold);
+    mt = fmax(mt, fabs(double(t_term(q, tk)) - t64) / t64);
+  }
+  for (int s = tid; s < 766; s += nt) {
+    const double d64 = 2.0 / (1.0 + exp(2.0 * (double(s) / 3.0) / p.intensity_threshold));
+    if (d64 > 1e-300) md = fmax(md, fabs(double(d_term(s, tk)) - d64) / d64);
+  }
+  for (int d = 16; d; d >>= 1) {
+    mt = fmax(mt, __shfl_xor_sync(kFull, mt, d));
+    md = fmax(md, __shfl_xor_sync(kFull, md, d));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_pos(out, mt);
+    atomic_max_pos(out + 1, md);
+  }
+}
+
+__device__ double theta64(double ps) {
+  const double pi = 3.14159265358979323846;
+  ps = fmin(fmax(ps, 0.0), 2.0);
+  return ps <= 1.0 ? atan2(ps, 1.0 - ps) : pi - atan2(2.0 - ps, ps - 1.0);
+}
+
+__global__ void selftest_tables(const EcaParams p, float pad, double* out) {
+  __shared__ float2 tt[kTBins], at[kABins + 2], dt[kDBins];
+  build_tables(p, pad, tt, at, dt);
+  __syncthreads();
+  const double pi = 3.14159265358979323846, u = ldexp(1.0, -24);
+  auto T = [&](double q) { return tanh(sqrt(q) / 3.0 / p.gradient_threshold); };
+  auto A = [&](double th) { return 2.0 / (1.0 + exp(2.0 * p.angle_scale * th)); };
+  int bad = 0;
+  for (int b = threadIdx.x; b < kTBins; b += blockDim.x) {
+    const int e = b >> 5, m = b & 31;
+    const double q_lo = b == 0 ? 1.0 : ldexp(1.0 + m / 32.0, e) * (1.0 - u);
+    const double q_hi = ldexp(1.0 + (m + 1) / 32.0, e) * (1.0 + u);
+    bad += double(tt[b].x) > T(q_lo) || (tt[b].y < 1.0f && double(tt[b].y) < T(q_hi));
+  }
+  for (int k = threadIdx.x; k < kABins; k += blockDim.x) {
+    const double w = 2.0 / kABins;
+    bad += double(at[k].x) > A(theta64((k + 1) * w + 2e-6)) ||
+           (at[k].y < 1.0f && double(at[k].y) < A(theta64(k * w - 2e-6)));
+  }
+  if (threadIdx.x == 0) bad += double(at[kABins].x) > A(pi);
+  for (int s = threadIdx.x; s < 766; s += blockDim.x) {
+    const double d = 2.0 / (1.0 + exp(2.0 * (double(s) / 3.0) / p.intensity_threshold));
+    bad += double(dt[s].x) > d || (dt[s].y < 1.0f && double(dt[s].y) < d);
+  }
+  if (bad) atomicAdd(out + 2, double(bad));
+}
+}  // namespace
+
+extern "C" int eca_prefilter_selftest(const EcaParams* params, double* dev_out, void* stream) {
+  if (!params || !dev_out) return ECA_ERR_ARG;
+  static const uint8_t dummy[16] = {};
+  const int32_t row = 3;
+  EcaParams q = *params;
+  if (q.width < 8) q.width = 8;
+  if (q.height < 14) q.height = 14;
+  StripJob J;
+  const int rc = prepare_strip_job(J, dummy, 0, 0, 3LL * q.width, &row, nullptr, 1, &q);
+  if (rc) return rc;
+  const PointsJob PJ = points_job(J, nullptr);
+  const TermK tk{PJ.kt, PJ.kd};
+  cudaStream_t st = as_stream(stream);
+  selftest_terms<<<4 * sm_count(), 256, 0, st>>>(q, tk, dev_out);
+  selftest_tables<<<1, 256, 0, st>>>(q, J.pad, dev_out);
+  const double pad = J.pad;
+  if (cudaMemcpyAsync(dev_out + 3, &pad, sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return ECA_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return ECA_ERR_CUDA;
+  return check_launch();
+}

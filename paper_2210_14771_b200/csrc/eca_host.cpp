@@ -143,28 +143,41 @@ extern "C" int eca_strip_rows(int height, int count, double weighting, int32_t* 
   return n;
 }
 
-// Relative error bound of the FP32 prefilter score (eca_points.cu: approx_score)
-// against the exact FP64 score, from the per-factor bounds:
-//   tanh term  : ex2.approx (2^-22.5) amplified by 1/(2u) in (1-e)/(1+e), u >= 1/(3 t_g)
-//   angle term : |dtheta| <= 1.2e-6 rad (poly 3.3e-7 + rounding) times 2*angle_scale
-//   darkness   : FP32 table, 2^-24
-//   products / rcp.approx : 10 * 2^-23
-// The candidate window is 4x the bound.  Returns 1 (use the all-FP64 path)
-// when FP32 range or conditioning cannot carry the config.
+// Relative error bound of the FP32 prefilter bounds against the exact FP64
+// score, per factor (x = the factor's natural-log exponent):
+//   tanh term (bounds kernel: 2^(kt*sqrt.approx(q)) by ex2.approx, then
+//     (1-e)*rcp(1+e); fused kernel: tanhf):  the cancellation in (1-e)
+//     amplifies the ex2 error by 1/x, x >= 2 u_min = 2/(3 t_g):
+//     eps_t = 2 * 2^-22 * (1 + 1/(2 u_min))
+//   darkness term 2/(1+e^x), x = 2(p/3)/t_i <= 2*255/t_i (ex2.approx / expf
+//     error plus the argument's roundings, |dx| <= x * 2^-22):
+//     eps_d = 2^-21 + x_max * 2^-22
+//   angle term (bounds kernel: FP64 host table, fused kernel: FP32 atan2f +
+//     expf at the bin edges), x = 2 * angle_scale * theta <= 2*zero_grad_angle:
+//     eps_a = 2 angle_scale * 1.2e-6 (theta error) + x_max * 3 * 2^-24 + 2^-22 + 2^-24
+//   products, rcp.approx, the pads' own rounding: 10 * 2^-23
+// Each bound is padded by 4x the sum (the pad is applied per factor, so every
+// factor is covered with margin); tests/test_gpu_parity.py measures the real
+// per-term FP32 error against FP64 on the GPU (eca_prefilter_selftest).
+// Returns 1 (always the exhaustive FP64 path) when FP32 range or conditioning
+// cannot carry the config: a factor's exponent >= 80 (e^80 < FLT_MAX, and
+// every factor's minimum stays a normal float) or a bound >= 1e-2.  A
+// PRODUCT of factors may still flush to zero: such a column's true score is
+// < 1e-37, below any LB >= tau, and halves with LB < tau are scored
+// exhaustively, so a flushed bound never drops a possible argmax.
 extern "C" int eca_prefilter_bound(const EcaParams* p, double* out_rel_bound) {
   if (!p || !out_rel_bound) return ECA_ERR_ARG;
   const double tg = p->gradient_threshold, ti = p->intensity_threshold;
   const double u_min = 1.0 / (3.0 * tg);
   const double max_exp_a = 2.0 * p->zero_grad_angle;  // natural-log exponent at 180 deg
   const double max_exp_d = 2.0 * 255.0 / ti;
-  const double t_min = std::tanh(u_min);
-  const double a_min = 2.0 / (1.0 + std::exp(max_exp_a));
-  const double d_min = 2.0 / (1.0 + std::exp(max_exp_d));
   const double eps_t = 2.0 * std::ldexp(1.0, -22) * (1.0 + 1.0 / (2.0 * u_min));
-  const double eps_a = 2.0 * p->angle_scale * 1.2e-6 + std::ldexp(1.0, -22);
-  const double eps = eps_t + eps_a + std::ldexp(1.0, -24) + 10.0 * std::ldexp(1.0, -23);
+  const double eps_d = std::ldexp(1.0, -21) + max_exp_d * std::ldexp(1.0, -22);
+  const double eps_a = 2.0 * p->angle_scale * 1.2e-6 + max_exp_a * 3.0 * std::ldexp(1.0, -24) +
+                       std::ldexp(1.0, -22) + std::ldexp(1.0, -24);
+  const double eps = eps_t + eps_d + eps_a + 10.0 * std::ldexp(1.0, -23);
   *out_rel_bound = 4.0 * eps;
-  const bool ok = max_exp_a < 80.0 && max_exp_d < 80.0 && t_min * a_min * d_min > 1e-30 &&
+  const bool ok = std::isfinite(*out_rel_bound) && max_exp_a < 80.0 && max_exp_d < 80.0 &&
                   *out_rel_bound < 1e-2;
   return ok ? 0 : 1;
 }

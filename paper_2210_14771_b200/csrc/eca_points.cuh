@@ -198,8 +198,11 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
 #endif
 
   const TermK tk{PJ.kt, PJ.kd};
-  const float lo_f = 1.0f - kPadRel, hi_f = 1.0f + kPadRel;
+  const float lo_f = 1.0f - J.pad, hi_f = 1.0f + J.pad;
   const double cxf = PJ.cxf, cyf = PJ.cyf;
+  // configs outside the FP32 envelope (tau = inf: every half is scored in
+  // FP64) never stop the scan on a bound
+  const bool trusted = J.tau < 1.0f;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int gi = lane & 7;   // column within an evaluated lane-chunk
 
@@ -451,7 +454,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
         if (last || (ECA_EARLY_EXIT && dc < kEarlyD)) {
           __syncwarp();
           step_ab(k + 1);
-          if (!last && lb > dc) {
+          if (!last && lb > dc && trusted) {
             nch_eff = k + 1;
             break;
           }

@@ -39,7 +39,9 @@ constexpr int kPx = 8;        // pixels per thread
 constexpr int kTBins = 800;   // tanh-term bins: float(|3g|^2) exponent (25) x 5 mantissa bits
 constexpr int kABins = 128;   // angle-term bins over pseudo-angle [0, 2]
 constexpr int kDBins = 768;   // darkness-term table over preceding sums 0..765
-constexpr float kPadRel = 1e-4f;
+// Relative outward pad of every FP32 bound: not a constant but the modelled
+// error bound of the config (StripJob::pad = eca_prefilter_bound, >= 4x the
+// summed per-factor FP32 error), so every accepted config is covered.
 constexpr int kFpWarps = 2;   // FP64 warps per CTA (item parity)
 
 // named barriers (0 is __syncthreads)
@@ -52,6 +54,7 @@ struct StripJob {
   int64_t frame_stride, row_stride;
   int batch, n_strips, nthreads, rowcap, contiguous;
   float tau;          // halves whose LB < tau are scored fully in FP64
+  float pad;          // relative pad of the FP32 bounds (eca_prefilter_bound)
   int exhaustive;
   EcaParams p;
   int16_t rows[ECA_MAX_STRIPS];  // geometric centre row y of each strip
@@ -230,8 +233,8 @@ ECA_DEV float theta_of(float ps) {
 }
 
 // Bound tables (per CTA, from the config): float2 (lower, upper) per bin.
-ECA_DEV void build_tables(const EcaParams& p, float2* tt, float2* at, float2* dt) {
-  const float lo_f = 1.0f - kPadRel, hi_f = 1.0f + kPadRel;
+ECA_DEV void build_tables(const EcaParams& p, float pad, float2* tt, float2* at, float2* dt) {
+  const float lo_f = 1.0f - pad, hi_f = 1.0f + pad;
   const float c = float(1.0 / (3.0 * p.gradient_threshold));
   for (int b = threadIdx.x; b < kTBins; b += blockDim.x) {
     const int e = b >> 5, m = b & 31;
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(MAXT, MINB) strip_kernel(const __grid_constant
       if (item < n_items) issue_item(J, item, raw + s * SL.stage, &bars[s], pol);
     }
   }
-  build_tables(J.p, ttab, atab, dtab);
+  build_tables(J.p, J.pad, ttab, atab, dtab);
   __syncthreads();
 
   if (tid < npx) {

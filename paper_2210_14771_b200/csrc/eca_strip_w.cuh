@@ -8,9 +8,10 @@
 // half-row is independent.  Each WARP owns a ring of 1-D TMA bulk copies
 // (3 rows x half width + 1 neighbour column) and its mbarriers.
 // The tanh and darkness terms are evaluated with MUFU ex2/rcp/sqrt and padded
-// by kPadRel (their FP32 error is < 1e-5 for every config eca_prefilter_bound
-// accepts); the angle term comes from a small per-CTA table (A over a
-// pseudo-angle).
+// by StripJob::pad (eca_prefilter_bound: >= 4x their modelled FP32 error for
+// the config; tests/test_gpu_parity.py measures the real error of every term
+// against FP64 with eca_prefilter_selftest); the angle term comes from a small
+// per-CTA table (A over a pseudo-angle).
 #pragma once
 
 #include "eca_strip.cuh"

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .shapes import Circle
+from paper_2210_14771_b200.shapes import Circle
 
 CATEGORIES = ("clean", "dark", "bleed", "overlay", "corner")     # dataset.py:359
 
@@ -187,32 +187,38 @@ def c2_frame(k: int, width: int = 1920, height: int = 1080, seed: int = 2024, sp
 
 
 def c4_frames(width: int = 3840, height: int = 2160) -> dict[str, np.ndarray]:
-    """4K edge cases: full circle, rectangle, heavy noise + overlay + glyphs, no content."""
+    """4K edge cases: full circle, rectangle, heavy noise +
+    box overlay + OSD text, no content.  Pinned by tests/golden (c4_* cases)."""
     cx0, cy0 = (width - 1) / 2.0, (height - 1) / 2.0
-    out = {
-        "full_circle": render(SyntheticSpec(width, height, circle=Circle(cx0, cy0, 0.26 * width)), 7),
-        "rectangle": render(SyntheticSpec(width, height, circle=None), 7),
-    }
     noisy = render(SyntheticSpec(width, height, circle=Circle(cx0 + 100, cy0 - 50, 0.38 * width),
                                  border_noise_sigma=12, overlay=BoxOverlay(0, 0, 843, 258, 90)), 7)
-    out["heavy_noise_text"] = _stamp_glyphs(noisy, seed=7)
-    out["all_zeros"] = np.zeros((height, width, 3), dtype=np.uint8)
-    out["uniform_128"] = np.full((height, width, 3), 128, dtype=np.uint8)
-    out["dark_noise"] = np.random.default_rng(3).integers(0, 12, (height, width, 3)).astype(np.uint8)
-    return out
+    return {
+        "full_circle": render(SyntheticSpec(width, height, circle=Circle(cx0, cy0, 0.26 * width)), 7),
+        "rectangle": render(SyntheticSpec(width, height, circle=None), 7),
+        "heavy_noise": noisy,
+        "heavy_noise_text": stamp_osd_text(noisy, seed=7),
+        "all_zeros": np.zeros((height, width, 3), dtype=np.uint8),
+        "uniform_128": np.full((height, width, 3), 128, dtype=np.uint8),
+        "dark_noise": np.random.default_rng(3).integers(0, 12, (height, width, 3)).astype(np.uint8),
+    }
 
 
-def _stamp_glyphs(frame: np.ndarray, seed: int) -> np.ndarray:
-    """Burn deterministic 5x7 block 'text' lines into the frame corners (OSD-like)."""
+def stamp_osd_text(frame: np.ndarray, seed: int) -> np.ndarray:
+    """Burn deterministic on-screen-display "text" into a copy of the frame:
+    four lines of 24 random 5x7 block glyphs (one blank column between
+    glyphs), scaled by max(2, W // 640), two lines at the top left and two at
+    the bottom right, brightness 235 / 215 / 195 / 175.  Integer-only, so the
+    golden generator (tests/golden/make_golden_configs.py) and the tests build
+    identical bytes; the text crosses strip rows on both sides."""
     rng = np.random.default_rng(seed)
     f = frame.copy()
     h, w = f.shape[:2]
     cell = max(2, w // 640)
     for line, (x0, y0) in enumerate([(40, 300), (40, 360), (w - 900, h - 200), (w - 900, h - 140)]):
-        bits = rng.integers(0, 2, size=(7, 5 * 24)).astype(bool)
+        bits = rng.integers(0, 2, size=(7, 6 * 24)).astype(bool)
         bits[:, 5::6] = False                       # inter-glyph gap
         ys, xs = np.nonzero(np.kron(bits, np.ones((cell, cell), dtype=bool)))
         ys, xs = ys + y0, xs + x0
-        ok = (ys < h) & (xs < w)
+        ok = (ys >= 0) & (xs >= 0) & (ys < h) & (xs < w)
         f[ys[ok], xs[ok]] = 235 - 20 * line
     return f

@@ -9,7 +9,7 @@ from pathlib import Path
 
 import numpy as np
 
-from paper_2210_14771_b200 import synth
+from support import synth
 from paper_2210_14771_b200.params import EcaConfig
 from paper_2210_14771_b200.shapes import Circle
 
@@ -55,6 +55,8 @@ def make_frame(rec):
         return f
     if k == "flip":
         return np.ascontiguousarray(make_frame(rec["base"])[:, ::-1, :])
+    if k == "osd":   # tests/golden/make_golden_configs.py
+        return synth.stamp_osd_text(make_frame(rec["base"]), rec["seed"])
     raise ValueError(k)
 
 
@@ -76,6 +78,6 @@ def frame_cases(max_pixels=None):
 def _pixels(rec):
     if rec["kind"] == "spec":
         return rec["spec"]["width"] * rec["spec"]["height"]
-    if rec["kind"] == "flip":
+    if rec["kind"] in ("flip", "osd"):
         return _pixels(rec["base"])
     return rec["w"] * rec["h"]

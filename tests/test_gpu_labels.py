@@ -10,7 +10,8 @@ import logging
 import numpy as np
 import pytest
 
-from paper_2210_14771_b200 import labels, synth
+from paper_2210_14771_b200 import labels
+from support import synth
 
 from ._fixtures import load_json
 

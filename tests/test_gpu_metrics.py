@@ -127,7 +127,7 @@ def test_evaluate_dataset_reference_unit_cases():
 def test_fitted_records_evaluate_against_truth():
     """The evaluation consumes the hot path's records directly (estimate ->
     area_errors), as the paper's accuracy tables do."""
-    from paper_2210_14771_b200 import synth
+    from support import synth
     specs = synth.bench_specs(8, 640, 480, seed=2024)
     frames = np.stack([synth.render(s, 30000 + k) for k, (_, s) in enumerate(specs)])
     areas = eb.estimate_batch(list(frames))

@@ -11,7 +11,7 @@ import torch
 
 import paper_2210_14771_b200 as eb
 from oracle import eca_oracle as orc
-from paper_2210_14771_b200 import synth
+from support import synth
 
 from ._fixtures import case_cfg, frame_cases, load_json, load_npz, make_frame, sha
 

@@ -12,7 +12,7 @@ import torch
 import torch.distributed as dist
 
 import paper_2210_14771_b200 as eb
-from paper_2210_14771_b200 import synth
+from support import synth
 from paper_2210_14771_b200.shard import ShardedEstimator, gather_records
 
 pytestmark = pytest.mark.gpu

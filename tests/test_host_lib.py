@@ -115,3 +115,55 @@ def test_validate_frame_messages():
     with pytest.raises(ValueError, match="too small"):
         api.validate_frame(np.zeros((10, 10, 3), dtype=np.uint8))
     assert api.validate_frame(np.zeros((14, 8, 3), dtype=np.uint8)) == (8, 14)
+
+
+def _model_bound(tg, th, ti):
+    """Independent restatement of eca_prefilter_bound's error model
+    (eca_host.cpp): 4x the summed per-factor FP32 error."""
+    import math
+    asc = 180.0 / (math.pi * th)
+    u = 2.0 ** -22
+    eps_t = 2 * u * (1 + 3 * tg / 2)
+    x_d = 2 * 255 / ti
+    eps_d = 2 * u + x_d * u
+    x_a = 2 * math.pi * asc
+    eps_a = 2 * asc * 1.2e-6 + x_a * 3 * 2.0 ** -24 + u + 2.0 ** -24
+    bound = 4 * (eps_t + eps_d + eps_a + 10 * 2.0 ** -23)
+    ok = x_a < 80 and x_d < 80 and bound < 1e-2
+    return bound, ok
+
+
+@pytest.mark.parametrize("tg", [1.0, 3.0, 20.0, 35.0, 100.0, 200.0, 1000.0, 5000.0])
+@pytest.mark.parametrize("th", [1.0, 5.0, 30.0, 90.0, 180.0])
+@pytest.mark.parametrize("ti", [0.5, 5.0, 7.0, 25.0, 200.0, 1000.0])
+def test_prefilter_bound_sweep(tg, th, ti):
+    """The kernels pad every FP32 bound by exactly this bound (rounded up to
+    float), so 'accepted => the modelled error is inside the pad' holds by
+    construction; here the host's bound and accept/reject decision are
+    checked against an independent restatement of the model, and accepted
+    bounds stay below the 1e-2 limit (the GPU test measures the real FP32
+    error against the same bound: test_gpu_configs.py)."""
+    lib = _lib.load()
+    b = ctypes.c_double()
+    p = EcaConfig(gradient_threshold=tg, angle_threshold_deg=th,
+                  intensity_threshold=ti).device_params(1920, 1080)
+    rc = lib.eca_prefilter_bound(ctypes.byref(p), ctypes.byref(b))
+    want, ok = _model_bound(tg, th, ti)
+    assert b.value == pytest.approx(want, rel=1e-12)
+    assert rc == (0 if ok else 1)
+    if rc == 0:
+        assert b.value < 1e-2
+        assert float(np.nextafter(np.float32(b.value), np.float32(np.inf))) >= b.value
+
+
+def test_prefilter_accepts_the_golden_configs():
+    """Which golden non-default configs take the FP32-pruned path (ti=5 is
+    outside the FP32 envelope and always scores exhaustively in FP64)."""
+    lib = _lib.load()
+    got = {}
+    for c in load_json("configs.json"):
+        p = EcaConfig(**c["cfg"]).device_params(640, 480)
+        b = ctypes.c_double()
+        got[c["name"].split("_")[0]] = lib.eca_prefilter_bound(ctypes.byref(p), ctypes.byref(b))
+    assert got["ti5"] == 1
+    assert all(v == 0 for k, v in got.items() if k != "ti5"), got

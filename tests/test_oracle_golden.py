@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from oracle import eca_oracle as orc
-from paper_2210_14771_b200 import synth
+from support import synth
 from paper_2210_14771_b200.params import EcaConfig
 
 from ._fixtures import case_cfg, frame_cases, load_json, load_npz, make_frame, sha, spec_from_dict
@@ -73,6 +73,27 @@ def test_oracle_large_frames(case):
     assert sha(frame) == case["sha256"]
     st, cx, cy, r, s, n = orc.estimate(frame, EcaConfig(), case["seed"])
     assert [st, cx, cy, r, s, n] == case["fit"]
+
+
+@pytest.mark.parametrize("case", load_json("configs.json"), ids=lambda c: c["name"])
+def test_oracle_config_cases(case):
+    """Non-default configs (t_g 3/100/200, theta 5/90, t_i 5/200, a combo)
+    and the 4K OSD-text frame: the oracle reproduces the reference's
+    candidates, scores, filter and fit bit for bit."""
+    frame = make_frame(case["recipe"])
+    assert sha(frame) == case["sha256"]
+    cfg = case_cfg(case)
+    xs, ys, sc, rows, scores = orc.handcrafted_candidates(frame, cfg)
+    assert rows == case["rows"]
+    assert xs.tolist() == case["cand_x"] and ys.tolist() == case["cand_y"]
+    assert sc.tolist() == case["cand_score"]
+    npz = load_npz("configs_scores.npz")
+    if case["name"] in npz:
+        assert np.array_equal(scores, npz[case["name"]])
+    h, w = frame.shape[:2]
+    keep = orc.keep_mask(xs, ys, sc, w, h, cfg)
+    assert keep.tolist() == case["kept"]
+    assert list(orc.ransac(xs[keep], ys[keep], sc[keep], w, h, cfg, case["seed"])) == case["fit"]
 
 
 def test_triplets_match_reference():

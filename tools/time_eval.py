@@ -7,7 +7,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, '.')
-from paper_2210_14771_b200 import _lib, api, metrics, synth  # noqa: E402
+from paper_2210_14771_b200 import _lib, api, metrics  # noqa: E402
+from support import synth  # noqa: E402
 
 B, W, H = 256, 1920, 1080
 dev = torch.device('cuda', 0)
