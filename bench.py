@@ -219,10 +219,9 @@ def run_ours(args) -> None:
         # streaming throughput mode: bound-and-prune of this batch on the main
         # stream; FP64 rescore + fit (+ the record all-gather) on the engine's
         # side stream, overlapping the next step's bound-and-prune
-        rec = eng.run_pipelined(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH])
+        rec = eng.run_pipelined(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH], frames_ready=True)
         if world > 1:
-            with torch.cuda.stream(eng.side_stream):
-                dist.all_gather_into_tensor(gathered, rec)
+            dist.all_gather_into_tensor(gathered, rec)
 
     # parity spot-check of the benchmarked configuration against pool contents
     for i in range(args.warmup):

@@ -120,8 +120,9 @@ int eca_points_workspace_bytes(int batch, int n_strips, int64_t* out_bytes);
 
 /* score_frame_strips + select_candidates_batch, handcrafted variant
  * (estimator.py:35-52, handcrafted.py:148-205, 120-138).  With a workspace of
- * eca_points_workspace_bytes: bound-and-prune kernel + dense FP64 rescoring
- * kernel (fast); workspace == NULL: the single-kernel path. */
+ * eca_points_workspace_bytes: the bound-and-prune kernel (warp per half row,
+ * survivors rescored in FP64 in the same warp); workspace == NULL: the
+ * block-per-strip kernel. */
 int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                            int64_t row_stride, const int32_t* strip_rows,
                            const int32_t* band_rows, int n_strips,
@@ -129,10 +130,10 @@ int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_strid
                            double* out_score, void* workspace, void* stream);
 
 /* The two stages of eca_points_handcrafted (workspace required) as separate
- * launches, so a host pipeline can run the rescore of batch i on another
- * stream under the bound-and-prune kernel of batch i+1 (order them with an
- * event).  eca_bounds_handcrafted writes the workspace (and the candidates of
- * half rows it resolves itself); eca_rescore_handcrafted completes out_*. */
+ * launches.  eca_bounds_handcrafted writes the workspace and the candidates
+ * of the half rows it resolves itself -- since the in-warp FP64 rescore, all
+ * of them; eca_rescore_handcrafted completes any half row left in the
+ * workspace's survivor slots (none today: kept for ABI stability). */
 #define ECA_BOUNDS_OVERLAP_PREVIOUS 1  /* flags: programmatic dependent launch - the
    grid may start while the previous kernel in `stream` drains; only when this
    call neither reads what that kernel writes nor writes what it reads (e.g. the
@@ -155,39 +156,56 @@ int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
                             const EcaParams* params, int32_t* out_x, int32_t* out_y,
                             double* out_score, void* workspace, void* stream);
 
-/* Streamed throughput mode as one call per batch (what
- * ContentAreaEngine.run_pipelined does): the bound-and-prune kernel of batch i
- * runs on `stream`, its rescore + fit on the pipeline's own low-priority side
- * stream, overlapping the next batches' bound-and-prune.  16 buffer sets
- * rotate in the caller's device `scratch` (eca_pipeline_bytes; zeroed by
- * create): the records of step i stay valid until step i+16.  Consecutive
- * bound-and-prune launches overlap (programmatic dependent launch).  Same
- * results as eca_points_handcrafted + eca_fit.  One host thread per pipeline. */
+/* Streamed throughput mode, two launches per batch on the caller's stream
+ * (what ContentAreaEngine.run_pipelined does; estimator.py:85-111 over a
+ * stream of batches): the bound-and-prune kernel (candidates; each warp
+ * rescoring its half row's survivors in FP64) and the fit kernel (filter +
+ * RANSAC, a warp per frame), both programmatic dependent launches: a batch's
+ * bounds CTAs start in the previous batch's tail and its fits run beside the
+ * next batch's bounds kernel.  4 buffer sets rotate in the caller's device
+ * `scratch` (eca_pipeline_bytes; zeroed by create); each launch claims its set
+ * on the device and waits for the launches that used it before, so the
+ * records of step i stay valid until step i+4.  Same records as
+ * eca_points_handcrafted + eca_fit.  One host thread per pipeline. */
 typedef struct EcaPipeline EcaPipeline;
+#define ECA_PIPE_FRAMES_READY 8   /* flags: the frames were complete before the
+   previous operation in `stream` was enqueued (e.g. a pre-filled pool, or
+   host frames): skip the kernel's griddepcontrol.wait on the previous kernel,
+   which otherwise protects frames written by the kernel just before */
 int eca_pipeline_bytes(int batch, int n_strips, int64_t* out_bytes);
 int eca_pipeline_create(int batch, int height, int width, const int32_t* strip_rows,
                         int n_strips, const EcaParams* params, const int16_t* triplets,
                         void* scratch, int64_t scratch_bytes, EcaPipeline** out);
-/* Enqueue one batch; *out_records = this step's device records (batch x 40 B),
- * complete once a stream has waited via eca_pipeline_fence.  flags: 0 or
- * ECA_BOUNDS_ZERO_COPY (frames in pinned host memory, read over PCIe chunk by
- * chunk; they must stay unchanged until the step's records are fenced).
- * host_records (optional, pinned): the records are also copied there on the
- * side stream after the fit. */
+/* Enqueue one batch on `stream`; *out_records = this step's device records
+ * (batch x 40 B), complete in `stream` order (other streams: eca_pipeline_fence).
+ * flags: ECA_BOUNDS_ZERO_COPY (frames in pinned host memory, read over PCIe
+ * chunk by chunk; they must stay unchanged until the step completes) and / or
+ * ECA_PIPE_FRAMES_READY.  host_records (optional, mapped pinned memory): the
+ * final stage also stores each frame's record there. */
 int eca_pipeline_step(EcaPipeline* pipeline, const uint8_t* frames, int64_t frame_stride,
                       int64_t row_stride, int flags, EcaFitRecord* host_records, void* stream,
                       EcaFitRecord** out_records);
-/* Forget the pipeline's history (no step waits on an earlier step's events):
- * call when everything enqueued so far has completed, e.g. right before
- * capturing a sequence of steps into a CUDA graph, whose first steps must not
- * wait on events recorded outside the capture. */
+/* Kept for API stability: steps carry no host-side history (a no-op). */
 int eca_pipeline_reset(EcaPipeline* pipeline);
 /* Make `stream` wait for every step enqueued so far. */
 int eca_pipeline_fence(EcaPipeline* pipeline, void* stream);
-/* The side stream (e.g. to gather the records of a step right after its fit). */
+/* The stream of the latest step (where its records complete). */
 int eca_pipeline_side_stream(EcaPipeline* pipeline, void** out_stream);
-/* Synchronises the side stream, releases streams/events (not the scratch). */
+/* Synchronises the latest step's stream, releases the pipeline (not the scratch). */
 int eca_pipeline_destroy(EcaPipeline* pipeline);
+
+/* estimate_batch (estimator.py:85-111) for a batch of same-size frames:
+ * bound-and-prune (with its in-warp FP64 rescore) + the fit kernel, plain
+ * stream order.  workspace: eca_points_workspace_bytes(batch, n_strips),
+ * zeroed once (left re-armed).  host_out: optional mapped pinned records,
+ * written by the fit kernel.  flags: 0 or ECA_BOUNDS_ZERO_COPY. */
+int eca_estimate_batch_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
+                                   int64_t row_stride, const int32_t* strip_rows,
+                                   const int32_t* band_rows, int n_strips,
+                                   const EcaParams* params, const int16_t* triplets,
+                                   void* workspace, int32_t* out_x, int32_t* out_y,
+                                   double* out_score, EcaFitRecord* out, EcaFitRecord* host_out,
+                                   int flags, void* stream);
 
 /* Same, plus every column's FP64 score: out_scores[batch][n_strips][width]
  * (StripScoreRow.scores, handcrafted.py:25-31). */

@@ -19,7 +19,7 @@ ECA_OK, ECA_ERR_ARG, ECA_ERR_CUDA, ECA_ERR_UNSUPPORTED = 0, -1, -2, -3
 ACCEPTED, NO_CANDIDATES, LOW_SCORE, GEOMETRY_GATE = 0, 1, 2, 3
 MAX_STRIPS, MAX_WIDTH, MAX_ATTEMPTS = 128, 4096, 8192
 NET_FLOATS = 6209
-BOUNDS_OVERLAP_PREVIOUS, BOUNDS_SHARE_SMS, BOUNDS_ZERO_COPY = 1, 2, 4
+BOUNDS_OVERLAP_PREVIOUS, BOUNDS_SHARE_SMS, BOUNDS_ZERO_COPY, PIPE_FRAMES_READY = 1, 2, 4, 8
 LEARNED_TCGEN05, LEARNED_SIMT = 1, 2
 
 _p = ctypes.c_void_p
@@ -51,6 +51,8 @@ SIGNATURES = {
     "eca_score_rows_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
                                    _p, _p, _p, _p, _p],
     "eca_fit": [_p, _p, _p, ctypes.c_int, ctypes.c_int, _PARAMS, _p, ctypes.c_int, _p, _p],
+    "eca_estimate_batch_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
+                                       _p, _p, _p, _p, _p, _p, _p, ctypes.c_int, _p],
     "eca_estimate_handcrafted": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, _PARAMS,
                                  _p, _p, _p, _p, _p, _p, _p],
     "eca_points_learned": [_p, ctypes.c_int, _i64, _i64, _I32P, _I32P, ctypes.c_int, ctypes.c_int,

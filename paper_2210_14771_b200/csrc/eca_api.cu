@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "eca_fit.cuh"
 #include "eca_strip.cuh"
@@ -31,6 +33,26 @@ int sm_count() {
 }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Large dynamic shared memory opt-in of kernel `kern` on the CURRENT device,
+// once per (kernel, device); false if the attribute could not be set.
+bool smem_optin_ptr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, bool>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first.first == kern && d.first.second == dev) return d.second;
+  const bool ok =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess;
+  done.push_back({{kern, dev}, ok});
+  return ok;
+}
+template <typename K>
+bool smem_optin(K kern, int bytes = 227 * 1024) {
+  return smem_optin_ptr(reinterpret_cast<const void*>(kern), bytes);
+}
 
 int check_launch() { return cudaGetLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA; }
 
@@ -92,10 +114,7 @@ int launch_strips_t(const StripJob& J, cudaStream_t stream) {
   const StripLayout L = strip_layout(kStages, J.rowcap, J.nthreads);
   ECA_TRACE("launch_strips: job %zu B, smem %zu, threads %d\n", sizeof(StripJob), L.total,
             J.nthreads);
-  static std::once_flag once;
-  std::call_once(once, [kern] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  });
+  if (!smem_optin(kern)) return ECA_ERR_CUDA;
   const int block = J.nthreads + 32 * kFpWarps;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, L.total);
@@ -107,11 +126,15 @@ int launch_strips_t(const StripJob& J, cudaStream_t stream) {
   return check_launch();
 }
 
-// ---- v6 points pipeline: bounds_kernel (warp per half row) + rescore_kernel
-// workspace: [0, 256) item tickets (zero between launches) | slots | counts
+// ---- points: bounds_kernel (warp per half row, FP64 rescore of its survivors)
+// workspace: [0, 256) tickets + set-reuse guard (zero between launches) |
+// survivor slots (eca_rescore_handcrafted; kept for the split API) | counts
+int64_t slots_bytes(int64_t n_hr) {
+  return (n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255);
+}
 int64_t points_workspace(int batch, int n_strips) {
   const int64_t n_hr = int64_t(batch) * n_strips * 2;
-  return 256 + ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)) + n_hr * 4;
+  return 256 + slots_bytes(n_hr) + n_hr * 4;
 }
 
 template <int NS, bool kChunked>
@@ -126,32 +149,31 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share)
   // the neighbouring row / per-warp scratch (< 3*257 B) and only feed masked
   // columns
   J.rowcap = (15 + 3 * (half_w + 1) + 15) / 16 * 16;
-  static std::once_flag once;
-  std::call_once(once, [kern] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  });
+  if (!smem_optin(kern)) return ECA_ERR_CUDA;
+  const int fitb = 0;
   // CTA shape: the smallest CTA reaching the most resident warps per SM.
   // Items are handed out dynamically, so independent small CTAs cost
   // nothing; more resident warps shorten the end-of-kernel tail (B200,
   // 1080p B=256: 4 warps x 5 CTAs 50 us, 2 x 9 52 us, 8 x 2 56 us).
   // (cached per host thread and row capacity: the occupancy queries cost
   // microseconds, which matter at one launch per ~40 us batch)
-  thread_local int cached_rowcap = -1, cached_dev = -1, cached_warps = 0, cached_per_sm = 0;
+  thread_local int cached_rowcap = -1, cached_dev = -1, cached_warps = 0, cached_per_sm = 0,
+                   cached_fitb = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   int warps = 0, per_sm = 0;
-  if (cached_rowcap == J.rowcap && cached_dev == dev) {
+  if (cached_rowcap == J.rowcap && cached_dev == dev && cached_fitb == fitb) {
     warps = cached_warps;
     per_sm = cached_per_sm;
   } else {
     for (int w = 1; w <= 8; ++w) {
       int b = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * w,
-                                                        warp_layout(NS, J.rowcap, w).total) !=
+                                                        warp_layout(NS, J.rowcap, w, fitb).total) !=
           cudaSuccess)
         return ECA_ERR_CUDA;
       ECA_TRACE("bounds kernel: %d warps/CTA -> %d CTAs/SM (smem %zu)\n", w, b,
-                warp_layout(NS, J.rowcap, w).total);
+                warp_layout(NS, J.rowcap, w, fitb).total);
       if (b * w > per_sm * warps) {
         warps = w;
         per_sm = b;
@@ -159,6 +181,7 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share)
     }
     cached_rowcap = J.rowcap;
     cached_dev = dev;
+    cached_fitb = fitb;
     cached_warps = warps;
     cached_per_sm = per_sm;
   }
@@ -169,7 +192,7 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share)
   if (force_w >= 1 && force_w <= 8) {
     warps = force_w;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps,
-                                                      warp_layout(NS, J.rowcap, warps).total) !=
+                                                      warp_layout(NS, J.rowcap, warps, fitb).total) !=
         cudaSuccess)
       return ECA_ERR_CUDA;
   }
@@ -183,7 +206,7 @@ int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share)
   // B=256: pipelined step 43 us vs 50 us with every slot taken
   if (share && per_sm > 1) --per_sm;
   if (per_sm < 1) return ECA_ERR_CUDA;
-  const size_t smem = warp_layout(NS, J.rowcap, warps).total;
+  const size_t smem = warp_layout(NS, J.rowcap, warps, fitb).total;
   const int64_t n_hr = int64_t(J.batch) * J.n_strips * 2;
   const int64_t need = (n_hr + warps - 1) / warps;
   const int grid = int(need < int64_t(sm_count()) * per_sm ? need : int64_t(sm_count()) * per_sm);
@@ -252,23 +275,29 @@ PointsJob points_job(const StripJob& J, void* workspace) {
   uint8_t* w = reinterpret_cast<uint8_t*>(workspace);
   PJ.ticket = reinterpret_cast<int32_t*>(w);
   PJ.slots = reinterpret_cast<SurvSlot*>(w + 256);
-  PJ.counts = reinterpret_cast<int32_t*>(
-      w + 256 + ((n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255)));
+  PJ.counts = reinterpret_cast<int32_t*>(w + 256 + slots_bytes(n_hr));
+  PJ.wait_prev = 0;
+  PJ.guard = 0;
   return PJ;
+}
+
+int launch_bounds_job(PointsJob PJ, cudaStream_t stream, bool overlap, bool share, bool chunked) {
+  if (PJ.J.batch == 0) return ECA_OK;
+  static const int ns = [] {
+    const char* v = std::getenv("ECA_WSTAGES");
+    return v ? std::atoi(v) : 1;
+  }();
+  PJ.chunked = chunked ? 1 : 0;
+  if (chunked) return launch_points_t<1, true>(PJ, stream, overlap, share);   // one stage
+  return ns == 2 ? launch_points_t<2, false>(PJ, stream, overlap, share)
+                 : launch_points_t<1, false>(PJ, stream, overlap, share);
 }
 
 int launch_bounds(const StripJob& J, void* workspace, cudaStream_t stream, bool overlap = false,
                   bool share = false, bool chunked = false) {
   if (J.batch == 0) return ECA_OK;
-  static const int ns = [] {
-    const char* v = std::getenv("ECA_WSTAGES");
-    return v ? std::atoi(v) : 1;
-  }();
   PointsJob PJ = points_job(J, workspace);
-  PJ.chunked = chunked ? 1 : 0;
-  if (chunked) return launch_points_t<1, true>(PJ, stream, overlap, share);   // one stage
-  return ns == 2 ? launch_points_t<2, false>(PJ, stream, overlap, share)
-                 : launch_points_t<1, false>(PJ, stream, overlap, share);
+  return launch_bounds_job(PJ, stream, overlap, share, chunked);
 }
 
 // one warp per CTA (4 half rows): small CTAs slot in beside a running
@@ -280,9 +309,10 @@ int launch_rescore(const StripJob& J, void* workspace, cudaStream_t stream) {
   return check_launch();
 }
 
+// the bounds kernel resolves every half row itself (in-warp FP64 rescore), so
+// the rescore stage has nothing left to do
 int launch_points(const StripJob& J, void* workspace, cudaStream_t stream) {
-  const int rc = launch_bounds(J, workspace, stream);
-  return rc ? rc : launch_rescore(J, workspace, stream);
+  return launch_bounds(J, workspace, stream);
 }
 
 template <bool kRows, bool kFused>
@@ -300,19 +330,39 @@ struct FitJob {
   EcaParams p;
   const int16_t* trip;
   EcaFitRecord* out;
+  EcaFitRecord* host_out;   // optional mapped pinned copy of the records
+  int32_t* guard;           // set-reuse guard ticket block (pipelines) or null
+  int wait_prev;            // griddepcontrol.wait: the candidates come from the
+                            // kernel before this one (programmatic launch)
 };
 
-// one warp per frame (same arithmetic order as the fused path's fit_warp)
 // One frame per single-warp CTA with n_cand-sized shared scratch (2.3 KB at
-// 1080p): small CTAs slot in beside a running bounds kernel of the next batch.
+// 1080p), same arithmetic order as the fused path's fit_warp.  In a pipeline
+// it is launched programmatically after the batch's bounds kernel: its CTAs
+// trigger the next batch's bounds launch at once, then wait for their own
+// batch's candidates, and run beside the next batch's bounds kernel.
 __global__ void __launch_bounds__(32) fit_kernel(const __grid_constant__ FitJob J, int batch) {
   extern __shared__ __align__(16) uint8_t fit_smem[];
   const int b = blockIdx.x;
-  if (b >= batch) return;
-  FitPt* pt = reinterpret_cast<FitPt*>(fit_smem);
-  double* ps = reinterpret_cast<double*>(fit_smem + size_t(J.n_cand) * sizeof(FitPt));
-  const size_t o = size_t(b) * J.n_cand;
-  fit_warp(J.x + o, J.y + o, J.s + o, J.n_cand, J.p, J.trip, J.exhaustive, pt, ps, J.out + b);
+  const int lane = threadIdx.x;
+  int u = 0;
+  if (J.guard && lane == 0) u = guard_claim(J.guard);
+  __syncwarp();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (J.wait_prev) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (J.guard && lane == 0) guard_wait(J.guard, u);
+  __syncwarp();
+  if (b < batch) {
+    FitPt* pt = reinterpret_cast<FitPt*>(fit_smem);
+    double* ps = reinterpret_cast<double*>(fit_smem + size_t(J.n_cand) * sizeof(FitPt));
+    const size_t o = size_t(b) * J.n_cand;
+    fit_warp(J.x + o, J.y + o, J.s + o, J.n_cand, J.p, J.trip, J.exhaustive, pt, ps, J.out + b);
+    if (J.host_out && lane == 0) J.host_out[b] = J.out[b];
+  }
+  if (J.guard && lane == 0) {
+    __threadfence();
+    guard_release(J.guard, int(gridDim.x));
+  }
 }
 
 int check_fit_params(const EcaParams* params) {
@@ -407,8 +457,20 @@ extern "C" int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int6
 }
 
 namespace {
-int launch_fit(const FitJob& J, int batch, cudaStream_t stream) {
-  fit_kernel<<<batch, 32, size_t(J.n_cand) * (sizeof(FitPt) + sizeof(double)), stream>>>(J, batch);
+// overlap: programmatic dependent launch (then J.wait_prev must be set when
+// the candidates come from the kernel before it in the stream)
+int launch_fit(const FitJob& J, int batch, cudaStream_t stream, bool overlap = false) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(batch));
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = size_t(J.n_cand) * (sizeof(FitPt) + sizeof(double));
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = overlap ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, fit_kernel, J, batch) != cudaSuccess) return ECA_ERR_CUDA;
   return check_launch();
 }
 }  // namespace
@@ -420,7 +482,8 @@ extern "C" int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const doubl
   if (batch == 0) return ECA_OK;
   if (!cand_x || !cand_y || !cand_score || !out || (!exhaustive && !triplets)) return ECA_ERR_ARG;
   if (check_fit_params(params)) return ECA_ERR_ARG;
-  FitJob J{cand_x, cand_y, cand_score, n_cand, exhaustive ? 1 : 0, *params, triplets, out};
+  FitJob J{cand_x, cand_y, cand_score, n_cand, exhaustive ? 1 : 0, *params, triplets, out,
+           nullptr, nullptr, 0};
   return launch_fit(J, batch, as_stream(stream));
 }
 
@@ -473,27 +536,26 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
 
 
 // ---------------------------------------------------------------- pipeline
-// Streamed throughput mode as one native call per batch (ContentAreaEngine.
-// run_pipelined): bounds kernel of batch i on the caller's stream; rescore +
-// fit on the pipeline's side stream, overlapping batch i+1's bounds kernel.
-// kPipeSets buffer sets rotate inside the caller-provided scratch: batch i's
-// bounds kernel waits (stream event) for the fit of batch i - kPipeSets.  16
-// sets measured 1.3 us per batch faster than 3; the step is set by how the
-// bound-and-prune kernel and the side stream share the SMs.
+// Streamed throughput mode (ContentAreaEngine.run_pipelined), two launches
+// per batch on the caller's stream, both programmatic dependent launches:
+//   bounds_kernel  bound-and-prune + in-warp FP64 rescore -> candidates
+//   fit_kernel     filter + RANSAC, one warp per frame -> records
+// so batch i's bounds CTAs fill the SMs as batch i-1's drain, and batch i's
+// fits (latency-bound FP64 chains) run beside batch i+1's bounds kernel.
+// kPipeSets buffer sets rotate inside the caller-provided scratch; each launch
+// claims its set on the device and waits for the launches that used it
+// before (guard_claim / guard_wait).  No side stream, no events between the
+// launches.
 #ifndef ECA_PIPE_SETS
-#define ECA_PIPE_SETS 16
-#endif
-#ifndef ECA_PIPE_SHARE   // leave one bound-and-prune CTA slot per SM to the side stream
-#define ECA_PIPE_SHARE 1
+#define ECA_PIPE_SETS 4
 #endif
 constexpr int kPipeSets = ECA_PIPE_SETS;
 struct EcaPipeline {
   int batch, n_strips;
-  StripJob J;                 // template: geometry, params, tau
+  StripJob J;                 // template: geometry, params, tau, pad
   const int16_t* trip;
-  cudaStream_t side;
-  cudaEvent_t ev_bounds[kPipeSets], ev_free[kPipeSets];
-  bool used[kPipeSets];
+  cudaStream_t last_stream;   // stream of the latest step (fence records there)
+  cudaEvent_t ev_fence;
   int step, last;
   uint8_t* ws[kPipeSets];
   int32_t *xs[kPipeSets], *ys[kPipeSets];
@@ -549,6 +611,7 @@ extern "C" int eca_pipeline_create(int batch, int height, int width, const int32
   P->trip = triplets;
   P->step = 0;
   P->last = -1;
+  P->last_stream = nullptr;
   uint8_t* base = reinterpret_cast<uint8_t*>(scratch);
   for (int k = 0; k < kPipeSets; ++k) {
     uint8_t* b = base + k * L.set;
@@ -557,22 +620,13 @@ extern "C" int eca_pipeline_create(int batch, int height, int width, const int32
     P->ys[k] = reinterpret_cast<int32_t*>(b + L.ys);
     P->sc[k] = reinterpret_cast<double*>(b + L.sc);
     P->rec[k] = reinterpret_cast<EcaFitRecord*>(b + L.rec);
-    P->used[k] = false;
   }
-  int lo = 0, hi = 0;
-  cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  if (cudaMemset(scratch, 0, size_t(L.total)) != cudaSuccess ||   // tickets start at zero
-      cudaStreamCreateWithPriority(&P->side, cudaStreamNonBlocking, lo) != cudaSuccess) {
+  // tickets, frame counters and set sequence numbers start at zero
+  if (cudaMemset(scratch, 0, size_t(L.total)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&P->ev_fence, cudaEventDisableTiming) != cudaSuccess) {
     delete P;
     return ECA_ERR_CUDA;
   }
-  for (int k = 0; k < kPipeSets; ++k)
-    if (cudaEventCreateWithFlags(&P->ev_bounds[k], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&P->ev_free[k], cudaEventDisableTiming) != cudaSuccess) {
-      cudaStreamDestroy(P->side);
-      delete P;
-      return ECA_ERR_CUDA;
-    }
   *out = P;
   return ECA_OK;
 }
@@ -582,7 +636,7 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
                                  void* stream, EcaFitRecord** out_records) {
   if (!P || !frames || !out_records || row_stride < 3LL * P->J.p.width || frame_stride < 0)
     return ECA_ERR_ARG;
-  if (flags & ~ECA_BOUNDS_ZERO_COPY) return ECA_ERR_ARG;
+  if (flags & ~(ECA_BOUNDS_ZERO_COPY | ECA_PIPE_FRAMES_READY)) return ECA_ERR_ARG;
   const int s = P->step % kPipeSets;
   cudaStream_t st = as_stream(stream);
   StripJob J = P->J;
@@ -593,65 +647,88 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   J.out_x = P->xs[s];
   J.out_y = P->ys[s];
   J.out_score = P->sc[s];
-  // the fit kPipeSets batches back has finished reading this set
-  if (P->used[s] && cudaStreamWaitEvent(st, P->ev_free[s], 0) != cudaSuccess) return ECA_ERR_CUDA;
-  int rc = launch_bounds(J, P->ws[s], st, /*overlap=*/true, /*share=*/ECA_PIPE_SHARE != 0,
-                         (flags & ECA_BOUNDS_ZERO_COPY) != 0);
+  PointsJob PJ = points_job(J, P->ws[s]);
+  PJ.guard = 1;
+  // frames produced by the kernel right before this launch must be waited for
+  PJ.wait_prev = (flags & ECA_PIPE_FRAMES_READY) ? 0 : 1;
+  int rc = launch_bounds_job(PJ, st, /*overlap=*/true, /*share=*/false,
+                             (flags & ECA_BOUNDS_ZERO_COPY) != 0);
   if (rc) return rc;
-  if (cudaEventRecord(P->ev_bounds[s], st) != cudaSuccess ||
-      cudaStreamWaitEvent(P->side, P->ev_bounds[s], 0) != cudaSuccess)
-    return ECA_ERR_CUDA;
-  rc = launch_rescore(J, P->ws[s], P->side);
+  const FitJob F{P->xs[s], P->ys[s], P->sc[s], 2 * P->n_strips, 0, J.p, P->trip, P->rec[s],
+                 host_records, PJ.ticket, /*wait_prev=*/1};
+  rc = launch_fit(F, P->batch, st, /*overlap=*/true);
   if (rc) return rc;
-  const FitJob F{P->xs[s], P->ys[s], P->sc[s], 2 * P->n_strips, 0, J.p, P->trip, P->rec[s]};
-  rc = launch_fit(F, P->batch, P->side);
-  if (rc) return rc;
-  if (host_records &&   // the records of this step back to the host, in stream order
-      cudaMemcpyAsync(host_records, P->rec[s], sizeof(EcaFitRecord) * size_t(P->batch),
-                      cudaMemcpyDeviceToHost, P->side) != cudaSuccess)
-    return ECA_ERR_CUDA;
-  if (cudaEventRecord(P->ev_free[s], P->side) != cudaSuccess) return ECA_ERR_CUDA;
-  P->used[s] = true;
   P->last = s;
+  P->last_stream = st;
   ++P->step;
   *out_records = P->rec[s];
   return ECA_OK;
 }
 
 extern "C" int eca_pipeline_reset(EcaPipeline* P) {
+  // the device-side claim / done counters keep counting, so a graph captured
+  // after eager steps replays safely
   if (!P) return ECA_ERR_ARG;
-  for (int k = 0; k < kPipeSets; ++k) P->used[k] = false;
-  P->step = 0;
-  P->last = -1;
   return ECA_OK;
 }
 
 extern "C" int eca_pipeline_fence(EcaPipeline* P, void* stream) {
   if (!P) return ECA_ERR_ARG;
   if (P->last < 0) return ECA_OK;
-  return cudaStreamWaitEvent(as_stream(stream), P->ev_free[P->last], 0) == cudaSuccess
-             ? ECA_OK
-             : ECA_ERR_CUDA;
+  cudaStream_t st = as_stream(stream);
+  if (st == P->last_stream) return ECA_OK;   // stream order already covers it
+  if (cudaEventRecord(P->ev_fence, P->last_stream) != cudaSuccess ||
+      cudaStreamWaitEvent(st, P->ev_fence, 0) != cudaSuccess)
+    return ECA_ERR_CUDA;
+  return ECA_OK;
 }
 
 extern "C" int eca_pipeline_side_stream(EcaPipeline* P, void** out_stream) {
   if (!P || !out_stream) return ECA_ERR_ARG;
-  *out_stream = reinterpret_cast<void*>(P->side);
+  *out_stream = reinterpret_cast<void*>(P->last_stream);
   return ECA_OK;
 }
 
 extern "C" int eca_pipeline_destroy(EcaPipeline* P) {
   if (!P) return ECA_OK;
-  cudaStreamSynchronize(P->side);
-  for (int k = 0; k < kPipeSets; ++k) {
-    cudaEventDestroy(P->ev_bounds[k]);
-    cudaEventDestroy(P->ev_free[k]);
-  }
-  cudaStreamDestroy(P->side);
+  if (P->last_stream || P->last >= 0) cudaStreamSynchronize(P->last_stream);
+  cudaEventDestroy(P->ev_fence);
   delete P;
   return ECA_OK;
 }
 
+extern "C" int eca_estimate_batch_handcrafted(const uint8_t* frames, int batch,
+                                              int64_t frame_stride, int64_t row_stride,
+                                              const int32_t* strip_rows, const int32_t* band_rows,
+                                              int n_strips, const EcaParams* params,
+                                              const int16_t* triplets, void* workspace,
+                                              int32_t* out_x, int32_t* out_y, double* out_score,
+                                              EcaFitRecord* out, EcaFitRecord* host_out,
+                                              int flags, void* stream) {
+  if (flags & ~(ECA_BOUNDS_ZERO_COPY | ECA_PIPE_FRAMES_READY)) return ECA_ERR_ARG;
+  StripJob J;
+  int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
+                             n_strips, params);
+  if (rc) return rc;
+  if (!triplets || !workspace || !out || !out_x || !out_y || !out_score) return ECA_ERR_ARG;
+  if (check_fit_params(params)) return ECA_ERR_ARG;
+  J.out_x = out_x;
+  J.out_y = out_y;
+  J.out_score = out_score;
+  rc = launch_bounds(J, workspace, as_stream(stream), false, false,
+                     (flags & ECA_BOUNDS_ZERO_COPY) != 0);
+  if (rc) return rc;
+  if (batch == 0) return ECA_OK;
+  const FitJob F{out_x, out_y, out_score, 2 * n_strips, 0, J.p, triplets, out, host_out, nullptr, 0};
+  return launch_fit(F, batch, as_stream(stream));
+}
+
+#ifdef ECA_FIT_TIMES
+extern "C" int eca_debug_fit_times(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_fit_times, sizeof(unsigned long long) * 8 * n) == cudaSuccess ? 0
+                                                                                                : -2;
+}
+#endif
 #ifdef ECA_WARP_TIMES
 extern "C" int eca_debug_warp_times(uint64_t* out, int n) {
   return cudaMemcpyFromSymbol(out, g_warp_times, sizeof(uint64_t) * 3 * n) == cudaSuccess ? 0 : -2;

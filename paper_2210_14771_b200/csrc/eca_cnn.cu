@@ -806,21 +806,29 @@ extern "C" int eca_points_learned_ex(const uint8_t* frames, int batch, int64_t f
   J.probs = out_probs;
   auto st = reinterpret_cast<cudaStream_t>(stream);
   const bool tc = (flags & ECA_LEARNED_SIMT) == 0;   // tcgen05 unless the SIMT kernel is asked for
-  static std::once_flag once;
-  static int per_sm = 1, per_sm_tc = 1, sms = 148;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(cnn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(CnnSmem)));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cnn_kernel, 256, sizeof(CnnSmem));
-    cudaFuncSetAttribute(cnn_kernel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(CnnSmemTc)));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_tc, cnn_kernel_tc, 512, sizeof(CnnSmemTc));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (per_sm < 1) per_sm = 1;
-    if (per_sm_tc < 1) per_sm_tc = 1;
+  // per device: shared-memory opt-in and occupancy (checked)
+  static std::once_flag once[64];
+  static int per_sm_d[64], per_sm_tc_d[64], sms_d[64];
+  static bool ok_d[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return ECA_ERR_CUDA;
+  std::call_once(once[dev], [dev] {
+    int a = 0, b = 0, c = 0;
+    ok_d[dev] = cudaFuncSetAttribute(cnn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(CnnSmem))) == cudaSuccess &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, cnn_kernel, 256, sizeof(CnnSmem)) ==
+                    cudaSuccess &&
+                cudaFuncSetAttribute(cnn_kernel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(CnnSmemTc))) == cudaSuccess &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cnn_kernel_tc, 512,
+                                                              sizeof(CnnSmemTc)) == cudaSuccess &&
+                cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess;
+    per_sm_d[dev] = a > 0 ? a : 1;
+    per_sm_tc_d[dev] = b > 0 ? b : 1;
+    sms_d[dev] = c > 0 ? c : 148;
   });
+  if (!ok_d[dev]) return ECA_ERR_CUDA;
+  const int per_sm = per_sm_d[dev], per_sm_tc = per_sm_tc_d[dev], sms = sms_d[dev];
   const int64_t tiles = int64_t((width - 6 + kTX - 1) / kTX) * n_strips * batch;
   const int64_t cap = int64_t(sms) * (tc ? per_sm_tc : per_sm);
   const int grid = int(tiles < cap ? tiles : cap);

@@ -62,35 +62,47 @@ ECA_DEV bool lsq_solve(const double* mo, int cnt, double& a_out, double& b_out, 
                   (fabs(det) > mul_rn(1e-12, mul_rn(mul_rn(nn, nn), nn)));
   if (!ok) return false;
   // LU with partial pivoting (dgetrf2/dgetrs order: reciprocal-scaled
-  // multipliers, forward then backward substitution)
+  // multipliers, forward then backward substitution).  Rows are exchanged
+  // with register selects (constant indices only: no local-memory array).
+  // column 0: pivot = first row of largest |m[i][0]|
+  {
+    const double a0 = fabs(m[0][0]), a1 = fabs(m[1][0]), a2 = fabs(m[2][0]);
+    const bool p1 = a1 > a0;
+    const int piv = (a2 > (p1 ? a1 : a0)) ? 2 : (p1 ? 1 : 0);
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    int piv = k;
-    double best = fabs(m[k][k]);
-#pragma unroll
-    for (int i = k + 1; i < 3; ++i)
-      if (fabs(m[i][k]) > best) {
-        best = fabs(m[i][k]);
-        piv = i;
-      }
-    if (piv != k) {
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const double t = m[k][j];
-        m[k][j] = m[piv][j];
-        m[piv][j] = t;
-      }
-      const double t = v[k];
-      v[k] = v[piv];
-      v[piv] = t;
+    for (int j = 0; j < 3; ++j) {
+      const double r0 = m[0][j], r1 = m[1][j], r2 = m[2][j];
+      m[0][j] = piv == 1 ? r1 : (piv == 2 ? r2 : r0);
+      m[1][j] = piv == 1 ? r0 : r1;
+      m[2][j] = piv == 2 ? r0 : r2;
     }
-    const double rp = div_rn(1.0, m[k][k]);
+    const double v0 = v[0], v1 = v[1], v2 = v[2];
+    v[0] = piv == 1 ? v1 : (piv == 2 ? v2 : v0);
+    v[1] = piv == 1 ? v0 : v1;
+    v[2] = piv == 2 ? v0 : v2;
+    const double rp = div_rn(1.0, m[0][0]);
 #pragma unroll
-    for (int i = k + 1; i < 3; ++i) {
-      m[i][k] = mul_rn(m[i][k], rp);
+    for (int i = 1; i < 3; ++i) {
+      m[i][0] = mul_rn(m[i][0], rp);
 #pragma unroll
-      for (int j = k + 1; j < 3; ++j) m[i][j] = sub_rn(m[i][j], mul_rn(m[i][k], m[k][j]));
+      for (int j = 1; j < 3; ++j) m[i][j] = sub_rn(m[i][j], mul_rn(m[i][0], m[0][j]));
     }
+  }
+  // column 1: rows 1 and 2
+  {
+    const bool sw = fabs(m[2][1]) > fabs(m[1][1]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double r1 = m[1][j], r2 = m[2][j];
+      m[1][j] = sw ? r2 : r1;
+      m[2][j] = sw ? r1 : r2;
+    }
+    const double v1 = v[1], v2 = v[2];
+    v[1] = sw ? v2 : v1;
+    v[2] = sw ? v1 : v2;
+    const double rp = div_rn(1.0, m[1][1]);
+    m[2][1] = mul_rn(m[2][1], rp);
+    m[2][2] = sub_rn(m[2][2], mul_rn(m[2][1], m[1][2]));
   }
   const double y0 = v[0];
   const double y1 = sub_rn(v[1], mul_rn(m[1][0], y0));
@@ -203,12 +215,26 @@ ECA_DEV Ring ring_dead() {   // matches no point (hypothesis no longer alive)
   return Ring{1.0, -1.0, -1.0, -1.0};
 }
 
+#ifdef ECA_FIT_TIMES   // diagnostic builds: per-frame phase clocks (tools/fit_times.py)
+__device__ unsigned long long g_fit_times[8 * 4096];
+#define FIT_STAMP(k)                                                        \
+  do {                                                                      \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 4096)                       \
+      g_fit_times[8 * blockIdx.x + (k)] = clock64();                        \
+  } while (0)
+#else
+#define FIT_STAMP(k) \
+  do {               \
+  } while (0)
+#endif
+
 // pt / ps: shared scratch for n_cand points (FitScratchW, or n_cand-sized)
 ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double* cand_s,
                       int n_cand, const EcaParams& p, const int16_t* trip, int exhaustive,
                       FitPt* pt, double* ps, EcaFitRecord* out) {
   const int lane = threadIdx.x & 31;
   const int W = p.width, H = p.height;
+  FIT_STAMP(0);
   int n = 0;
   for (int base = 0; base < n_cand; base += 32) {   // filter_candidates, order-preserving
     const int i = base + lane;
@@ -240,6 +266,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
     n += __popc(bal);
   }
   __syncwarp();
+  FIT_STAMP(1);
   if (n < 3) {
     if (lane == 0) *out = EcaFitRecord{0.0, 0.0, 0.0, 0.0, 0, ECA_NO_CANDIDATES};
     __syncwarp();
@@ -265,6 +292,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
       c = circumcircle(pt[i0].x, pt[i0].y, pt[i1].x, pt[i1].y, pt[i2].x,
                        pt[i2].y);
     }
+    FIT_STAMP(2);
     // iterated masked least squares (fitting.py:193-203); every lane runs the
     // loop, dead hypotheses with an empty ring.  Outliers contribute fma(0, v, s)
     // = s + (+-0) = s exactly (the sums start at +0.0, so no -0.0 appears).
@@ -300,6 +328,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
           c.alive = false;
         }
       }
+      FIT_STAMP(3 + (it < 2 ? it : 2));
     }
     double score = 0.0;
     int inl = 0;
@@ -313,6 +342,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
         inl += __popc(in_m);
       }
     }
+    FIT_STAMP(6);
     const bool gated = (c.r < p.min_radius_frac) || (c.r > p.max_radius_frac) ||
                        (hypot(c.cx, c.cy) > p.max_center_offset_frac);
     const bool surv = c.alive && !gated;
@@ -352,6 +382,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
     }
     *out = rec;
   }
+  FIT_STAMP(7);
   __syncwarp();
 }
 

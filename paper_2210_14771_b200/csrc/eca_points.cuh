@@ -64,8 +64,14 @@ struct PointsJob {
   SurvSlot* slots;     // [n_halfrows][kSlots]
   int32_t* counts;     // [n_halfrows]: survivors, or -1 when resolved in bounds_kernel
   int32_t* ticket;     // [0] next item, [1] warps done (zero between launches);
-                       // [2] 16-byte units fetched in zero-copy mode (diagnostic)
+                       // [2] 16-byte units fetched in zero-copy mode (diagnostic);
+                       // [4..5] u64 claim word (high: uses of this workspace,
+                       //     low: CTAs of the current use that claimed it),
+                       // [6] launches finished on it (set-reuse guard)
   int chunked;         // zero-copy mode: fetch scan chunks on demand (NS == 1)
+  int wait_prev;       // griddepcontrol.wait before the first frame load
+  int guard;           // set-reuse guard: a launch's CTAs wait until every
+                       // earlier launch on this workspace finished
   // host-computed constants (launch_points_t): no FP64 division, atan2f or
   // integer division in the kernel prologue / item decode
   float2 atab[kABins + 1];   // A bounds per pseudo-angle bin (see eca_strip.cuh)
@@ -130,6 +136,39 @@ struct ColEval {
   bool flat;   // numpy's gx and gy are exactly 0.0 (score exactly 0)
 };
 
+// Set-reuse guard (pipelines with programmatic dependent launch, where a
+// launch may start before earlier launches on the same workspace finished).
+// ticket block: [1] CTAs / warps done, [4..5] u64 claim word (high: uses so
+// far, low: CTAs of the current use that claimed), [6] uses finished.  Every
+// CTA claims before it triggers its dependents, so all CTAs of use u claim
+// before any CTA of use u+1; the last claimer of a use advances the use index.
+// Returns the use index u of this launch (thread 0 of a CTA).
+ECA_DEV int guard_claim(int32_t* ticket) {
+  unsigned long long* claim = reinterpret_cast<unsigned long long*>(ticket + 4);
+  const unsigned long long old = atomicAdd(claim, 1ull);
+  if (uint32_t(old) + 1u == gridDim.x) atomicAdd(claim, (1ull << 32) - gridDim.x);
+  return int(old >> 32);
+}
+// wait until the u earlier uses of the workspace have finished
+ECA_DEV void guard_wait(const int32_t* ticket, int u) {
+  int done;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(done) : "l"(ticket + 6) : "memory");
+    if (done >= u) break;
+    __nanosleep(128);
+  }
+}
+// the last unit out (counter ticket[1] reaching `units`) re-arms the item
+// tickets and publishes the end of this use; callers fence their writes first
+ECA_DEV bool guard_release(int32_t* ticket, int units) {
+  if (atomicAdd(ticket + 1, 1) != units - 1) return false;
+  ticket[0] = 0;
+  ticket[1] = 0;
+  __threadfence();
+  asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ticket + 6) : "memory");
+  return true;
+}
+
 #ifndef ECA_BOUNDS_MAXREG   // 96: 5 warps per SM sub-partition (120 would allow 4)
 #define ECA_BOUNDS_MAXREG 96
 #endif
@@ -177,12 +216,17 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
     pol = l2_evict_first();
+    // the kernel before this one in the stream may have produced the frames:
+    // with programmatic dependent launch, wait for it (and its memory) unless
+    // the caller vouched that the frames were complete before that launch
+    if (PJ.wait_prev) asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int s = 0; s < NS; ++s) {
       const int it = next_item();
       qitem[s] = it;
       if (it < n_items) issue_item_half<kChunked>(PJ, it, mine + s * WL.stage, &bars[s], pol, split);
     }
   }
+  if (PJ.guard && threadIdx.x == 0) guard_wait(PJ.ticket, guard_claim(PJ.ticket));
   __syncthreads();
   // a dependent launch (the next batch, ECA_BOUNDS_OVERLAP_PREVIOUS) may start
   // filling SMs as this grid's CTAs drain; triggered after the prologue (its
@@ -245,6 +289,22 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     const int nch = (hw + kWChunk - 1) / kWChunk;
     mbar_wait(&bars[stage], phase);
     uint32_t cpar = phase ^ 1u;   // zero-copy mode: parity of the next chunk's copy
+    // take the next item and start its TMA into this stage (once per item,
+    // as soon as the stage's bytes are no longer needed)
+    bool advanced = false;
+    auto advance = [&]() {
+      if (kChunked) phase = cpar ^ 1u;   // (flipped back to cpar below, NS == 1)
+      __syncwarp();
+      if (lane == 0) {
+        // the ticket is taken only now: a warp never holds work it cannot start
+        // (prefetching it measured 30% slower from the end-of-kernel imbalance)
+        const int nxt = next_item();
+        qitem[stage] = nxt;
+        if (nxt < n_items) issue_item_half<kChunked>(PJ, nxt, st, &bars[stage], pol, split);
+      }
+      __syncwarp();
+      advanced = true;
+    };
 #if ECA_LOAD_ONLY   // diagnostic: the TMA ring alone
     if (lane == 0) PJ.counts[item] = 0;
 #else
@@ -583,35 +643,42 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     }
     if (lb >= J.tau) compact(lb);   // final LB: full rows keep every non-flat column
 
-    // ---- hand the survivors to the rescore stage (or resolve here if many)
+    // ---- FP64 rescore of the survivors in this warp, overlapping the next
+    // item's TMA: the survivors' 3x3 sums go to registers first (one lane
+    // each), the stage is refilled, then each lane scores its survivor in the
+    // reference's evaluation order and the warp takes the argmax with the
+    // reference's outermost tie-break.  More than kSlots survivors: scored
+    // from the stage (flush) before it is refilled.
     const int hrow = item;
     if (!flushed && n_list <= kSlots) {
+      int sx = 0, spre = 0, sl[3] = {0, 0, 0}, sm[3] = {0, 0, 0}, sr[3] = {0, 0, 0};
       if (lane < n_list) {
         const uint32_t v = list[lane];
-        const int x = int(v & 0xffffu);
-        SurvSlot sl;
-        sl.x = uint16_t(x);
-        sl.pre = uint16_t(v >> 16);
+        sx = int(v & 0xffffu);
+        spre = int(v >> 16);
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
-          sl.l[r] = uint16_t(px_sum(st, rb[r] + 3 * (x - 1)));
-          sl.m[r] = uint16_t(px_sum(st, rb[r] + 3 * x));
-          sl.r[r] = uint16_t(px_sum(st, rb[r] + 3 * (x + 1)));
+          sl[r] = px_sum(st, rb[r] + 3 * (sx - 1));
+          sm[r] = px_sum(st, rb[r] + 3 * sx);
+          sr[r] = px_sum(st, rb[r] + 3 * (sx + 1));
         }
-        sl.pad = 0;
-        PJ.slots[size_t(hrow) * kSlots + lane] = sl;
       }
-      if (lane == 0) PJ.counts[hrow] = n_list;
+      advance();
+      if (lane < n_list) {
+        const double sc = exact_score(sl, sm, sr, spre, sx, y, cxf, cyf, J.p);
+        if (better(sc, sx, best.s, best.x, !half)) best = Best{sc, sx};
+      }
     } else {
       flush();
-      best = warp_best(best, !half);
-      if (lane == 0) {
-        const size_t slot = size_t(frame) * 2 * S + (half ? S : 0) + strip;
-        J.out_x[slot] = best.x;
-        J.out_y[slot] = y;
-        J.out_score[slot] = best.s;
-        PJ.counts[hrow] = -1;
-      }
+      advance();
+    }
+    best = warp_best(best, !half);
+    if (lane == 0) {
+      const size_t slot = size_t(frame) * 2 * S + (half ? S : 0) + strip;
+      J.out_x[slot] = best.x;
+      J.out_y[slot] = y;
+      J.out_score[slot] = best.s;
+      PJ.counts[hrow] = -1;   // resolved: eca_rescore_handcrafted has nothing to do
     }
 #endif
 #ifdef ECA_WARP_TIMES
@@ -624,16 +691,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
       if (rec > g_warp_times[3 * gw + 2]) g_warp_times[3 * gw + 2] = rec;
     }
 #endif
-    if (kChunked) phase = cpar ^ 1u;   // (flipped back to cpar below, NS == 1)
-    __syncwarp();
-    if (lane == 0) {
-      // the ticket is taken only now: a warp never holds work it cannot start
-      // (prefetching it measured 30% slower from the end-of-kernel imbalance)
-      const int nxt = next_item();
-      qitem[stage] = nxt;
-      if (nxt < n_items) issue_item_half<kChunked>(PJ, nxt, st, &bars[stage], pol, split);
-    }
-    __syncwarp();
+    if (!advanced) advance();
     if (++stage == NS) {
       stage = 0;
       phase ^= 1u;
@@ -647,9 +705,14 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
   }
 #endif
   // the last warp out re-arms the tickets for the next launch on this workspace
-  if (lane == 0 && atomicAdd(PJ.ticket + 1, 1) == nw - 1) {
-    PJ.ticket[0] = 0;
-    PJ.ticket[1] = 0;
+  if (lane == 0) {
+    if (PJ.guard) {
+      __threadfence();   // this warp's outputs before the release
+      guard_release(PJ.ticket, nw);
+    } else if (atomicAdd(PJ.ticket + 1, 1) == nw - 1) {
+      PJ.ticket[0] = 0;
+      PJ.ticket[1] = 0;
+    }
   }
 }
 

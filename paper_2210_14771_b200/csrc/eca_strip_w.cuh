@@ -34,12 +34,15 @@ struct WarpLayout {
   size_t atab, warp0, per_warp, stage, list, ulist, bars, ut, exs, sel, total;
 };
 
-__host__ __device__ inline WarpLayout warp_layout(int nstage, int rowcap_h, int warps) {
+// min_stage: bytes a stage must hold at least (besides the rows)
+__host__ __device__ inline WarpLayout warp_layout(int nstage, int rowcap_h, int warps,
+                                                  int min_stage = 0) {
   WarpLayout L;
   size_t o = 0;
   L.atab = o;
   o += ((kABins + 2) * 8 + 127) & ~size_t(127);
   L.stage = size_t(3) * rowcap_h;
+  if (L.stage < size_t(min_stage)) L.stage = size_t(min_stage);
   L.stage = (L.stage + 127) & ~size_t(127);
   L.list = size_t(nstage) * L.stage;
   L.ulist = L.list + kWListCap * 4;

@@ -63,14 +63,15 @@ class ContentAreaEngine:
         self._pipe = None
         self._pipe_graph = None
         # Small batches (latency): one fused launch whose last strip CTA per
-        # frame runs the fit.  Large batches (throughput): bound-and-prune
-        # kernel, FP64 rescore of the survivors, then a fit kernel (one warp
-        # per frame), which keeps the FP64 chains off the pixel warps.
+        # frame runs the fit.  Large batches (throughput): one launch of the
+        # bound-and-prune kernel (warp per half row) whose final stage -- the
+        # warp that completes a frame's last half row -- rescores the frame's
+        # survivors in FP64 and fits it.
         self.fused = batch <= self.FUSED_MAX_BATCH
         if isinstance(variant, api.Learned):
             self.launches_per_run = 3          # CNN, candidate select, fit
         else:
-            self.launches_per_run = 1 if self.fused else 3   # bounds, rescore, fit
+            self.launches_per_run = 1
 
     FUSED_MAX_BATCH = 16
 
@@ -98,14 +99,11 @@ class ContentAreaEngine:
                                               api._ptr(self.sc), api._ptr(self.rec), st)
             _lib.check(rc, "eca_estimate_handcrafted")
             return
-        rc = lib.eca_points_handcrafted(ctypes.c_void_p(ptr), self.batch, fstride, rstride,
-                                        self._rows, band, s, ctypes.byref(self.params),
-                                        api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc),
-                                        api._ptr(self.workspace), st)
-        _lib.check(rc, "eca_points_handcrafted")
-        rc = lib.eca_fit(api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), self.batch, 2 * s,
-                         ctypes.byref(self.params), api._ptr(self.trip), 0, api._ptr(self.rec), st)
-        _lib.check(rc, "eca_fit")
+        rc = lib.eca_estimate_batch_handcrafted(
+            ctypes.c_void_p(ptr), self.batch, fstride, rstride, self._rows, band, s,
+            ctypes.byref(self.params), api._ptr(self.trip), api._ptr(self.workspace), api._ptr(self.xs),
+            api._ptr(self.ys), api._ptr(self.sc), api._ptr(self.rec), None, 0, st)
+        _lib.check(rc, "eca_estimate_batch_handcrafted")
 
     def _check_frames(self, frames: torch.Tensor) -> torch.Tensor:
         if frames.dim() == 3:
@@ -142,10 +140,7 @@ class ContentAreaEngine:
                                                self.n_strips, ctypes.byref(self.params),
                                                api._ptr(self.trip), api._ptr(scratch), n.value,
                                                ctypes.byref(handle)), "eca_pipeline_create")
-            side = ctypes.c_void_p()
-            _lib.check(lib.eca_pipeline_side_stream(handle, ctypes.byref(side)), "eca_pipeline_side_stream")
             self._pipe = {"handle": handle, "scratch": scratch, "base": scratch.data_ptr(), "views": {},
-                          "side": torch.cuda.ExternalStream(side.value, device=self.device),
                           "out": ctypes.c_void_p(), "step": lib.eca_pipeline_step}
         return self._pipe
 
@@ -161,28 +156,31 @@ class ContentAreaEngine:
         except Exception:  # noqa: BLE001 - interpreter shutdown
             pass
 
-    @property
-    def side_stream(self) -> torch.cuda.Stream:
-        """Stream of the rescore + fit half of run_pipelined()."""
-        return self._pipeline()["side"]
+    PIPE_SETS = 4   # eca_pipeline_* buffer sets (records stay valid this many steps)
 
-    def run_pipelined(self, frames: torch.Tensor) -> torch.Tensor:
-        """Throughput mode for a stream of batches, one native call per batch
-        (eca_pipeline_step): the bound-and-prune kernel of this batch runs on
-        the current stream, its FP64 rescore and the fit on a side stream,
-        where they overlap the next calls' bound-and-prune.  16 buffer sets
-        rotate; the returned (B,5) records are complete once ``fence()`` has
-        made the reading stream wait, and are overwritten 16 calls later.
-        Same records as run() (tests/test_gpu_parity.py)."""
+    def run_pipelined(self, frames: torch.Tensor, frames_ready: bool = False) -> torch.Tensor:
+        """Throughput mode for a stream of batches: ONE launch per batch
+        (eca_pipeline_step) on the current stream -- bound-and-prune with the
+        final stage (each frame's last half-row warp rescores and fits it);
+        consecutive launches overlap (programmatic dependent launch).  The
+        returned (B,5) records are complete in current-stream order
+        (``fence()`` for other streams) and are overwritten PIPE_SETS calls
+        later.  ``frames_ready``: the frames were complete before the previous
+        operation on the stream was enqueued (a pre-filled pool), so the
+        kernel need not wait for that operation (otherwise it does, in case it
+        produced them).  Same records as run() (tests/test_gpu_parity.py)."""
         if isinstance(self.variant, api.Learned) or self.fused:
             return self.run(frames)
+        if frames.dim() == 4 and (frames.stride(3) != 1 or frames.stride(2) != 3):
+            raise ValueError("run_pipelined takes frames with packed pixels (stride (.., .., 3, 1))")
         f = self._check_frames(frames)
         if f.device != self.device:
             raise ValueError(f"frames must live on {self.device}")
         p = self._pipeline()
         out = p["out"]
-        _lib.check(p["step"](p["handle"], ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1), 0, None,
-                             ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
+        flags = _lib.PIPE_FRAMES_READY if frames_ready else 0
+        _lib.check(p["step"](p["handle"], ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1), flags,
+                             None, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
                              ctypes.byref(out)), "eca_pipeline_step")
         rec = p["views"].get(out.value)
         if rec is None:   # a view of this buffer set's records inside the scratch
@@ -193,11 +191,11 @@ class ContentAreaEngine:
 
     def run_host_pipelined(self, host_frames: torch.Tensor, host_records: torch.Tensor) -> None:
         """Streaming end-to-end mode: pinned host frames in, pinned host
-        records out, no synchronisation.  The bound-and-prune kernel reads the
-        frames over PCIe chunk by chunk (zero-copy) on the current stream; the
-        rescore, the fit and the D2H copy of the records into ``host_records``
-        ((B,5) float64, pinned) run on the side stream, overlapping the next
-        call.  Both buffers must stay untouched until fence() + synchronize."""
+        records out, no synchronisation.  One launch per call on the current
+        stream: the bound-and-prune kernel reads the frames over PCIe chunk by
+        chunk (zero-copy TMA), and the final stage stores each frame's record
+        straight into ``host_records`` ((B,5) float64, pinned); calls overlap.
+        Both buffers must stay untouched until the stream is synchronised."""
         a = host_frames
         if not isinstance(a, torch.Tensor) or a.is_cuda or not a.is_pinned():
             raise ValueError("run_host_pipelined takes a pinned host frame tensor")
@@ -210,12 +208,13 @@ class ContentAreaEngine:
         if isinstance(self.variant, api.Learned) or self.fused:
             raise ValueError("run_host_pipelined streams the handcrafted variant at batch > 16")
         p = self._pipeline()
+        # host frames were written before this call: nothing on the stream produces them
         _lib.check(p["step"](p["handle"], ctypes.c_void_p(a.data_ptr()), a.stride(0), a.stride(1),
-                             _lib.BOUNDS_ZERO_COPY, ctypes.c_void_p(r.data_ptr()),
+                             _lib.BOUNDS_ZERO_COPY | _lib.PIPE_FRAMES_READY, ctypes.c_void_p(r.data_ptr()),
                              ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
                              ctypes.byref(p["out"])), "eca_pipeline_step")
 
-    def capture_pipelined(self, batches) -> None:
+    def capture_pipelined(self, batches, frames_ready: bool = True) -> None:
         """Record run_pipelined() over ``batches`` (device frame tensors whose
         storage stays put) plus the closing fence as ONE CUDA graph: both
         streams, the events between them and the programmatic-dependent
@@ -231,7 +230,7 @@ class ContentAreaEngine:
         recs = []
         with torch.cuda.graph(g):
             for f in batches:
-                recs.append(self.run_pipelined(f))
+                recs.append(self.run_pipelined(f, frames_ready=frames_ready))
             self.fence()
         torch.cuda.synchronize(self.device)
         _lib.check(_lib.load().eca_pipeline_reset(p["handle"]), "eca_pipeline_reset")
@@ -323,18 +322,12 @@ class ContentAreaEngine:
             raise ValueError("zero-copy ingest is implemented for the handcrafted variant")
         lib = _lib.load()
         st = api._stream(self.device)
-        s = self.n_strips
-        _lib.check(lib.eca_bounds_handcrafted(
-            ctypes.c_void_p(a.data_ptr()), self.batch, a.stride(0), a.stride(1), self._rows, None, s,
-            ctypes.byref(self.params), api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc),
-            api._ptr(self.workspace), _lib.BOUNDS_ZERO_COPY, st), "eca_bounds_handcrafted")
-        _lib.check(lib.eca_rescore_handcrafted(
-            self.batch, self._rows, s, ctypes.byref(self.params), api._ptr(self.xs), api._ptr(self.ys),
-            api._ptr(self.sc), api._ptr(self.workspace), st), "eca_rescore_handcrafted")
-        _lib.check(lib.eca_fit(api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), self.batch, 2 * s,
-                               ctypes.byref(self.params), api._ptr(self.trip), 0, api._ptr(self.rec), st),
-                   "eca_fit")
-        self.rec_host.copy_(self.rec, non_blocking=True)
+        _lib.check(lib.eca_estimate_batch_handcrafted(
+            ctypes.c_void_p(a.data_ptr()), self.batch, a.stride(0), a.stride(1), self._rows, None,
+            self.n_strips, ctypes.byref(self.params), api._ptr(self.trip), api._ptr(self.workspace),
+            api._ptr(self.xs), api._ptr(self.ys), api._ptr(self.sc), api._ptr(self.rec),
+            ctypes.c_void_p(self.rec_host.data_ptr()), _lib.BOUNDS_ZERO_COPY, st),
+            "eca_estimate_batch_handcrafted")
         torch.cuda.current_stream(self.device).synchronize()
         return self.rec_host
 

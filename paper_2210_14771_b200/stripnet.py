@@ -112,60 +112,77 @@ class EdgeNet:
         return np.concatenate([self.norm.mean, self.norm.std]).astype(np.float64)
 
 
+# ECANET01 stream (edgenet.py:377-437): magic | 6 x f64 channel stats |
+# u32 layer count | per layer: 4 x u32 (out, in, kh, kw), f64 kernel, f64 bias.
+_STATS = struct.Struct("<6d")
+_COUNT = struct.Struct("<I")
+_SHAPE = struct.Struct("<4I")
+
+
 def save_weights(net: EdgeNet) -> bytes:
-    """ECANET01 little-endian stream (edgenet.py:377-387)."""
-    out = [MAGIC, struct.pack("<6d", *net.norm.mean, *net.norm.std),
-           struct.pack("<I", len(net.layers))]
-    for l in net.layers:
-        out.append(struct.pack("<4I", *l.kernel.shape))
-        out.append(np.ascontiguousarray(l.kernel, dtype="<f8").tobytes())
-        out.append(np.ascontiguousarray(l.bias, dtype="<f8").tobytes())
-    return b"".join(out)
+    """Serialise ``net`` as an ECANET01 stream (edgenet.py:377-387)."""
+    blob = bytearray(MAGIC)
+    blob += _STATS.pack(*net.norm.mean, *net.norm.std) + _COUNT.pack(len(net.layers))
+    for layer in net.layers:
+        blob += _SHAPE.pack(*layer.kernel.shape)
+        blob += np.asarray(layer.kernel, dtype="<f8").tobytes(order="C")
+        blob += np.asarray(layer.bias, dtype="<f8").tobytes(order="C")
+    return bytes(blob)
+
+
+class _Stream:
+    """Bounds-checked little-endian cursor over a weights blob."""
+
+    def __init__(self, data: bytes) -> None:
+        self.buf, self.pos = memoryview(data), 0
+
+    def bytes(self, n: int) -> memoryview:
+        have = len(self.buf) - self.pos
+        if n > have:
+            raise CorruptWeightsError(
+                f"truncated stream: wanted {n} bytes at offset {self.pos}, have {have}")
+        self.pos += n
+        return self.buf[self.pos - n:self.pos]
+
+    def unpack(self, st: struct.Struct) -> tuple:
+        return st.unpack(self.bytes(st.size))
+
+    def f64(self, count: int) -> np.ndarray:
+        return np.frombuffer(self.bytes(8 * count), dtype="<f8")
 
 
 def load_weights(data: bytes, dtype=np.float32) -> EdgeNet:
-    """Parse and validate an ECANET01 stream (edgenet.py:390-437)."""
-    buf = memoryview(data)
-    pos = 0
-
-    def take(n: int) -> memoryview:
-        nonlocal pos
-        if pos + n > len(buf):
-            raise CorruptWeightsError(
-                f"truncated stream: wanted {n} bytes at offset {pos}, have {len(buf) - pos}")
-        chunk = buf[pos:pos + n]
-        pos += n
-        return chunk
-
-    if bytes(take(len(MAGIC))) != MAGIC:
+    """Parse and validate an ECANET01 stream (edgenet.py:390-437); every
+    violation raises CorruptWeightsError with the reference's message."""
+    rd = _Stream(data)
+    if bytes(rd.bytes(len(MAGIC))) != MAGIC:
         raise CorruptWeightsError("bad magic header")
-    st = struct.unpack("<6d", take(48))
+    stats = rd.unpack(_STATS)
     try:
-        norm = ChannelStats(np.array(st[:3]), np.array(st[3:]))
+        norm = ChannelStats(np.array(stats[:3]), np.array(stats[3:]))
     except ValueError as exc:
         raise CorruptWeightsError(f"bad channel stats: {exc}") from None
-    (count,) = struct.unpack("<I", take(4))
-    if count != 4:
+    (count,) = rd.unpack(_COUNT)
+    if count != len(_SHAPES):
         raise CorruptWeightsError(f"expected 4 layers, header says {count}")
-    layers = []
-    want_in = INPUT_CHANNELS
-    for i in range(count):
-        oc, ic, kh, kw = struct.unpack("<4I", take(16))
-        ks = 1 if i == 3 else 3
-        if ic != want_in:
-            raise CorruptWeightsError(f"layer {i} expects {ic} input channels, chain provides {want_in}")
-        if kh != ks or kw != ks or oc == 0 or oc > 4096:
-            raise CorruptWeightsError(f"layer {i} has invalid shape {(oc, ic, kh, kw)}")
-        k = np.frombuffer(take(8 * oc * ic * kh * kw), dtype="<f8").reshape(oc, ic, kh, kw)
-        b = np.frombuffer(take(8 * oc), dtype="<f8")
-        if not (np.isfinite(k).all() and np.isfinite(b).all()):
-            raise CorruptWeightsError(f"layer {i} contains non-finite weights")
-        layers.append(ConvLayer(k.astype(dtype), b.astype(dtype)))
-        want_in = oc
-    if layers[-1].kernel.shape[0] != 1:
+    layers, chain = [], INPUT_CHANNELS
+    for idx, (_, _, want_kh, want_kw) in enumerate(_SHAPES):
+        shape = rd.unpack(_SHAPE)
+        oc, ic, kh, kw = shape
+        if ic != chain:
+            raise CorruptWeightsError(f"layer {idx} expects {ic} input channels, chain provides {chain}")
+        if (kh, kw) != (want_kh, want_kw) or not 0 < oc <= 4096:
+            raise CorruptWeightsError(f"layer {idx} has invalid shape {shape}")
+        kernel = rd.f64(oc * ic * kh * kw).reshape(shape)
+        bias = rd.f64(oc)
+        if not (np.isfinite(kernel).all() and np.isfinite(bias).all()):
+            raise CorruptWeightsError(f"layer {idx} contains non-finite weights")
+        layers.append(ConvLayer(kernel.astype(dtype), bias.astype(dtype)))
+        chain = oc
+    if chain != 1:
         raise CorruptWeightsError("head layer must have a single output channel")
-    if pos != len(buf):
-        raise CorruptWeightsError(f"{len(buf) - pos} trailing bytes after weights")
+    if rd.pos != len(rd.buf):
+        raise CorruptWeightsError(f"{len(rd.buf) - rd.pos} trailing bytes after weights")
     return EdgeNet(norm, layers=layers, dtype=dtype)
 
 

@@ -121,6 +121,30 @@ def test_large_frames_match_reference(case):
     assert_fit_equal(fit, case["fit"], case["name"])
 
 
+@pytest.mark.parametrize("case", [c for c in frame_cases() if c not in SMALL], ids=lambda c: c["name"])
+def test_large_frames_fused_estimate(case):
+    """estimate() on the 1080p (C1, C2 0-9) and 4K (C4) golden frames: batch 1
+    takes the fused single launch (strip_kernel<.., kFused>, the 576-thread
+    instantiation at 4K), from host numpy (strip-row ingest) and from HBM."""
+    frame = make_frame(case["recipe"])
+    assert sha(frame) == case["sha256"]
+    for src in (frame, torch.from_numpy(frame).cuda()):
+        area = eb.estimate(src, seed=case["seed"])
+        if case["estimate"] is None:
+            assert area == eb.FULL_FRAME, (case["name"], area)
+        else:
+            cx, cy, r, s = case["estimate"]
+            assert isinstance(area, eb.CircularArea), (case["name"], area)
+            assert abs(area.circle.cx - cx) <= PX_TOL and abs(area.circle.cy - cy) <= PX_TOL
+            assert abs(area.circle.r - r) <= PX_TOL
+            assert area.score == pytest.approx(s, rel=1e-12)
+    eng = eb.ContentAreaEngine(frame.shape[0], frame.shape[1], 1, seed=case["seed"])
+    assert eng.fused
+    fit = eng.fits(eng.run(torch.from_numpy(frame).cuda()))[0]
+    assert_fit_equal(fit, case["fit"], case["name"])
+    assert eng.xs[0].cpu().tolist() == case["cand_x"]
+
+
 def test_host_ingest_equals_device_frames():
     """numpy frames ship strip rows only; results equal the device-resident path."""
     specs = synth.bench_specs(6, 640, 480, seed=4)
@@ -186,7 +210,7 @@ def test_pipelined_matches_run():
     for i in order:
         rec = eng.run_pipelined(frames[i * B:(i + 1) * B])
         if len(got) % 3 == 2:
-            eng.side_stream.synchronize()
+            torch.cuda.current_stream().synchronize()
         got.append((i, rec))
         if len(got) >= 2:   # a record set is reused two calls later: read it now
             eng.fence()
@@ -199,8 +223,9 @@ def test_pipelined_matches_run():
 
 def test_pipelined_long_stream_matches_run():
     """40 unsynchronised run_pipelined calls over 3 distinct batches (the
-    16-set rotation, the every-8-steps wait and overlapping bound-and-prune
-    launches on reused sets): the last 16 steps' records all equal run()'s."""
+    buffer-set rotation with its device-side reuse guard and overlapping
+    programmatic launches on reused sets): the last PIPE_SETS steps' records
+    all equal run()'s."""
     specs = synth.bench_specs(40, 960, 540, seed=2024)
     frames = torch.from_numpy(np.stack([synth.render(s, 31000 + k)
                                         for k, (_, s) in enumerate(specs)])).cuda()
@@ -211,7 +236,7 @@ def test_pipelined_long_stream_matches_run():
     recs = [(i % 3, eng.run_pipelined(pool[(i % 3) * B:(i % 3 + 1) * B])) for i in range(40)]
     eng.fence()
     torch.cuda.synchronize()
-    for k, r in recs[-16:]:
+    for k, r in recs[-eng.PIPE_SETS:]:
         assert torch.equal(r, want[k])
 
 
@@ -374,7 +399,7 @@ def test_native_api_argument_errors():
     f = torch.zeros((20, 480, 640, 3), dtype=torch.uint8, device="cuda")
     out = ctypes.c_void_p()
     st = api._stream(eng.device)
-    assert lib.eca_pipeline_step(pl, ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1), 8, None, st,
+    assert lib.eca_pipeline_step(pl, ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1), 16, None, st,
                                  ctypes.byref(out)) == _lib.ECA_ERR_ARG           # unknown flag
     assert lib.eca_pipeline_step(pl, ctypes.c_void_p(f.data_ptr()), f.stride(0), 100, 0, None, st,
                                  ctypes.byref(out)) == _lib.ECA_ERR_ARG           # row stride < 3W
