@@ -120,9 +120,8 @@ int eca_points_workspace_bytes(int batch, int n_strips, int64_t* out_bytes);
 
 /* score_frame_strips + select_candidates_batch, handcrafted variant
  * (estimator.py:35-52, handcrafted.py:148-205, 120-138).  With a workspace of
- * eca_points_workspace_bytes: the bound-and-prune kernel (warp per half row,
- * survivors rescored in FP64 in the same warp); workspace == NULL: the
- * block-per-strip kernel. */
+ * eca_points_workspace_bytes: bound-and-prune kernel + dense FP64 rescoring
+ * kernel (fast); workspace == NULL: the block-per-strip kernel. */
 int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                            int64_t row_stride, const int32_t* strip_rows,
                            const int32_t* band_rows, int n_strips,
@@ -130,10 +129,9 @@ int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t frame_strid
                            double* out_score, void* workspace, void* stream);
 
 /* The two stages of eca_points_handcrafted (workspace required) as separate
- * launches.  eca_bounds_handcrafted writes the workspace and the candidates
- * of the half rows it resolves itself -- since the in-warp FP64 rescore, all
- * of them; eca_rescore_handcrafted completes any half row left in the
- * workspace's survivor slots (none today: kept for ABI stability). */
+ * launches.  eca_bounds_handcrafted writes the workspace (survivor slots) and
+ * the candidates of the half rows it resolves itself (more than 8
+ * survivors); eca_rescore_handcrafted completes out_*. */
 #define ECA_BOUNDS_OVERLAP_PREVIOUS 1  /* flags: programmatic dependent launch - the
    grid may start while the previous kernel in `stream` drains; only when this
    call neither reads what that kernel writes nor writes what it reads (e.g. the
@@ -158,9 +156,9 @@ int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
 
 /* Streamed throughput mode, two launches per batch on the caller's stream
  * (what ContentAreaEngine.run_pipelined does; estimator.py:85-111 over a
- * stream of batches): the bound-and-prune kernel (candidates; each warp
- * rescoring its half row's survivors in FP64) and the fit kernel (filter +
- * RANSAC, a warp per frame), both programmatic dependent launches: a batch's
+ * stream of batches): the bound-and-prune kernel (survivor columns) and the
+ * fit kernel (a warp per frame: FP64 rescore of the survivors -> candidates,
+ * then filter + RANSAC), both programmatic dependent launches: a batch's
  * bounds CTAs start in the previous batch's tail and its fits run beside the
  * next batch's bounds kernel.  4 buffer sets rotate in the caller's device
  * `scratch` (eca_pipeline_bytes; zeroed by create); each launch claims its set
@@ -195,8 +193,8 @@ int eca_pipeline_side_stream(EcaPipeline* pipeline, void** out_stream);
 int eca_pipeline_destroy(EcaPipeline* pipeline);
 
 /* estimate_batch (estimator.py:85-111) for a batch of same-size frames:
- * bound-and-prune (with its in-warp FP64 rescore) + the fit kernel, plain
- * stream order.  workspace: eca_points_workspace_bytes(batch, n_strips),
+ * bound-and-prune + the fit kernel (FP64 rescore stage, filter, RANSAC),
+ * plain stream order.  workspace: eca_points_workspace_bytes(batch, n_strips),
  * zeroed once (left re-armed).  host_out: optional mapped pinned records,
  * written by the fit kernel.  flags: 0 or ECA_BOUNDS_ZERO_COPY. */
 int eca_estimate_batch_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,

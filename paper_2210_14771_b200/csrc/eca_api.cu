@@ -126,9 +126,10 @@ int launch_strips_t(const StripJob& J, cudaStream_t stream) {
   return check_launch();
 }
 
-// ---- points: bounds_kernel (warp per half row, FP64 rescore of its survivors)
+// ---- points: bounds_kernel (warp per half row) -> survivor slots, FP64
+// rescore in rescore_kernel or in the fit kernel's rescore stage
 // workspace: [0, 256) tickets + set-reuse guard (zero between launches) |
-// survivor slots (eca_rescore_handcrafted; kept for the split API) | counts
+// survivor slots | counts
 int64_t slots_bytes(int64_t n_hr) {
   return (n_hr * kSlots * int64_t(sizeof(SurvSlot)) + 255) & ~int64_t(255);
 }
@@ -278,6 +279,7 @@ PointsJob points_job(const StripJob& J, void* workspace) {
   PJ.counts = reinterpret_cast<int32_t*>(w + 256 + slots_bytes(n_hr));
   PJ.wait_prev = 0;
   PJ.guard = 0;
+  PJ.dbg_seq = 0;
   return PJ;
 }
 
@@ -309,10 +311,9 @@ int launch_rescore(const StripJob& J, void* workspace, cudaStream_t stream) {
   return check_launch();
 }
 
-// the bounds kernel resolves every half row itself (in-warp FP64 rescore), so
-// the rescore stage has nothing left to do
 int launch_points(const StripJob& J, void* workspace, cudaStream_t stream) {
-  return launch_bounds(J, workspace, stream);
+  const int rc = launch_bounds(J, workspace, stream);
+  return rc ? rc : launch_rescore(J, workspace, stream);
 }
 
 template <bool kRows, bool kFused>
@@ -332,15 +333,132 @@ struct FitJob {
   EcaFitRecord* out;
   EcaFitRecord* host_out;   // optional mapped pinned copy of the records
   int32_t* guard;           // set-reuse guard ticket block (pipelines) or null
-  int wait_prev;            // griddepcontrol.wait: the candidates come from the
+  int wait_prev;            // griddepcontrol.wait: the inputs come from the
                             // kernel before this one (programmatic launch)
+  // rescore stage (counts != null): the bound-and-prune kernel's survivor
+  // slots of each frame are scored in FP64 here first (handcrafted.py:148-205
+  // evaluation order), their half-row winners become the candidates x / y / s
+  // (written out too), then the fit runs on them from shared memory
+  int dbg_seq;              // launch number (ECA_TIMELINE diagnostic builds)
+  const int32_t* counts;    // [batch][n_strips][2] survivors, -1 = resolved
+  const SurvSlot* slots;    // [batch][n_strips][2][kSlots]
+  double cxf, cyf;
+  int16_t rows[ECA_MAX_STRIPS];
 };
 
-// One frame per single-warp CTA with n_cand-sized shared scratch (2.3 KB at
-// 1080p), same arithmetic order as the fused path's fit_warp.  In a pipeline
-// it is launched programmatically after the batch's bounds kernel: its CTAs
-// trigger the next batch's bounds launch at once, then wait for their own
-// batch's candidates, and run beside the next batch's bounds kernel.
+// fit_kernel shared memory: the fit's point scratch, then (rescore stage) the
+// candidates and the per-survivor scores
+struct FitSmem {
+  size_t pt, ps, cx, cy, cs, ent, ex, esc, total;
+};
+__host__ __device__ inline FitSmem fit_smem_layout(int n_cand, bool rescore) {
+  FitSmem L;
+  size_t o = 0;
+  L.pt = o;
+  o += size_t(n_cand) * sizeof(FitPt);
+  L.ps = o;
+  o += size_t(n_cand) * 8;
+  L.cs = o;
+  o += rescore ? size_t(n_cand) * 8 : 0;
+  L.esc = o;
+  o += rescore ? size_t(n_cand) * kSlots * 8 : 0;
+  L.cx = o;
+  o += rescore ? size_t(n_cand) * 4 : 0;
+  L.cy = o;
+  o += rescore ? size_t(n_cand) * 4 : 0;
+  L.ent = o;
+  o += rescore ? size_t(n_cand) * kSlots * 2 : 0;
+  L.ex = o;
+  o += rescore ? size_t(n_cand) * kSlots * 2 : 0;
+  L.total = (o + 15) & ~size_t(15);
+  return L;
+}
+
+// Rescore stage of frame b (one warp): compact the frame's survivors (lane =
+// candidate / half row), score them 32 at a time (full lanes), then each
+// half row's winner with the reference's outermost tie-break.
+ECA_DEV void rescore_frame(const FitJob& J, int b, uint8_t* smem) {
+  const int lane = threadIdx.x & 31;
+  const int nc = J.n_cand, S = nc / 2, W = J.p.width;
+  const FitSmem L = fit_smem_layout(nc, true);
+  int32_t* cx = reinterpret_cast<int32_t*>(smem + L.cx);
+  int32_t* cy = reinterpret_cast<int32_t*>(smem + L.cy);
+  double* cs = reinterpret_cast<double*>(smem + L.cs);
+  uint16_t* ent = reinterpret_cast<uint16_t*>(smem + L.ent);
+  uint16_t* ex = reinterpret_cast<uint16_t*>(smem + L.ex);
+  double* esc = reinterpret_cast<double*>(smem + L.esc);
+  auto hrow_of = [&](int hk) {
+    const int half = hk >= S ? 1 : 0;
+    return (b * S + (hk - half * S)) * 2 + half;
+  };
+  int base = 0;
+  for (int h0 = 0; h0 < nc; h0 += 32) {   // compaction: (candidate << 3 | slot)
+    const int hk = h0 + lane;
+    const int cnt = hk < nc ? __ldcg(J.counts + hrow_of(hk)) : -1;
+    const int n = cnt > 0 ? cnt : 0;
+    int incl = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int off = base + incl - n;
+    for (int k = 0; k < n; ++k) ent[off + k] = uint16_t((hk << 3) | k);
+    if (hk < nc) {
+      cx[hk] = off;   // parked until the winners are taken
+      cy[hk] = cnt;
+    }
+    base += __shfl_sync(kFull, incl, 31);
+  }
+  __syncwarp();
+  for (int e = lane; e < base; e += 32) {   // FP64 scores, full lanes
+    const int hk = ent[e] >> 3, k = ent[e] & 7;
+    const int half = hk >= S ? 1 : 0;
+    const SurvSlot* sp = J.slots + size_t(hrow_of(hk)) * kSlots + k;
+    uint2 w[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) w[q] = __ldcg(reinterpret_cast<const uint2*>(sp) + q);
+    SurvSlot sl;
+    memcpy(&sl, w, sizeof(sl));
+    const int l[3] = {sl.l[0], sl.l[1], sl.l[2]}, m[3] = {sl.m[0], sl.m[1], sl.m[2]},
+              r[3] = {sl.r[0], sl.r[1], sl.r[2]};
+    esc[e] = exact_score(l, m, r, sl.pre, sl.x, J.rows[hk - half * S], J.cxf, J.cyf, J.p);
+    ex[e] = sl.x;
+  }
+  __syncwarp();
+  const size_t o = size_t(b) * nc;
+  for (int h0 = 0; h0 < nc; h0 += 32) {   // winners
+    const int hk = h0 + lane;
+    if (hk >= nc) continue;
+    const int half = hk >= S ? 1 : 0;
+    const int off = cx[hk], cnt = cy[hk];
+    Best bb = half ? Best{0.0, W - 1} : Best{0.0, 0};   // border columns score 0
+    if (cnt < 0) {   // resolved by its bounds warp (more than kSlots survivors)
+      bb = Best{__ldcg(J.s + o + hk), __ldcg(J.x + o + hk)};
+    } else {
+      for (int k = 0; k < cnt; ++k)
+        if (better(esc[off + k], int(ex[off + k]), bb.s, bb.x, !half))
+          bb = Best{esc[off + k], int(ex[off + k])};
+    }
+    const int y = J.rows[hk - half * S];
+    cx[hk] = bb.x;
+    cy[hk] = y;
+    cs[hk] = bb.s;
+    if (cnt >= 0) {   // the API's candidate outputs
+      const_cast<int32_t*>(J.x)[o + hk] = bb.x;
+      const_cast<int32_t*>(J.y)[o + hk] = y;
+      const_cast<double*>(J.s)[o + hk] = bb.s;
+    }
+  }
+  __syncwarp();
+}
+
+// One frame per single-warp CTA with n_cand-sized shared scratch (5.4 KB at
+// 1080p with the rescore stage), same arithmetic order as the fused path's
+// fit_warp.  In a pipeline it is launched programmatically after the batch's
+// bounds kernel: its CTAs trigger the next batch's bounds launch at once,
+// then wait for their own batch's survivors, and run beside the next batch's
+// bounds kernel.
 __global__ void __launch_bounds__(32) fit_kernel(const __grid_constant__ FitJob J, int batch) {
   extern __shared__ __align__(16) uint8_t fit_smem[];
   const int b = blockIdx.x;
@@ -349,20 +467,60 @@ __global__ void __launch_bounds__(32) fit_kernel(const __grid_constant__ FitJob 
   if (J.guard && lane == 0) u = guard_claim(J.guard);
   __syncwarp();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (J.wait_prev) asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (J.guard && lane == 0) guard_wait(J.guard, u);
+  // inputs from the kernel just before: a guarded launch waits for exactly
+  // that kernel (its use of the workspace, release / acquire); griddepcontrol
+  // .wait would also wait for everything before it in the stream (the
+  // previous batch's fits, transitively), serialising the fits
+  if (J.guard) {
+    if (lane == 0) guard_wait(J.guard, u);
+  } else if (J.wait_prev) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   __syncwarp();
+  TL_STAMP(1, J.dbg_seq, 0);
   if (b < batch) {
-    FitPt* pt = reinterpret_cast<FitPt*>(fit_smem);
-    double* ps = reinterpret_cast<double*>(fit_smem + size_t(J.n_cand) * sizeof(FitPt));
-    const size_t o = size_t(b) * J.n_cand;
-    fit_warp(J.x + o, J.y + o, J.s + o, J.n_cand, J.p, J.trip, J.exhaustive, pt, ps, J.out + b);
+    const FitSmem L = fit_smem_layout(J.n_cand, J.counts != nullptr);
+    FitPt* pt = reinterpret_cast<FitPt*>(fit_smem + L.pt);
+    double* ps = reinterpret_cast<double*>(fit_smem + L.ps);
+    if (J.counts) {
+      rescore_frame(J, b, fit_smem);
+      fit_warp<false>(reinterpret_cast<const int32_t*>(fit_smem + L.cx),
+                      reinterpret_cast<const int32_t*>(fit_smem + L.cy),
+                      reinterpret_cast<const double*>(fit_smem + L.cs), J.n_cand, J.p, J.trip,
+                      J.exhaustive, pt, ps, J.out + b);
+    } else {
+      const size_t o = size_t(b) * J.n_cand;
+      fit_warp(J.x + o, J.y + o, J.s + o, J.n_cand, J.p, J.trip, J.exhaustive, pt, ps, J.out + b);
+    }
     if (J.host_out && lane == 0) J.host_out[b] = J.out[b];
   }
+  TL_STAMP(1, J.dbg_seq, 1);
   if (J.guard && lane == 0) {
     __threadfence();
     guard_release(J.guard, int(gridDim.x));
   }
+}
+
+// FitJob whose rescore stage reads the survivors of a points workspace
+FitJob rescore_fit_job(const StripJob& J, void* workspace, const int16_t* trip, EcaFitRecord* out,
+                       EcaFitRecord* host_out) {
+  FitJob F;
+  std::memset(&F, 0, sizeof(F));
+  F.x = J.out_x;
+  F.y = J.out_y;
+  F.s = J.out_score;
+  F.n_cand = 2 * J.n_strips;
+  F.p = J.p;
+  F.trip = trip;
+  F.out = out;
+  F.host_out = host_out;
+  const PointsJob PJ = points_job(J, workspace);
+  F.counts = PJ.counts;
+  F.slots = PJ.slots;
+  F.cxf = PJ.cxf;
+  F.cyf = PJ.cyf;
+  for (int k = 0; k < J.n_strips; ++k) F.rows[k] = J.rows[k];
+  return F;
 }
 
 int check_fit_params(const EcaParams* params) {
@@ -463,7 +621,8 @@ int launch_fit(const FitJob& J, int batch, cudaStream_t stream, bool overlap = f
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(batch));
   cfg.blockDim = dim3(32);
-  cfg.dynamicSmemBytes = size_t(J.n_cand) * (sizeof(FitPt) + sizeof(double));
+  cfg.dynamicSmemBytes = fit_smem_layout(J.n_cand, J.counts != nullptr).total;
+  if (cfg.dynamicSmemBytes > 48 * 1024 && !smem_optin(fit_kernel)) return ECA_ERR_CUDA;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -482,8 +641,16 @@ extern "C" int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const doubl
   if (batch == 0) return ECA_OK;
   if (!cand_x || !cand_y || !cand_score || !out || (!exhaustive && !triplets)) return ECA_ERR_ARG;
   if (check_fit_params(params)) return ECA_ERR_ARG;
-  FitJob J{cand_x, cand_y, cand_score, n_cand, exhaustive ? 1 : 0, *params, triplets, out,
-           nullptr, nullptr, 0};
+  FitJob J;
+  std::memset(&J, 0, sizeof(J));
+  J.x = cand_x;
+  J.y = cand_y;
+  J.s = cand_score;
+  J.n_cand = n_cand;
+  J.exhaustive = exhaustive ? 1 : 0;
+  J.p = *params;
+  J.trip = triplets;
+  J.out = out;
   return launch_fit(J, batch, as_stream(stream));
 }
 
@@ -538,8 +705,9 @@ extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_
 // ---------------------------------------------------------------- pipeline
 // Streamed throughput mode (ContentAreaEngine.run_pipelined), two launches
 // per batch on the caller's stream, both programmatic dependent launches:
-//   bounds_kernel  bound-and-prune + in-warp FP64 rescore -> candidates
-//   fit_kernel     filter + RANSAC, one warp per frame -> records
+//   bounds_kernel  bound-and-prune -> survivor slots
+//   fit_kernel     per frame (one warp): FP64 rescore of the survivors with
+//                  full lanes -> candidates, then filter + RANSAC -> records
 // so batch i's bounds CTAs fill the SMs as batch i-1's drain, and batch i's
 // fits (latency-bound FP64 chains) run beside batch i+1's bounds kernel.
 // kPipeSets buffer sets rotate inside the caller-provided scratch; each launch
@@ -649,13 +817,21 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   J.out_score = P->sc[s];
   PointsJob PJ = points_job(J, P->ws[s]);
   PJ.guard = 1;
+  PJ.dbg_seq = P->step;
   // frames produced by the kernel right before this launch must be waited for
   PJ.wait_prev = (flags & ECA_PIPE_FRAMES_READY) ? 0 : 1;
-  int rc = launch_bounds_job(PJ, st, /*overlap=*/true, /*share=*/false,
-                             (flags & ECA_BOUNDS_ZERO_COPY) != 0);
+  // share: one bound-and-prune CTA slot per SM stays free for the previous
+  // batch's fit CTAs, so the next bounds launch is fully resident at once
+  static const bool share = [] {
+    const char* v = std::getenv("ECA_PIPE_SHARE");
+    return v ? std::atoi(v) != 0 : true;
+  }();
+  int rc = launch_bounds_job(PJ, st, /*overlap=*/true, share, (flags & ECA_BOUNDS_ZERO_COPY) != 0);
   if (rc) return rc;
-  const FitJob F{P->xs[s], P->ys[s], P->sc[s], 2 * P->n_strips, 0, J.p, P->trip, P->rec[s],
-                 host_records, PJ.ticket, /*wait_prev=*/1};
+  FitJob F = rescore_fit_job(J, P->ws[s], P->trip, P->rec[s], host_records);
+  F.guard = PJ.ticket;
+  F.dbg_seq = P->step;
+  F.wait_prev = 1;   // its survivors come from the bounds kernel just before
   rc = launch_fit(F, P->batch, st, /*overlap=*/true);
   if (rc) return rc;
   P->last = s;
@@ -719,10 +895,15 @@ extern "C" int eca_estimate_batch_handcrafted(const uint8_t* frames, int batch,
                      (flags & ECA_BOUNDS_ZERO_COPY) != 0);
   if (rc) return rc;
   if (batch == 0) return ECA_OK;
-  const FitJob F{out_x, out_y, out_score, 2 * n_strips, 0, J.p, triplets, out, host_out, nullptr, 0};
-  return launch_fit(F, batch, as_stream(stream));
+  return launch_fit(rescore_fit_job(J, workspace, triplets, out, host_out), batch,
+                    as_stream(stream));
 }
 
+#ifdef ECA_TIMELINE
+extern "C" int eca_debug_timeline(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tl, sizeof(g_tl)) == cudaSuccess ? 0 : -2;
+}
+#endif
 #ifdef ECA_FIT_TIMES
 extern "C" int eca_debug_fit_times(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, g_fit_times, sizeof(unsigned long long) * 8 * n) == cudaSuccess ? 0

@@ -228,7 +228,10 @@ __device__ unsigned long long g_fit_times[8 * 4096];
   } while (0)
 #endif
 
-// pt / ps: shared scratch for n_cand points (FitScratchW, or n_cand-sized)
+// pt / ps: shared scratch for n_cand points (FitScratchW, or n_cand-sized).
+// kCG: the candidates are in global memory, written by other CTAs of the same
+// kernel (L2 loads); otherwise any memory this warp wrote (e.g. shared).
+template <bool kCG = true>
 ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double* cand_s,
                       int n_cand, const EcaParams& p, const int16_t* trip, int exhaustive,
                       FitPt* pt, double* ps, EcaFitRecord* out) {
@@ -242,9 +245,9 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
     int x = 0, y = 0;
     double s = 0.0;
     if (i < n_cand) {
-      x = __ldcg(cand_x + i);
-      y = __ldcg(cand_y + i);
-      s = __ldcg(cand_s + i);
+      x = kCG ? __ldcg(cand_x + i) : cand_x[i];
+      y = kCG ? __ldcg(cand_y + i) : cand_y[i];
+      s = kCG ? __ldcg(cand_s + i) : cand_s[i];
       const int edge = min(min(x, W - 1 - x), min(y, H - 1 - y));
       keep = edge >= p.edge_margin_px && s >= p.min_point_score;
     }

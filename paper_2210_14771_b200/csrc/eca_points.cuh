@@ -55,6 +55,23 @@ struct SurvSlot {
 };
 static_assert(sizeof(SurvSlot) == 24, "slot layout");
 
+#ifdef ECA_TIMELINE   // diagnostic builds: per-CTA start / end (tools/timeline.py)
+__device__ unsigned long long g_tl[2][64][1024][2];   // [bounds|fit][launch][cta][start|end]
+ECA_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_STAMP(kind, seq, which)                                                   \
+  do {                                                                               \
+    if (threadIdx.x == 0 && blockIdx.x < 1024)                                       \
+      g_tl[kind][(seq) & 63][blockIdx.x][which] = gtime();                           \
+  } while (0)
+#else
+#define TL_STAMP(kind, seq, which) \
+  do {                             \
+  } while (0)
+#endif
 #ifdef ECA_WARP_TIMES   // diagnostic builds: per-warp timeline (tools/warp_times.py)
 __device__ uint64_t g_warp_times[3 * 8192];
 #endif
@@ -72,6 +89,7 @@ struct PointsJob {
   int wait_prev;       // griddepcontrol.wait before the first frame load
   int guard;           // set-reuse guard: a launch's CTAs wait until every
                        // earlier launch on this workspace finished
+  int dbg_seq;         // launch number (ECA_TIMELINE diagnostic builds)
   // host-computed constants (launch_points_t): no FP64 division, atan2f or
   // integer division in the kernel prologue / item decode
   float2 atab[kABins + 1];   // A bounds per pseudo-angle bin (see eca_strip.cuh)
@@ -227,6 +245,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     }
   }
   if (PJ.guard && threadIdx.x == 0) guard_wait(PJ.ticket, guard_claim(PJ.ticket));
+  TL_STAMP(0, PJ.dbg_seq, 0);
   __syncthreads();
   // a dependent launch (the next batch, ECA_BOUNDS_OVERLAP_PREVIOUS) may start
   // filling SMs as this grid's CTAs drain; triggered after the prologue (its
@@ -643,42 +662,39 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     }
     if (lb >= J.tau) compact(lb);   // final LB: full rows keep every non-flat column
 
-    // ---- FP64 rescore of the survivors in this warp, overlapping the next
-    // item's TMA: the survivors' 3x3 sums go to registers first (one lane
-    // each), the stage is refilled, then each lane scores its survivor in the
-    // reference's evaluation order and the warp takes the argmax with the
-    // reference's outermost tie-break.  More than kSlots survivors: scored
-    // from the stage (flush) before it is refilled.
+    // ---- hand the survivors to the FP64 rescore (rescore_kernel, or the fit
+    // kernel's rescore stage); resolve the half row here if it has more than
+    // kSlots.  The next item's TMA starts as soon as the stage is read.
     const int hrow = item;
     if (!flushed && n_list <= kSlots) {
-      int sx = 0, spre = 0, sl[3] = {0, 0, 0}, sm[3] = {0, 0, 0}, sr[3] = {0, 0, 0};
       if (lane < n_list) {
         const uint32_t v = list[lane];
-        sx = int(v & 0xffffu);
-        spre = int(v >> 16);
+        const int x = int(v & 0xffffu);
+        SurvSlot sl;
+        sl.x = uint16_t(x);
+        sl.pre = uint16_t(v >> 16);
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
-          sl[r] = px_sum(st, rb[r] + 3 * (sx - 1));
-          sm[r] = px_sum(st, rb[r] + 3 * sx);
-          sr[r] = px_sum(st, rb[r] + 3 * (sx + 1));
+          sl.l[r] = uint16_t(px_sum(st, rb[r] + 3 * (x - 1)));
+          sl.m[r] = uint16_t(px_sum(st, rb[r] + 3 * x));
+          sl.r[r] = uint16_t(px_sum(st, rb[r] + 3 * (x + 1)));
         }
+        sl.pad = 0;
+        PJ.slots[size_t(hrow) * kSlots + lane] = sl;
       }
+      if (lane == 0) PJ.counts[hrow] = n_list;
       advance();
-      if (lane < n_list) {
-        const double sc = exact_score(sl, sm, sr, spre, sx, y, cxf, cyf, J.p);
-        if (better(sc, sx, best.s, best.x, !half)) best = Best{sc, sx};
-      }
     } else {
       flush();
       advance();
-    }
-    best = warp_best(best, !half);
-    if (lane == 0) {
-      const size_t slot = size_t(frame) * 2 * S + (half ? S : 0) + strip;
-      J.out_x[slot] = best.x;
-      J.out_y[slot] = y;
-      J.out_score[slot] = best.s;
-      PJ.counts[hrow] = -1;   // resolved: eca_rescore_handcrafted has nothing to do
+      best = warp_best(best, !half);
+      if (lane == 0) {
+        const size_t slot = size_t(frame) * 2 * S + (half ? S : 0) + strip;
+        J.out_x[slot] = best.x;
+        J.out_y[slot] = y;
+        J.out_score[slot] = best.s;
+        PJ.counts[hrow] = -1;
+      }
     }
 #endif
 #ifdef ECA_WARP_TIMES
@@ -704,6 +720,12 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     g_warp_times[3 * (blockIdx.x * warps + wib) + 1] = t;
   }
 #endif
+  __syncwarp();
+  if (lane == 0) {   // CTA end: the last warp of the CTA to get here stamps
+#ifdef ECA_TIMELINE
+    if (blockIdx.x < 1024) g_tl[0][PJ.dbg_seq & 63][blockIdx.x][1] = gtime();
+#endif
+  }
   // the last warp out re-arms the tickets for the next launch on this workspace
   if (lane == 0) {
     if (PJ.guard) {
