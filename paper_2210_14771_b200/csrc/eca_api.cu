@@ -459,34 +459,36 @@ ECA_DEV void rescore_frame(const FitJob& J, int b, uint8_t* smem) {
 // bounds kernel: its CTAs trigger the next batch's bounds launch at once,
 // then wait for their own batch's survivors, and run beside the next batch's
 // bounds kernel.
-__global__ void __launch_bounds__(32) fit_kernel(const __grid_constant__ FitJob J, int batch) {
+// blockDim.x = 32 * frames per CTA; warp w of CTA c fits frame c * warps + w
+__global__ void __launch_bounds__(256) fit_kernel(const __grid_constant__ FitJob J, int batch) {
   extern __shared__ __align__(16) uint8_t fit_smem[];
-  const int b = blockIdx.x;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int b = blockIdx.x * (blockDim.x >> 5) + wib;
+  const FitSmem L = fit_smem_layout(J.n_cand, J.counts != nullptr);
+  uint8_t* mine = fit_smem + size_t(wib) * L.total;
   int u = 0;
-  if (J.guard && lane == 0) u = guard_claim(J.guard);
-  __syncwarp();
+  if (J.guard && threadIdx.x == 0) u = guard_claim(J.guard);
+  __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // inputs from the kernel just before: a guarded launch waits for exactly
   // that kernel (its use of the workspace, release / acquire); griddepcontrol
   // .wait would also wait for everything before it in the stream (the
   // previous batch's fits, transitively), serialising the fits
   if (J.guard) {
-    if (lane == 0) guard_wait(J.guard, u);
+    if (threadIdx.x == 0) guard_wait(J.guard, u);
+    __syncthreads();
   } else if (J.wait_prev) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
-  __syncwarp();
   TL_STAMP(1, J.dbg_seq, 0);
   if (b < batch) {
-    const FitSmem L = fit_smem_layout(J.n_cand, J.counts != nullptr);
-    FitPt* pt = reinterpret_cast<FitPt*>(fit_smem + L.pt);
-    double* ps = reinterpret_cast<double*>(fit_smem + L.ps);
+    FitPt* pt = reinterpret_cast<FitPt*>(mine + L.pt);
+    double* ps = reinterpret_cast<double*>(mine + L.ps);
     if (J.counts) {
-      rescore_frame(J, b, fit_smem);
-      fit_warp<false>(reinterpret_cast<const int32_t*>(fit_smem + L.cx),
-                      reinterpret_cast<const int32_t*>(fit_smem + L.cy),
-                      reinterpret_cast<const double*>(fit_smem + L.cs), J.n_cand, J.p, J.trip,
+      rescore_frame(J, b, mine);
+      fit_warp<false>(reinterpret_cast<const int32_t*>(mine + L.cx),
+                      reinterpret_cast<const int32_t*>(mine + L.cy),
+                      reinterpret_cast<const double*>(mine + L.cs), J.n_cand, J.p, J.trip,
                       J.exhaustive, pt, ps, J.out + b);
     } else {
       const size_t o = size_t(b) * J.n_cand;
@@ -495,9 +497,12 @@ __global__ void __launch_bounds__(32) fit_kernel(const __grid_constant__ FitJob 
     if (J.host_out && lane == 0) J.host_out[b] = J.out[b];
   }
   TL_STAMP(1, J.dbg_seq, 1);
-  if (J.guard && lane == 0) {
-    __threadfence();
-    guard_release(J.guard, int(gridDim.x));
+  if (J.guard) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      guard_release(J.guard, int(gridDim.x));
+    }
   }
 }
 
@@ -618,10 +623,21 @@ namespace {
 // overlap: programmatic dependent launch (then J.wait_prev must be set when
 // the candidates come from the kernel before it in the stream)
 int launch_fit(const FitJob& J, int batch, cudaStream_t stream, bool overlap = false) {
+  // frames (warps) per CTA: few, wide CTAs find room in a draining bounds
+  // kernel sooner than many small ones (the next programmatic launch waits
+  // until every CTA of this one is resident)
+  static const int fpb_env = [] {
+    const char* v = std::getenv("ECA_FIT_FPB");
+    return v ? std::atoi(v) : 0;
+  }();
+  const size_t per = fit_smem_layout(J.n_cand, J.counts != nullptr).total;
+  int fpb = fpb_env > 0 ? fpb_env : (overlap ? 8 : 1);
+  if (fpb > 8) fpb = 8;
+  while (fpb > 1 && per * fpb > 96 * 1024) fpb /= 2;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(batch));
-  cfg.blockDim = dim3(32);
-  cfg.dynamicSmemBytes = fit_smem_layout(J.n_cand, J.counts != nullptr).total;
+  cfg.gridDim = dim3(unsigned((batch + fpb - 1) / fpb));
+  cfg.blockDim = dim3(unsigned(32 * fpb));
+  cfg.dynamicSmemBytes = per * fpb;
   if (cfg.dynamicSmemBytes > 48 * 1024 && !smem_optin(fit_kernel)) return ECA_ERR_CUDA;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

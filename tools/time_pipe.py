@@ -27,12 +27,14 @@ st = torch.cuda.current_stream()
 def timed(fn, steps, warm=5):
     for i in range(warm):
         fn(i)
+    eng.fence()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     a.record(st)
     for i in range(steps):
         fn(warm + i)
+    eng.fence()
     b.record(st)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / steps * 1e3, (time.perf_counter() - w0) / steps * 1e6
@@ -45,11 +47,14 @@ def sl(i):
 want = [eng.run(sl(i)).clone() for i in range(n_slots)]
 for ready in (True, False):
     recs = [(i, eng.run_pipelined(sl(i), frames_ready=ready)) for i in range(4)]
+    eng.fence()
     torch.cuda.synchronize()
     assert all(torch.equal(r, want[i % n_slots]) for i, r in recs), "pipelined != run"
     for steps in (20, 200):
-        us, host = timed(lambda i: eng.run_pipelined(sl(i), frames_ready=ready), steps)
-        print(f"pipelined ready={ready} steps={steps}: {us:.1f} us/step (host {host:.1f} us)")
+        r = [timed(lambda i: eng.run_pipelined(sl(i), frames_ready=ready), steps) for _ in range(3)]
+        us = sorted(x[0] for x in r)
+        host = sorted(x[1] for x in r)[1]
+        print(f"pipelined ready={ready} steps={steps}: {us[1]:.1f} us/step (min {us[0]:.1f} max {us[2]:.1f}; host {host:.1f} us)")
 us, _ = timed(lambda i: eng.run(sl(i)), 100)
 print(f"run() single launch, no overlap: {us:.1f} us")
 us, _ = timed(lambda i: eng.bounds(sl(i), overlap=True, slot=i % 4), 100)
