@@ -14,9 +14,13 @@ without a CUDA device these functions raise — there is no CPU fallback.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import dataclasses
+import functools
+import inspect
 import math
+import threading
 from dataclasses import dataclass
 from enum import Enum
 from functools import lru_cache
@@ -34,6 +38,7 @@ HALF_WINDOW = 3
 MIN_FRAME_WIDTH = 8
 MIN_FRAME_HEIGHT = 2 * WINDOW_ROWS
 MIN_CROP_SIDE = 14
+MAX_FRAME_HEIGHT = 32767
 
 
 # ----------------------------------------------------------------- types ---
@@ -113,6 +118,26 @@ def _stream(device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+def _on(device) -> contextlib.AbstractContextManager:
+    """Make ``device`` current for the native calls (they launch on the
+    current device; torch tensors and streams may belong to another one)."""
+    return torch.cuda.device(device)
+
+
+def _with_device(fn):
+    """Run ``fn`` with its ``device`` argument (default: the current device)
+    made current.  Without a GPU ``fn`` runs as is (and raises where it needs one)."""
+    sig = inspect.signature(fn)
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        if not torch.cuda.is_available():
+            return fn(*args, **kwargs)
+        with _on(_device(sig.bind(*args, **kwargs).arguments.get("device"))):
+            return fn(*args, **kwargs)
+    return wrapper
+
+
 def _ptr(t: torch.Tensor) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr())
 
@@ -138,7 +163,21 @@ def validate_frame(frame) -> tuple[int, int]:
     if width < MIN_FRAME_WIDTH or height < MIN_FRAME_HEIGHT:
         raise ValueError(f"frame {width}x{height} too small: need width >= {MIN_FRAME_WIDTH} "
                          f"and height >= {MIN_FRAME_HEIGHT}")
+    if width > _lib.MAX_WIDTH or height > MAX_FRAME_HEIGHT:
+        # outside the kernels' envelope (the reference has no cap): a per-frame
+        # ValueError, so estimate_batch reports a FrameError for this index
+        raise ValueError(f"frame {width}x{height} too large: the GPU kernels take width <= "
+                         f"{_lib.MAX_WIDTH} and height <= {MAX_FRAME_HEIGHT}")
     return width, height
+
+
+def _check_config(cfg: EcaConfig) -> None:
+    """The native limits on EcaConfig (include/eca_b200.h) as ValueError."""
+    if cfg.strip_count > _lib.MAX_STRIPS:
+        raise ValueError(f"strip_count {cfg.strip_count} exceeds the GPU limit {_lib.MAX_STRIPS}")
+    if cfg.ransac_attempts > _lib.MAX_ATTEMPTS:
+        raise ValueError(f"ransac_attempts {cfg.ransac_attempts} exceeds the GPU limit "
+                         f"{_lib.MAX_ATTEMPTS}")
 
 
 @lru_cache(maxsize=256)
@@ -201,7 +240,8 @@ def _host_bands(items, rows, half: int, device) -> _DevFrames:
         a = it.numpy() if isinstance(it, torch.Tensor) else it
         if a.ndim == 3:
             a = a[None]
-        if a.strides[-1] != 1 or a.strides[-2] != 3:
+        # packed pixels, and non-negative row / frame strides (e.g. frame[::-1])
+        if a.strides[-1] != 1 or a.strides[-2] != 3 or a.strides[1] < 3 * a.shape[2] or a.strides[0] < 0:
             a = np.ascontiguousarray(a)
         views.append(a)
         total += a.shape[0]
@@ -251,16 +291,22 @@ def _dev_triplets(seed: int, attempts: int, max_n: int, device) -> torch.Tensor:
 _WORKSPACES: dict = {}
 
 
+def _stream_key(device) -> tuple:
+    return (str(device), torch.cuda.current_stream(device).cuda_stream)
+
+
 def points_workspace(batch: int, n_strips: int, device) -> torch.Tensor:
     """Device scratch for eca_points_handcrafted (tickets + survivor slots),
-    zero-initialised once (the kernels leave the tickets zeroed), cached per device."""
+    zero-initialised once (the kernels leave the tickets zeroed), cached per
+    (device, current stream): calls on different streams never share one."""
     n = ctypes.c_int64()
     _lib.check(_lib.load().eca_points_workspace_bytes(batch, n_strips, ctypes.byref(n)),
                "eca_points_workspace_bytes")
-    t = _WORKSPACES.get(str(device))
+    key = _stream_key(device)
+    t = _WORKSPACES.get(key)
     if t is None or t.numel() < n.value:
         t = torch.zeros(max(n.value, 1 << 20), dtype=torch.uint8, device=device)
-        _WORKSPACES[str(device)] = t
+        _WORKSPACES[key] = t
     return t
 
 
@@ -268,10 +314,13 @@ _COUNTERS: dict = {}
 
 
 def _dev_counters(n: int, device) -> torch.Tensor:
-    t = _COUNTERS.get(str(device))
+    """Per-frame completion counters of the fused launch (left zeroed), cached
+    per (device, current stream)."""
+    key = _stream_key(device)
+    t = _COUNTERS.get(key)
     if t is None or t.numel() < n:
         t = torch.zeros(max(n, 1024), dtype=torch.int32, device=device)
-        _COUNTERS[str(device)] = t
+        _COUNTERS[key] = t
     return t
 
 
@@ -393,6 +442,7 @@ def _candidates(xs_row, ys_row, sc_row, s) -> list[EdgeCandidate]:
 
 
 # ------------------------------------------------------------ public API ---
+@_with_device
 def score_frame_strips(frame, variant: EstimatorVariant = HANDCRAFTED, cfg: EcaConfig | None = None,
                        device=None):
     """Scored strip rows for one frame (estimator.py:35-52): (rows, (W, H))."""
@@ -428,6 +478,7 @@ def get_points(frame, variant: EstimatorVariant = HANDCRAFTED, cfg: EcaConfig | 
     return get_points_batch([frame], variant, cfg, device)[0]
 
 
+@_with_device
 def get_points_batch(frames, variant: EstimatorVariant = HANDCRAFTED, cfg: EcaConfig | None = None,
                      device=None) -> list[list[EdgeCandidate]]:
     cfg = cfg or config_default()
@@ -463,6 +514,7 @@ def filter_candidates(candidates: list[EdgeCandidate], frame_size: tuple[int, in
             if min(c.x, width - 1 - c.x, c.y, height - 1 - c.y) >= m and c.score >= cfg.min_point_score]
 
 
+@_with_device
 def ransac_fit(candidates: list[EdgeCandidate], frame_size: tuple[int, int], cfg: EcaConfig,
                seed: int = 0, *, exhaustive: bool = False,
                center: tuple[float, float] | None = None, device=None) -> FitResult:
@@ -482,6 +534,7 @@ def ransac_fit(candidates: list[EdgeCandidate], frame_size: tuple[int, int], cfg
     return _record_to_fit(rec[0].cpu().numpy())
 
 
+@_with_device
 def fit_area(candidates: list[EdgeCandidate], frame_size: tuple[int, int],
              cfg: EcaConfig | None = None, seed: int = 0, device=None) -> FitResult:
     """North-star name: filter_candidates + ransac_fit in one device call."""
@@ -512,14 +565,87 @@ def _batch_shape(frames) -> tuple[int, int]:
     return validate_frame(frames)
 
 
+class _FrameEstimator:
+    """estimate() of ONE handcrafted frame of a fixed (H, W, cfg, seed, device),
+    everything preallocated: one fused launch (strip scoring -> candidates ->
+    filter -> RANSAC, eca_estimate_handcrafted) whose fit writes the record
+    straight into pinned host memory, then a stream synchronisation.  Host
+    frames: the 3 rows of every strip are copied into a pinned buffer that the
+    kernel reads over PCIe (no H2D copy, no full-frame transfer).  A lock
+    serialises callers (the buffers are shared)."""
+
+    def __init__(self, height: int, width: int, cfg: EcaConfig, seed: int, device):
+        self.h, self.w, self.dev = height, width, device
+        self.rows = strip_heights(height, cfg.strip_count, cfg.strip_weighting)
+        s = self.s = len(self.rows)
+        self.c_rows = _i32_array(self.rows)
+        self.c_band = _i32_array([3 * k for k in range(s)])
+        self.params = cfg.device_params(width, height)
+        self.p_params = ctypes.byref(self.params)
+        with _on(device):
+            self.trip = _dev_triplets(seed, cfg.ransac_attempts, 2 * s, device)
+            self.cnt = torch.zeros(1, dtype=torch.int32, device=device)
+            self.xs = torch.empty((1, 2 * s), dtype=torch.int32, device=device)
+            self.ys = torch.empty_like(self.xs)
+            self.sc = torch.empty((1, 2 * s), dtype=torch.float64, device=device)
+        self.rec_host = torch.zeros((1, 5), dtype=torch.float64).pin_memory()
+        self.rec_np = self.rec_host.numpy()
+        self.bands_host = torch.empty((3 * s, width, 3), dtype=torch.uint8).pin_memory()
+        self.bands_np = self.bands_host.numpy()
+        self.row_idx = np.array([r + d for r in self.rows for d in (-1, 0, 1)], dtype=np.intp)
+        self.args = [_ptr(self.trip), _ptr(self.cnt), _ptr(self.xs), _ptr(self.ys), _ptr(self.sc),
+                     ctypes.c_void_p(self.rec_host.data_ptr())]
+        self.fn = _lib.load().eca_estimate_handcrafted
+        self.lock = threading.Lock()
+
+    def __call__(self, frame) -> ContentArea:
+        with self.lock, _on(self.dev):
+            if isinstance(frame, torch.Tensor) and frame.is_cuda:
+                t = frame if frame.device == self.dev else frame.to(self.dev)
+                if t.stride(2) != 1 or t.stride(1) != 3 or t.stride(0) < 3 * self.w:
+                    t = t.contiguous()
+                ptr, rs, band = ctypes.c_void_p(t.data_ptr()), t.stride(0), None
+            else:
+                a = frame.numpy() if isinstance(frame, torch.Tensor) else frame
+                np.take(a, self.row_idx, axis=0, out=self.bands_np)
+                ptr, rs, band = ctypes.c_void_p(self.bands_host.data_ptr()), 3 * self.w, self.c_band
+            stream = torch.cuda.current_stream(self.dev)
+            _lib.check(self.fn(ptr, 1, 0, rs, self.c_rows, band, self.s, self.p_params, *self.args,
+                               ctypes.c_void_p(stream.cuda_stream)), "eca_estimate_handcrafted")
+            stream.synchronize()
+            r = self.rec_np[0]
+            if int(r.view(np.int32)[9]) == _lib.ACCEPTED:
+                return CircularArea(Circle(float(r[0]), float(r[1]), float(r[2])), float(r[3]))
+            return FULL_FRAME
+
+
+_FRAME_ESTIMATORS: dict = {}
+
+
 def estimate(frame, variant: EstimatorVariant = HANDCRAFTED, cfg: EcaConfig | None = None,
              seed: int = 0, device=None) -> ContentArea:
-    """Content area of one RGB frame (estimator.py:55-74)."""
-    validate_frame(frame)
-    out = estimate_batch([frame], variant, cfg, seed, device=device)[0]
-    if isinstance(out, FrameError):
-        raise ValueError(out.message)
-    return out
+    """Content area of one RGB frame (estimator.py:55-74).  The handcrafted
+    variant takes the cached single-frame path (_FrameEstimator)."""
+    width, height = validate_frame(frame)
+    cfg = cfg or config_default()
+    if isinstance(variant, Learned):
+        out = estimate_batch([frame], variant, cfg, seed, device=device)[0]
+        if isinstance(out, FrameError):
+            raise ValueError(out.message)
+        return out
+    if seed < 0:
+        raise ValueError("expected non-negative integer seed")
+    _check_config(cfg)
+    if device is None and isinstance(frame, torch.Tensor) and frame.is_cuda:
+        device = frame.device
+    dev = _device(device)
+    key = (height, width, cfg, seed, dev)
+    est = _FRAME_ESTIMATORS.get(key)
+    if est is None:
+        if len(_FRAME_ESTIMATORS) > 32:
+            _FRAME_ESTIMATORS.clear()
+        est = _FRAME_ESTIMATORS[key] = _FrameEstimator(height, width, cfg, seed, dev)
+    return est(frame)
 
 
 estimate_area = estimate
@@ -533,6 +659,7 @@ def estimate_batch(frames, variant: EstimatorVariant = HANDCRAFTED, cfg: EcaConf
     ``threads`` is accepted for signature compatibility (the GPU replaces the
     reference's thread pool)."""
     cfg = cfg or config_default()
+    _check_config(cfg)
     items = list(frames) if not (isinstance(frames, (np.ndarray, torch.Tensor)) and frames.ndim == 4) \
         else [frames[i] for i in range(frames.shape[0])]
     out: list = [None] * len(items)
@@ -548,12 +675,13 @@ def estimate_batch(frames, variant: EstimatorVariant = HANDCRAFTED, cfg: EcaConf
     if not groups:
         return out
     dev = _device(device)
-    for (w, h), idx in groups.items():
-        rows = strip_heights(h, cfg.strip_count, cfg.strip_weighting)
-        sub = [items[i] for i in idx]
-        rec = _estimate_group(sub, w, h, rows, variant, cfg, seed, dev)
-        for i, res in zip(idx, _records_to_results(rec)):
-            out[i] = res
+    with _on(dev):
+        for (w, h), idx in groups.items():
+            rows = strip_heights(h, cfg.strip_count, cfg.strip_weighting)
+            sub = [items[i] for i in idx]
+            rec = _estimate_group(sub, w, h, rows, variant, cfg, seed, dev)
+            for i, res in zip(idx, _records_to_results(rec)):
+                out[i] = res
     return out
 
 
@@ -583,6 +711,7 @@ def _area_records(areas, device) -> torch.Tensor:
     return torch.from_numpy(rec).to(device)
 
 
+@_with_device
 def draw_mask(areas, height: int, width: int, device=None) -> torch.Tensor:
     """uint8 content masks on the GPU: 1 inside the closed disk at pixel centres
     (geometry.py:30-34), all ones for FullFrame.  ``areas`` is one area (-> (H,W))
@@ -600,6 +729,7 @@ def draw_mask(areas, height: int, width: int, device=None) -> torch.Tensor:
     return out[0] if single else out
 
 
+@_with_device
 def crop_bounds(areas, height: int, width: int, device=None) -> list[tuple[int, int, int, int] | None]:
     """crop_augment's inclusive rectangle per area (dataset.py:151-187), or None."""
     dev = _device(device)
@@ -610,6 +740,7 @@ def crop_bounds(areas, height: int, width: int, device=None) -> list[tuple[int, 
     return [None if r[0] < 0 else tuple(int(v) for v in r) for r in out.cpu().numpy()]
 
 
+@_with_device
 def crop_area(frame, area, device=None):
     """Largest centred axis-aligned rectangle inside the content disk, copied out
     on the GPU (dataset.py:151-187).  FullFrame raises ValueError like the

@@ -167,3 +167,18 @@ def test_prefilter_accepts_the_golden_configs():
         got[c["name"].split("_")[0]] = lib.eca_prefilter_bound(ctypes.byref(p), ctypes.byref(b))
     assert got["ti5"] == 1
     assert all(v == 0 for k, v in got.items() if k != "ti5"), got
+
+
+def test_validate_frame_rejects_frames_outside_the_kernel_envelope():
+    """Frames wider than the kernels take raise ValueError (a per-frame
+    FrameError in estimate_batch), not a native error for the whole batch."""
+    with pytest.raises(ValueError, match="too large"):
+        api.validate_frame(np.zeros((20, _lib.MAX_WIDTH + 1, 3), dtype=np.uint8))
+    big = np.lib.stride_tricks.as_strided(np.zeros(3, dtype=np.uint8), (api.MAX_FRAME_HEIGHT + 1, 8, 3),
+                                          (0, 0, 1))
+    with pytest.raises(ValueError, match="too large"):
+        api.validate_frame(big)
+    with pytest.raises(ValueError, match="strip_count"):
+        api._check_config(EcaConfig(strip_count=_lib.MAX_STRIPS + 1))
+    with pytest.raises(ValueError, match="ransac_attempts"):
+        api._check_config(EcaConfig(ransac_attempts=_lib.MAX_ATTEMPTS + 1))

@@ -55,6 +55,14 @@ for ready in (True, False):
         us = sorted(x[0] for x in r)
         host = sorted(x[1] for x in r)[1]
         print(f"pipelined ready={ready} steps={steps}: {us[1]:.1f} us/step (min {us[0]:.1f} max {us[2]:.1f}; host {host:.1f} us)")
+torch.cuda.synchronize()
+w0 = time.perf_counter()
+for i in range(100):
+    eng.run_pipelined(sl(i), frames_ready=True)
+w1 = time.perf_counter()
+eng.fence()
+torch.cuda.synchronize()
+print(f"host enqueue only: {(w1 - w0) / 100 * 1e6:.1f} us/step")
 us, _ = timed(lambda i: eng.run(sl(i)), 100)
 print(f"run() single launch, no overlap: {us:.1f} us")
 us, _ = timed(lambda i: eng.bounds(sl(i), overlap=True, slot=i % 4), 100)
