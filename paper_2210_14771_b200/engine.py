@@ -158,7 +158,8 @@ class ContentAreaEngine:
 
     PIPE_SETS = 4   # eca_pipeline_* buffer sets (records stay valid this many steps)
 
-    def run_pipelined(self, frames: torch.Tensor, frames_ready: bool = False) -> torch.Tensor:
+    def run_pipelined(self, frames: torch.Tensor, frames_ready: bool = False,
+                      records_out: torch.Tensor | None = None) -> torch.Tensor:
         """Throughput mode for a stream of batches: ONE launch per batch
         (eca_pipeline_step) on the current stream -- bound-and-prune with the
         final stage (each frame's last half-row warp rescores and fits it);
@@ -168,9 +169,19 @@ class ContentAreaEngine:
         later.  ``frames_ready``: the frames were complete before the previous
         operation on the stream was enqueued (a pre-filled pool), so the
         kernel need not wait for that operation (otherwise it does, in case it
-        produced them).  Same records as run() (tests/test_gpu_parity.py)."""
+        produced them).  ``records_out``: a (B,5) float64 tensor (device or
+        pinned host) the fit kernel also writes this batch's records to.  Same
+        records as run() (tests/test_gpu_parity.py)."""
+        if records_out is not None and (tuple(records_out.shape) != (self.batch, 5) or
+                                        records_out.dtype != torch.float64 or
+                                        not records_out.is_contiguous() or
+                                        not (records_out.is_cuda or records_out.is_pinned())):
+            raise ValueError("records_out must be a contiguous (B,5) float64 device or pinned tensor")
         if isinstance(self.variant, api.Learned) or self.fused:
-            return self.run(frames)
+            rec = self.run(frames)
+            if records_out is not None:
+                records_out.copy_(rec, non_blocking=True)
+            return rec
         if frames.dim() == 4 and (frames.stride(3) != 1 or frames.stride(2) != 3):
             raise ValueError("run_pipelined takes frames with packed pixels (stride (.., .., 3, 1))")
         f = self._check_frames(frames)
@@ -179,8 +190,9 @@ class ContentAreaEngine:
         p = self._pipeline()
         out = p["out"]
         flags = _lib.PIPE_FRAMES_READY if frames_ready else 0
+        extra = None if records_out is None else ctypes.c_void_p(records_out.data_ptr())
         _lib.check(p["step"](p["handle"], ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1), flags,
-                             None, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
+                             extra, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
                              ctypes.byref(out)), "eca_pipeline_step")
         rec = p["views"].get(out.value)
         if rec is None:   # a view of this buffer set's records inside the scratch

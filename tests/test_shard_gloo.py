@@ -70,3 +70,69 @@ def test_gather_records_world2(n_frames):
         assert np.array_equal(full[:, 3], 0.5 * np.arange(n_frames))
         assert np.array_equal(full.view(np.int32).reshape(n_frames, 10)[:, 9], np.arange(n_frames) % 4)
     assert np.array_equal(out[0], out[1])
+
+
+class _StubEngine:
+    """Stands in for ContentAreaEngine on CPU: 'frames' are global frame
+    indices; the records it writes encode them."""
+
+    def __init__(self, batch, log):
+        self.batch, self.log = batch, log
+        self.device = torch.device("cpu")
+
+    def run_pipelined(self, frames, frames_ready=False, records_out=None):
+        assert frames.shape[0] == self.batch and records_out.shape == (self.batch, 5)
+        records_out.zero_()
+        records_out[:, 0] = frames.double()
+        records_out[:, 3] = 0.25 * frames.double()
+        records_out.view(torch.int32).view(self.batch, 10)[:, 9] = (frames % 4).int()
+        self.log.append(("run", self.batch))
+        return records_out
+
+    def fence(self):
+        self.log.append(("fence", self.batch))
+
+
+def _sharded_worker(rank, world, port, n_frames, chunk, every, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2210_14771_b200.shard import ShardedEstimator
+        log = []
+        est = ShardedEstimator(n_frames, 8, 8, chunk=chunk, gather_every=every,
+                               engine_factory=lambda b: _StubEngine(b, log))
+        idx = torch.arange(est.start, est.stop)
+        full = est.run(lambda a, b: idx[a:b], frames_ready=True)
+        n_eng = (est.engine is not None) + (est.tail_engine is not None)
+        q.put((rank, full.numpy(), est.gathers, len(est.gather_spans()), n_eng,
+               sum(1 for k, _ in log if k == "run"), len(est.batches())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("n_frames,chunk,every", [(100, 8, 2), (37, 8, 1), (3, 4, 2)])
+def test_sharded_estimator_stream(world, n_frames, chunk, every):
+    """ShardedEstimator over world 2 and 4 (gloo): contiguous shards, one
+    engine per batch size (full + ragged tail) built once, the same gather
+    schedule on every rank (collectives), the full table in frame order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, n_frames, chunk, every, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {r: rest for r, *rest in (q.get(timeout=180) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        full, gathers, spans, n_eng, runs, batches = out[r]
+        assert full.shape == (n_frames, 5)
+        assert np.array_equal(full[:, 0], np.arange(n_frames))
+        assert np.array_equal(full[:, 3], 0.25 * np.arange(n_frames))
+        assert np.array_equal(full.view(np.int32).reshape(n_frames, 10)[:, 9], np.arange(n_frames) % 4)
+        assert gathers == spans == out[0][2]
+        assert runs == batches and n_eng <= 2
