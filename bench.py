@@ -72,54 +72,62 @@ def base_frames(n: int = N_BASE) -> np.ndarray:
 
 # ------------------------------------------------------------------ clocks ---
 class ClockSampler:
-    """NVML sampling of SM clock + throttle reasons while the timed region runs."""
+    """SM clock + throttle reasons while the timed region runs, sampled by an
+    `nvidia-smi -lms` subprocess (off the interpreter that enqueues the steps)."""
 
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index: int):
-        self.samples, self.reasons, self.ok = [], set(), False
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.ok = True
-        except Exception as exc:  # noqa: BLE001
-            log("clock sampling unavailable:", exc)
-            self.max_mhz = None
-        self._stop = threading.Event()
-
-    def _poll(self):
-        nv = self.nv
-        while not self._stop.is_set():
-            self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-            try:
-                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-            except AttributeError:
-                bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-            for b, name in self.REASONS.items():
-                if bits & b:
-                    self.reasons.add(name)
-            time.sleep(0.0005)
+    def __init__(self, index: int, period_ms: int = 20):
+        self.index, self.period = index, period_ms
+        self.proc, self.max_mhz = None, None
+        self.samples, self.reasons = [], set()
 
     def __enter__(self):
-        if self.ok:
-            self._t = threading.Thread(target=self._poll, daemon=True)
-            self._t.start()
+        import shutil
+        import subprocess
+        smi = shutil.which("nvidia-smi")
+        if smi:
+            try:
+                self.max_mhz = int(subprocess.run(
+                    [smi, "-i", str(self.index), "--query-gpu=clocks.max.sm", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=20).stdout.strip() or 0) or None
+                self.proc = subprocess.Popen(
+                    [smi, "-i", str(self.index), "--query-gpu=clocks.sm,clocks_event_reasons.active",
+                     "--format=csv,noheader,nounits", "-lms", str(self.period)],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                time.sleep(0.2)   # first sample before the timed region starts
+            except Exception as exc:  # noqa: BLE001
+                log("clock sampling unavailable:", exc)
+                self.proc = None
         return self
 
     def __exit__(self, *exc):
-        if self.ok:
-            self._stop.set()
-            self._t.join()
+        if self.proc is None:
+            return
+        time.sleep(2.5 * self.period / 1000)   # a sample after the region
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=20)
+        for line in out.splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 2:
+                continue
+            try:
+                self.samples.append(int(parts[0]))
+                bits = int(parts[1], 16)
+            except ValueError:
+                continue
+            for bit, name in self.REASONS.items():
+                if bits & bit:
+                    self.reasons.add(name)
 
     def summary(self):
-        if not self.ok or not self.samples:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "method": f"nvidia-smi -lms {self.period} subprocess, from just before to just after "
+                          "the timed region"}
 
 
 # ------------------------------------------------------------- CPU baseline ---
@@ -186,6 +194,39 @@ def run_reference(args) -> None:
 
 
 # --------------------------------------------------------------------- ours ---
+C5_FRAMES, C5_POOL = 100_000, 1024
+
+
+def pool_base_index(i: int, rank: int) -> int:
+    """Render (of the N_BASE distinct ones) in pool slot i of this rank."""
+    return (i + rank * 7) % N_BASE
+
+
+def oracle_records(base: np.ndarray) -> list:
+    """The reference's estimate of every distinct render (numpy oracle port),
+    the parity check of the timed runs' records."""
+    from oracle import eca_oracle as orc
+    from paper_2210_14771_b200.params import EcaConfig
+    cfg = EcaConfig()
+    return [orc.estimate(f, cfg, 0) for f in base]
+
+
+def check_records(recs, base_idx, want) -> dict:
+    """recs: (B,5) device record tensors; base_idx[k][i]: render of row i of
+    recs[k]; want: oracle tuples per render.  Status / inliers exact, circle
+    within 1e-3 px."""
+    n = bad = 0
+    for rec, idx in zip(recs, base_idx):
+        for row, k in zip(_records_np(rec), idx):
+            st, cx, cy, r, score, inl = want[k]
+            ok = row[5] == st and (st != 0 or (abs(row[0] - cx) <= 1e-3 and abs(row[1] - cy) <= 1e-3 and
+                                               abs(row[2] - r) <= 1e-3 and row[4] == inl))
+            n += 1
+            bad += not ok
+    return {"frames_checked": n, "mismatches": bad, "distinct_renders": len(set(i for ix in base_idx for i in ix)),
+            "bar": "status + inliers exact, cx/cy/r within 1e-3 px of the numpy oracle port"}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -204,43 +245,35 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=dev)
 
     base = base_frames()
+    want = oracle_records(base) if rank == 0 else None
     pool = torch.empty((POOL, HEIGHT, WIDTH, 3), dtype=torch.uint8, device=dev)
     base_dev = torch.from_numpy(base).to(dev)
     for i in range(POOL):   # distinct addresses: a step never re-reads L2-resident rows
-        pool[i].copy_(base_dev[(i + rank * 7) % N_BASE])
+        pool[i].copy_(base_dev[pool_base_index(i, rank)])
     del base_dev
     torch.cuda.synchronize()
 
     eng = ContentAreaEngine(HEIGHT, WIDTH, BATCH, device=dev)
-    gathered = torch.empty((world * BATCH, 5), dtype=torch.float64, device=dev) if world > 1 else None
     n_slots = POOL // BATCH
+    stream = torch.cuda.current_stream(dev)
 
-    def step(i: int):
-        # streaming throughput mode: bound-and-prune of this batch on the main
-        # stream; FP64 rescore + fit (+ the record all-gather) on the engine's
-        # side stream, overlapping the next step's bound-and-prune
-        rec = eng.run_pipelined(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH], frames_ready=True)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, rec)
-
-    # parity spot-check of the benchmarked configuration against pool contents
-    for i in range(args.warmup):
-        step(i)
+    # streaming throughput mode, host-light: the K steps are ONE native call
+    # (eca_pipeline_run): per batch a bound-and-prune launch + a fit launch,
+    # programmatic dependent launches so batches overlap.  The pool was
+    # filled before, so the kernels need not wait on the previous kernel.
+    eng.run_stream(pool, 0, args.warmup)
     eng.fence()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-
-    stream = torch.cuda.current_stream(dev)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0.record(stream)
-        for i in range(args.steps):
-            step(args.warmup + i)
-        eng.fence(stream)   # the last step's fit (and gather) are inside the timed region
+        recs = eng.run_stream(pool, args.warmup, args.steps)
+        eng.fence(stream)   # the last step's fits are inside the timed region
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -252,6 +285,11 @@ def run_ours(args) -> None:
     ms = float(ms_t.item())
     value = world * BATCH * args.steps / (ms / 1e3)
     ms_step = ms / args.steps
+    parity = None
+    if rank == 0:   # the timed run's last batches against the oracle (outside the timed region)
+        steps_done = [args.warmup + j for j in range(args.steps - len(recs), args.steps)]
+        idx = [[pool_base_index((st % n_slots) * BATCH + f, rank) for f in range(BATCH)] for st in steps_done]
+        parity = check_records(recs, idx, want)
 
     # kernel-only timing of the step's dominant kernel (K1 bound-and-prune,
     # bounds_kernel) over the same pool, on the same stream, in two launch
@@ -260,17 +298,18 @@ def run_ours(args) -> None:
     # previous launch's tail, on 4 rotating workspaces (the roofline number);
     # (b) isolated, each launch waiting for the previous one to finish
     kt0, kt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k_steps = max(args.steps, 50)
 
     def time_bounds(overlap: bool) -> float:
         for i in range(4):
             eng.bounds(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH], overlap=overlap, slot=i % 4)
         torch.cuda.synchronize()
         kt0.record(stream)
-        for i in range(args.steps):
+        for i in range(k_steps):
             eng.bounds(pool[(i % n_slots) * BATCH:(i % n_slots + 1) * BATCH], overlap=overlap, slot=i % 4)
         kt1.record(stream)
         torch.cuda.synchronize()
-        return kt0.elapsed_time(kt1) / args.steps
+        return kt0.elapsed_time(kt1) / k_steps
     k_ms = time_bounds(True)
     k_ms_isolated = time_bounds(False)
     bytes_launch = STRIP_BYTES_PER_FRAME * BATCH
@@ -282,62 +321,53 @@ def run_ours(args) -> None:
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
 
-    # end-to-end through the public engine API from pinned host frames: the
-    # bound-and-prune kernel reads the strip rows straight from pinned host
-    # memory, chunk by chunk as far as its scan gets (zero-copy), then the
-    # records come back D2H; every step synchronises.  The H2D-copy path
-    # (run_host: strided copies of every strip row) is reported beside it.
-    host = torch.from_numpy(np.stack([base[(i + rank) % N_BASE] for i in range(BATCH)])).pin_memory()
-    e_steps = max(3, min(args.steps, 50))
+    c5 = c5_leg(eb, dev, base, rank, world)
 
-    def e2e_rate(fn):
-        for _ in range(max(3, args.warmup // 4)):
-            fn(host)
-        torch.cuda.synchronize()
-        b0 = eng.zero_copy_bytes()
-        w0 = time.perf_counter()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(e_steps):
-            fn(host)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e_wall = time.perf_counter() - w0
-        e_ms = max(e0.elapsed_time(e1), e_wall * 1e3)
-        e_ms_t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e_ms_t, op=dist.ReduceOp.MAX)
-        return (world * BATCH * e_steps / (float(e_ms_t.item()) / 1e3),
-                (eng.zero_copy_bytes() - b0) // e_steps)
-
-    e2e_sync, h2d = e2e_rate(eng.run_host_zero_copy)  # h2d = bytes read over PCIe per step
-    e2e_copy, _ = e2e_rate(eng.run_host)                # H2D copies of all strip rows
-    h2d_copy = BATCH * eng.n_strips * 3 * WIDTH * 3
-    d2h = BATCH * 40
-    # streamed (the headline): each step reads its frames over PCIe (zero-copy)
-    # and lands its records in pinned host memory; steps overlap, the timed
-    # region ends when the last step's records are on the host
-    recs = [torch.empty((BATCH, 5), dtype=torch.float64).pin_memory() for _ in range(2)]
-    for i in range(max(3, args.warmup // 4)):
-        eng.run_host_pipelined(host, recs[i % 2])
+    # end to end through the public engine API from pinned HOST frames, 4
+    # distinct host batches rotating: every step the bound-and-prune kernel
+    # reads the strip rows it visits over PCIe (zero-copy TMA, bytes counted by
+    # the kernel) and the fit kernel writes the records into pinned host
+    # memory; steps overlap, wall clock until the last records are on the host
+    hosts = [torch.from_numpy(np.stack([base[(i + 5 * h + rank) % N_BASE] for i in range(BATCH)])).pin_memory()
+             for h in range(4)]
+    e_steps = max(8, min(args.steps, 64))
+    host_recs = [torch.zeros((BATCH, 5), dtype=torch.float64).pin_memory() for _ in range(4)]
+    for i in range(max(4, args.warmup)):
+        eng.run_host_pipelined(hosts[i % 4], host_recs[i % 4])
     eng.fence()
     torch.cuda.synchronize()
+    b0 = eng.pipeline_zero_copy_bytes()
     if world > 1:
         dist.barrier()
     w0 = time.perf_counter()
     for i in range(e_steps):
-        eng.run_host_pipelined(host, recs[i % 2])
+        eng.run_host_pipelined(hosts[i % 4], host_recs[i % 4])
     eng.fence()
     torch.cuda.synchronize()
-    e_ms_t = torch.tensor([(time.perf_counter() - w0) * 1e3], dtype=torch.float64, device=dev)
+    e_wall = time.perf_counter() - w0
+    h2d = (eng.pipeline_zero_copy_bytes() - b0) // e_steps
+    e_ms_t = torch.tensor([e_wall * 1e3], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e_ms_t, op=dist.ReduceOp.MAX)
     e2e = world * BATCH * e_steps / (float(e_ms_t.item()) / 1e3)
+    e2e_parity = None
+    if rank == 0:   # the last 4 host batches' records, straight from pinned memory
+        idx = [[(i + 5 * ((e_steps - 4 + j) % 4) + rank) % N_BASE for i in range(BATCH)] for j in range(4)]
+        e2e_parity = check_records([host_recs[(e_steps - 4 + j) % 4] for j in range(4)], idx, want)
+    e2e_sync = None
+    if rank == 0:   # the synchronous form (one call, host sync every step)
+        for _ in range(3):
+            eng.run_host_zero_copy(hosts[0])
+        w0 = time.perf_counter()
+        for i in range(16):
+            eng.run_host_zero_copy(hosts[i % 4])
+        e2e_sync = BATCH * 16 / (time.perf_counter() - w0)
+    d2h = BATCH * 40
 
     lat = learned = mask = crop = uhd = evaluation = training = labelling = None
     if rank == 0:
         lat = latency(eb, dev)
-        learned = learned_leg(eb, dev, pool, n_slots, peaks)
+        learned = learned_leg(eb, dev, pool, n_slots, peaks, base)
         mask = mask_leg(eb, dev, eng, pool, peaks)
         crop = crop_leg(eb, dev, eng, pool, peaks)
         uhd = uhd_leg(eb, dev, peaks)
@@ -372,12 +402,16 @@ def run_ours(args) -> None:
                        "pool_frames": POOL, "distinct_renders": N_BASE,
                        "l2": f"inputs larger than L2: {POOL}-slot HBM pool rotated "
                              f"({POOL * STRIP_BYTES_PER_FRAME / 1e6:.0f} MB of strip rows > 126 MB L2)",
-                       "parallelism": f"dp{world}" + (" + NCCL all-gather of 40-B records" if world > 1 else ""),
-                       "pipelining": "2 streams: rescore+fit of batch i overlap the next batches' "
-                                     "bound-and-prune (programmatic dependent launches, 16 buffer sets)"},
+                       "parallelism": f"dp{world}: each rank streams its own batches (weak scaling); "
+                                      "the 100k-frame sharded stream with NCCL record gathers is c5_stream",
+                       "pipelining": "one native call enqueues the K steps (eca_pipeline_run); per step a "
+                                     "bound-and-prune launch and a fit launch (FP64 rescore + RANSAC), both "
+                                     "programmatic dependent launches, 4 rotating buffer sets with a "
+                                     "device-side reuse guard"},
+            "parity": parity,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "eca::bounds_kernel<1> (K1 strip scoring: exact integer Sobel / "
+                         "kernel": "eca::bounds_kernel<1, 0> (K1 strip scoring: exact integer Sobel / "
                                    "preceding max, FP32 bound-and-prune, survivor slots)",
                          "kernel_share_of_step": round(k_ms / ms_step, 3),
                          "algorithmic_bytes_per_launch": bytes_launch,
@@ -387,19 +421,19 @@ def run_ours(args) -> None:
                                         "4 rotating workspaces; kernel_ms = event time / launches",
                          "kernel_ms_isolated": round(k_ms_isolated, 5),
                          "frac_isolated": round(bytes_launch / (k_ms_isolated / 1e3) / 1e9 / peak, 4),
+                         "step_frac": round(bytes_launch / (ms_step / 1e3) / 1e9 / peak, 4),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
             "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": d2h, "steps": e_steps,
-                    "path": "ContentAreaEngine.run_host_pipelined: every step, pinned host frames "
-                            "read over PCIe by the bound-and-prune kernel's TMA, chunk by chunk as "
-                            "far as its scan gets (h2d bytes counted by the kernel), rescore + fit, "
-                            "records D2H into pinned host memory; steps overlap, wall clock until the "
-                            "last step's records are on the host",
-                    "synchronous_path": {"value": round(e2e_sync, 2),
-                                         "path": "run_host_zero_copy: same reads, host sync every step"},
-                    "h2d_copy_path": {"value": round(e2e_copy, 2), "h2d_bytes_per_step": h2d_copy,
-                                      "path": "ContentAreaEngine.run_host: cudaMemcpy2DAsync of every "
-                                              "strip row, then the device-resident kernels"}},
+                    "d2h_bytes_per_step": d2h, "steps": e_steps, "host_batches": 4, "parity": e2e_parity,
+                    "path": "ContentAreaEngine.run_host_pipelined over 4 distinct pinned host batches: "
+                            "every step the bound-and-prune kernel reads the strip rows it visits from "
+                            "pinned host memory over PCIe (zero-copy TMA, h2d bytes counted by the kernel), "
+                            "the fit kernel writes the 40-B records into pinned host memory; steps overlap, "
+                            "wall clock until the last step's records are on the host",
+                    "synchronous_path": None if e2e_sync is None else {
+                        "value": round(e2e_sync, 2),
+                        "path": "run_host_zero_copy: same reads, host sync every step"}},
+            "c5_stream": c5,
             "latency_ms": lat,
             "learned": learned,
             "mask": mask,
@@ -409,7 +443,7 @@ def run_ours(args) -> None:
             "training": training,
             "pseudo_labelling": labelling,
             "clocks": clocks.summary(),
-            "gpu_launches": args.steps * eng.launches_per_run,
+            "gpu_launches": args.steps * eng.launches_per_step + 1,
             "cpu_baseline": cpu,
         }
     if world > 1:
@@ -419,13 +453,65 @@ def run_ours(args) -> None:
         print(json.dumps(out), flush=True)
 
 
+def c5_leg(eb, dev, base, rank: int, world: int) -> dict:
+    """BASELINE config 5: the 100k-frame 1080p stream (frame k = render of pool
+    slot k mod 1024), contiguous shards per rank (ShardedEstimator): batches of
+    256 through the pipeline, records written by the fit kernel into the send
+    buffer, one NCCL all_gather_into_tensor per 32 batches on a side stream.
+    frames/s = 100k / the slowest rank's device time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2210_14771_b200.shard import ShardedEstimator
+    pool = torch.empty((C5_POOL, HEIGHT, WIDTH, 3), dtype=torch.uint8, device=dev)
+    bd = torch.from_numpy(base).to(dev)
+    for i in range(C5_POOL):
+        pool[i].copy_(bd[i % N_BASE])
+    del bd
+    se = ShardedEstimator(C5_FRAMES, HEIGHT, WIDTH, device=dev, chunk=BATCH, gather_every=32)
+
+    def frames(a, b):   # local rows [a, b) -> pool views (a batch never wraps the pool: 1024 % 256 == 0)
+        k = (se.start + a) % C5_POOL
+        if k + (b - a) <= C5_POOL:
+            return pool[k:k + (b - a)]
+        return torch.cat([pool[k:], pool[:(k + b - a) - C5_POOL]])
+    torch.cuda.synchronize()
+    se.run(frames, frames_ready=True)   # warm-up (engines, pipeline, NCCL)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    table = se.run(frames, frames_ready=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms_t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    per_rank = [float(ms_t.item())]
+    if world > 1:
+        gathered = torch.empty(world, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(gathered, ms_t)
+        per_rank = gathered.cpu().tolist()
+    ms = max(per_rank)
+    st = table.view(torch.int32).view(C5_FRAMES, 10)[:, 9]
+    del pool
+    torch.cuda.empty_cache()
+    return {"metric": "100k-frame 1080p stream frames/s (C5: contiguous shards, NCCL gather of 40-B records)",
+            "value": round(C5_FRAMES / (ms / 1e3), 1), "unit": "frames/s", "frames": C5_FRAMES,
+            "ms": round(ms, 3), "rank_ms": [round(v, 3) for v in per_rank], "scaling": "strong",
+            "gathers_per_rank": se.gathers, "record_bytes_gathered": C5_FRAMES * 40,
+            "accepted": int((st == 0).sum().item()),
+            "path": "ShardedEstimator.run: full + tail engines, run_pipelined per 256-frame batch, "
+                    "all_gather_into_tensor per 32 batches on a side stream; device time on the compute "
+                    "stream incl. the final gather, max over ranks"}
+
+
 # FLOPs of the strip CNN per frame (SURVEY 8(d) K3): 16 strips x
 # 2 x [5*8*9*5*(W-2) + 8*16*9*3*(W-4) + 16*32*9*(W-6) + 32*(W-6)]
 CNN_FLOP_PER_FRAME = 16 * 2 * (5 * 8 * 9 * 5 * (WIDTH - 2) + 8 * 16 * 9 * 3 * (WIDTH - 4)
                                + 16 * 32 * 9 * (WIDTH - 6) + 32 * (WIDTH - 6))
 
 
-def learned_leg(eb, dev, pool, n_slots, peaks) -> dict:
+def learned_leg(eb, dev, pool, n_slots, peaks, base=None) -> dict:
     """C3: the learned variant (EdgeNet strip CNN, random-init FP32 weights
     of the reference architecture, edgenet.py) over the same 256-frame
     batches: CNN + half-row selection + fit, frames resident in HBM."""
@@ -465,7 +551,58 @@ def learned_leg(eb, dev, pool, n_slots, peaks) -> dict:
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (measured)"},
             "simt_variant": {"value": round(BATCH / (ms_simt * 1e-3), 1), "unit": "frames/s",
                              "ms_per_step": round(ms_simt, 4),
-                             "kernel": "cnn_kernel: FP32 FMA on the CUDA cores (ECA_LEARNED_SIMT)"}}
+                             "kernel": "cnn_kernel: FP32 FMA on the CUDA cores (ECA_LEARNED_SIMT)"},
+            "candidate_agreement": None if base is None else learned_agreement(eb, dev, net, base)}
+
+
+_CPU_LCANDS = None
+
+
+def _cpu_learned_cands(idx: int):
+    from oracle import eca_oracle as orc
+    from paper_2210_14771_b200.params import EcaConfig
+    frames, layers = _CPU_LCANDS
+    f = frames[idx]
+    cfg = EcaConfig()
+    rows = orc.strip_rows(f.shape[0], cfg.strip_count, cfg.strip_weighting)
+    sc = orc.learned_scores(f, rows, [100.0] * 3, [50.0] * 3, layers)
+    xs, _, _ = orc.candidates_from_scores(sc, rows)
+    return xs, sc
+
+
+def learned_agreement(eb, dev, net, base, n: int = 16) -> dict:
+    """SURVEY 8(c) learned contract: the learned variant's half-row winners
+    (3xTF32 tcgen05 CNN) against the numpy FP32 oracle on the same frames;
+    every disagreement must be a near-tie in the oracle's own probabilities."""
+    import torch
+    from paper_2210_14771_b200.engine import ContentAreaEngine
+    global _CPU_LCANDS
+    from oracle import eca_oracle as orc
+    frames = base[:n]
+    eng = ContentAreaEngine(HEIGHT, WIDTH, n, variant=eb.Learned(net), device=dev)
+    eng.run(torch.from_numpy(frames).to(dev))
+    got = eng.xs.cpu().numpy()
+    _CPU_LCANDS = (frames, orc.glorot_layers(0))
+    import multiprocessing as mp
+    with ProcessPoolExecutor(min(n, os.cpu_count() or 1), mp_context=mp.get_context("fork")) as ex:
+        ref = list(ex.map(_cpu_learned_cands, range(n)))
+    s = eng.n_strips
+    total = agree = ties = 0
+    worst = 0.0
+    for k, (xs, sc) in enumerate(ref):
+        for j in range(2 * s):
+            total += 1
+            if got[k, j] == xs[j]:
+                agree += 1
+                continue
+            row = sc[j % s]
+            gap = abs(float(row[xs[j]]) - float(row[got[k, j]]))
+            worst = max(worst, gap)
+            ties += gap <= 1e-5
+    return {"half_rows": total, "agree": agree, "rate": round(agree / total, 6),
+            "disagreements_near_tie": ties, "max_prob_gap_at_disagreement": worst,
+            "frames": n, "reference": "numpy FP32 oracle port of edgenet.score_strips_learned",
+            "near_tie_bar": "oracle probability gap between the two columns <= 1e-5"}
 
 
 def mask_leg(eb, dev, eng, pool, peaks) -> dict:
@@ -815,15 +952,13 @@ def uhd_leg(eb, dev, peaks) -> dict:
     del base
     eng = ContentAreaEngine(h, w, b, device=dev)
     stream = torch.cuda.current_stream(dev)
-    for i in range(3):
-        eng.run_pipelined(pool[(i % slots) * b:(i % slots + 1) * b])
+    eng.run_stream(pool, 0, 3)
     eng.fence()
     steps = 40
     a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     a.record(stream)
-    for i in range(steps):
-        eng.run_pipelined(pool[(i % slots) * b:(i % slots + 1) * b])
+    eng.run_stream(pool, 3, steps)
     eng.fence(stream)
     e.record(stream)
     torch.cuda.synchronize()
@@ -852,8 +987,9 @@ def uhd_leg(eb, dev, peaks) -> dict:
 
 
 def latency(eb, dev) -> dict:
-    """Single-frame (C1) latency: CUDA-graph replay of the one fused launch,
-    timed per replay with CUDA events; plus host wall time of estimate()."""
+    """Single-frame (C1 1080p) latency.  Device: CUDA-graph replay of the one
+    fused launch, CUDA events per replay.  Host: wall clock of the public
+    estimate() on a CUDA tensor and on a numpy frame (result on the host)."""
     import torch
     from support import synth
     from paper_2210_14771_b200.engine import ContentAreaEngine
@@ -864,7 +1000,6 @@ def latency(eb, dev) -> dict:
     stream = torch.cuda.current_stream(dev)
     for _ in range(50):
         eng.replay()
-    times = []
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(1000)]
     for a, b in evs:
         a.record(stream)
@@ -872,19 +1007,26 @@ def latency(eb, dev) -> dict:
         b.record(stream)
     torch.cuda.synchronize()
     times = sorted(a.elapsed_time(b) for a, b in evs)
-    host = []
-    for i in range(220):
-        w = time.perf_counter()
-        eb.estimate(frame)
-        if i >= 20:
-            host.append((time.perf_counter() - w) * 1e3)
-    host.sort()
     pct = lambda v, q: v[min(len(v) - 1, int(math.ceil(q * len(v))) - 1)]  # noqa: E731
-    return {"p50": round(pct(times, 0.50), 5), "p99": round(pct(times, 0.99), 5),
-            "mean": round(sum(times) / len(times), 5), "runs": len(times),
-            "method": "C1 1080p frame, CUDA graph replay of the fused launch, CUDA events per replay",
-            "host_api_p50": round(pct(host, 0.5), 4), "host_api_p99": round(pct(host, 0.99), 4),
-            "host_api_method": "estimate(numpy frame): strip-row H2D + launch + D2H, wall clock"}
+    out = {"p50": round(pct(times, 0.50), 5), "p99": round(pct(times, 0.99), 5),
+           "mean": round(sum(times) / len(times), 5), "runs": len(times),
+           "method": "C1 1080p frame, CUDA graph replay of the fused launch, CUDA events per replay"}
+    t3 = t[0]
+    for name, src in (("cuda", t3), ("numpy", frame)):
+        for _ in range(50):
+            eb.estimate(src)
+        host = []
+        for _ in range(1000):
+            w = time.perf_counter()
+            eb.estimate(src)
+            host.append((time.perf_counter() - w) * 1e3)
+        host.sort()
+        out[f"api_{name}_p50"] = round(pct(host, 0.5), 4)
+        out[f"api_{name}_p99"] = round(pct(host, 0.99), 4)
+    out["api_method"] = ("wall clock of eb.estimate(frame) -> ContentArea on the host, 1000 calls: a (H,W,3) "
+                         "CUDA tensor, and a numpy frame (strip rows staged in pinned memory, read by the kernel "
+                         "over PCIe)")
+    return out
 
 
 def main():

@@ -183,6 +183,15 @@ int eca_pipeline_create(int batch, int height, int width, const int32_t* strip_r
 int eca_pipeline_step(EcaPipeline* pipeline, const uint8_t* frames, int64_t frame_stride,
                       int64_t row_stride, int flags, EcaFitRecord* host_records, void* stream,
                       EcaFitRecord** out_records);
+/* n_steps eca_pipeline_step calls in one native call (a host-light stream
+ * loop): step j takes the batch at pool + ((first_slot + j) % n_slots) *
+ * batch_stride.  Records: eca_pipeline_records. */
+int eca_pipeline_run(EcaPipeline* pipeline, const uint8_t* pool, int64_t batch_stride, int n_slots,
+                     int first_slot, int n_steps, int64_t frame_stride, int64_t row_stride,
+                     int flags, void* stream);
+/* The device records of the step `back` steps before the latest one
+ * (0 <= back < 4 and < the steps so far). */
+int eca_pipeline_records(EcaPipeline* pipeline, int back, EcaFitRecord** out_records);
 /* Kept for API stability: steps carry no host-side history (a no-op). */
 int eca_pipeline_reset(EcaPipeline* pipeline);
 /* Make `stream` wait for every step enqueued so far. */

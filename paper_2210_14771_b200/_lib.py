@@ -45,6 +45,8 @@ SIGNATURES = {
                             _p, _i64, ctypes.POINTER(ctypes.c_void_p)],
     "eca_pipeline_step": [_p, _p, _i64, _i64, ctypes.c_int, _p, _p, ctypes.POINTER(ctypes.c_void_p)],
     "eca_pipeline_fence": [_p, _p],
+    "eca_pipeline_run": [_p, _p, _i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_int, _p],
+    "eca_pipeline_records": [_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)],
     "eca_pipeline_reset": [_p],
     "eca_pipeline_side_stream": [_p, ctypes.POINTER(ctypes.c_void_p)],
     "eca_pipeline_destroy": [_p],

@@ -857,6 +857,27 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   return ECA_OK;
 }
 
+extern "C" int eca_pipeline_run(EcaPipeline* P, const uint8_t* pool, int64_t batch_stride,
+                                int n_slots, int first_slot, int n_steps, int64_t frame_stride,
+                                int64_t row_stride, int flags, void* stream) {
+  if (!P || !pool || n_slots < 1 || first_slot < 0 || n_steps < 0 || batch_stride < 0)
+    return ECA_ERR_ARG;
+  EcaFitRecord* out = nullptr;
+  for (int j = 0; j < n_steps; ++j) {
+    const int slot = int((int64_t(first_slot) + j) % n_slots);
+    const int rc = eca_pipeline_step(P, pool + slot * batch_stride, frame_stride, row_stride, flags,
+                                     nullptr, stream, &out);
+    if (rc) return rc;
+  }
+  return ECA_OK;
+}
+
+extern "C" int eca_pipeline_records(EcaPipeline* P, int back, EcaFitRecord** out_records) {
+  if (!P || !out_records || back < 0 || back >= kPipeSets || back >= P->step) return ECA_ERR_ARG;
+  *out_records = P->rec[(P->step - 1 - back) % kPipeSets];
+  return ECA_OK;
+}
+
 extern "C" int eca_pipeline_reset(EcaPipeline* P) {
   // the device-side claim / done counters keep counting, so a graph captured
   // after eager steps replays safely

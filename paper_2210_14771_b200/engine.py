@@ -71,7 +71,8 @@ class ContentAreaEngine:
         if isinstance(variant, api.Learned):
             self.launches_per_run = 3          # CNN, candidate select, fit
         else:
-            self.launches_per_run = 1
+            self.launches_per_run = 1 if self.fused else 2   # fused | bounds, fit
+        self.launches_per_step = self.launches_per_run   # run_pipelined: bounds + fit launches
 
     FUSED_MAX_BATCH = 16
 
@@ -194,11 +195,41 @@ class ContentAreaEngine:
         _lib.check(p["step"](p["handle"], ctypes.c_void_p(f.data_ptr()), f.stride(0), f.stride(1), flags,
                              extra, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream),
                              ctypes.byref(out)), "eca_pipeline_step")
-        rec = p["views"].get(out.value)
+        return self._record_view(p, out.value)
+
+    def run_stream(self, pool: torch.Tensor, first: int, steps: int, frames_ready: bool = True) -> list:
+        """``steps`` run_pipelined calls in ONE native call (eca_pipeline_run):
+        step j takes batch ((first + j) % n_batches) of ``pool``, a (n_batches *
+        B, H, W, 3) device tensor.  Returns the record tensors of the last
+        min(steps, PIPE_SETS) steps, oldest first (complete in current-stream
+        order; valid until PIPE_SETS further steps)."""
+        if isinstance(self.variant, api.Learned) or self.fused:
+            raise ValueError("run_stream streams the handcrafted variant at batch > 16")
+        if pool.dim() != 4 or pool.shape[0] % self.batch or tuple(pool.shape[1:]) != \
+                (self.height, self.width, 3) or pool.dtype != torch.uint8 or not pool.is_contiguous():
+            raise ValueError("pool must be a contiguous (n * B, H, W, 3) uint8 tensor")
+        if pool.device != self.device:
+            raise ValueError(f"pool must live on {self.device}")
+        p = self._pipeline()
+        lib = _lib.load()
+        flags = _lib.PIPE_FRAMES_READY if frames_ready else 0
+        _lib.check(lib.eca_pipeline_run(p["handle"], ctypes.c_void_p(pool.data_ptr()),
+                                        self.batch * pool.stride(0), pool.shape[0] // self.batch, first,
+                                        steps, pool.stride(0), pool.stride(1), flags,
+                                        ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)),
+                   "eca_pipeline_run")
+        recs = []
+        for back in range(min(steps, self.PIPE_SETS) - 1, -1, -1):
+            _lib.check(lib.eca_pipeline_records(p["handle"], back, ctypes.byref(p["out"])), "eca_pipeline_records")
+            recs.append(self._record_view(p, p["out"].value))
+        return recs
+
+    def _record_view(self, p, ptr: int) -> torch.Tensor:
+        rec = p["views"].get(ptr)
         if rec is None:   # a view of this buffer set's records inside the scratch
-            off = out.value - p["base"]
+            off = ptr - p["base"]
             rec = p["scratch"][off:off + self.batch * 40].view(torch.float64).view(self.batch, 5)
-            p["views"][out.value] = rec
+            p["views"][ptr] = rec
         return rec
 
     def run_host_pipelined(self, host_frames: torch.Tensor, host_records: torch.Tensor) -> None:
@@ -342,6 +373,16 @@ class ContentAreaEngine:
             "eca_estimate_batch_handcrafted")
         torch.cuda.current_stream(self.device).synchronize()
         return self.rec_host
+
+    def pipeline_zero_copy_bytes(self) -> int:
+        """Bytes the pipelined bound-and-prune launches fetched over PCIe in
+        zero-copy mode so far (every buffer set's counter)."""
+        if self._pipe is None:
+            return 0
+        sc = self._pipe["scratch"]
+        per_set = sc.numel() // self.PIPE_SETS
+        return int(sum(int(sc[k * per_set + 8:k * per_set + 12].view(torch.int32).item())
+                       for k in range(self.PIPE_SETS))) * 16
 
     def zero_copy_bytes(self) -> int:
         """Bytes fetched over PCIe by run_host_zero_copy() calls so far."""

@@ -46,7 +46,7 @@ def assemble(parts: torch.Tensor, n_frames: int, world: int) -> torch.Tensor:
 def gather_records(local: torch.Tensor, n_frames: int, group=None) -> torch.Tensor:
     """All-gather per-rank (n_local, 5) float64 record blocks into the full
     (n_frames, 5) table in frame order (every rank receives it)."""
-    world = dist.get_world_size(group)
+    world = _rank_world(group)[1]
     if local.dim() != 2 or local.shape[1] != RECORD_DOUBLES or local.dtype != torch.float64:
         raise ValueError("records must be (n, 5) float64 EcaFitRecord rows")
     cap = shard_capacity(n_frames, world)
@@ -55,8 +55,17 @@ def gather_records(local: torch.Tensor, n_frames: int, group=None) -> torch.Tens
     return assemble(_all_gather(send, world, group), n_frames, world)
 
 
+def _rank_world(group=None) -> tuple[int, int]:
+    """(rank, world) of the group; a single process without a process group is (0, 1)."""
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
 def _all_gather(send: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """(rows, 5) from every rank -> (world, rows, 5)."""
+    if world == 1 and not dist.is_initialized():
+        return send.unsqueeze(0).clone()
     if dist.get_backend(group) == "nccl":
         out = torch.empty((world * send.shape[0], RECORD_DOUBLES), dtype=send.dtype, device=send.device)
         dist.all_gather_into_tensor(out, send, group=group)
@@ -87,7 +96,7 @@ class ShardedEstimator:
                  device=None, chunk: int = 256, gather_every: int = 32,
                  engine_factory: Callable | None = None, group=None):
         self.group = group
-        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.rank, self.world = _rank_world(group)
         self.n_frames = n_frames
         self.start, self.stop = shard_range(n_frames, self.rank, self.world)
         self.n_local = self.stop - self.start
@@ -109,7 +118,7 @@ class ShardedEstimator:
             self.device = torch.device(device)
         else:   # an empty shard still joins the collectives
             self.device = torch.device("cuda", torch.cuda.current_device()) \
-                if dist.get_backend(group) == "nccl" else torch.device("cpu")
+                if dist.is_initialized() and dist.get_backend(group) == "nccl" else torch.device("cpu")
         self.send = torch.zeros((self.cap, RECORD_DOUBLES), dtype=torch.float64, device=self.device)
         self.cuda = self.device.type == "cuda"
         self.gather_stream = torch.cuda.Stream(self.device) if self.cuda else None

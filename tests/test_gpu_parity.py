@@ -628,3 +628,20 @@ if given is not None:
         got = eb.ransac_fit(cands, (w, h), cfg, seed % 1000, exhaustive=exhaustive)
         want = orc.ransac(pts[:, 0], pts[:, 1], scores, w, h, cfg, seed % 1000, exhaustive=exhaustive)
         assert_fit_equal(got, want, (w, h, cx, cy, r, n_in, n_out, seed))
+
+
+def test_run_stream_matches_run():
+    """eca_pipeline_run (K steps in one native call over a pool of batches)
+    gives run()'s records for the last PIPE_SETS steps."""
+    specs = synth.bench_specs(40, 960, 540, seed=2024)
+    frames = torch.from_numpy(np.stack([synth.render(s, 32000 + k)
+                                        for k, (_, s) in enumerate(specs)])).cuda()
+    B = 20
+    pool = frames[[k % 40 for k in range(3 * B)]].contiguous()
+    eng = eb.ContentAreaEngine(540, 960, B)
+    want = [eng.run(pool[k * B:(k + 1) * B]).clone() for k in range(3)]
+    recs = eng.run_stream(pool, first=1, steps=11)
+    torch.cuda.synchronize()
+    assert len(recs) == eng.PIPE_SETS
+    for j, r in zip(range(11 - eng.PIPE_SETS, 11), recs):
+        assert torch.equal(r, want[(1 + j) % 3]), j

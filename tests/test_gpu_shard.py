@@ -50,3 +50,19 @@ def test_gather_records_nccl(nccl_world1):
     rec = torch.arange(35, dtype=torch.float64, device="cuda").view(7, 5)
     out = gather_records(rec, 7)
     assert torch.equal(out, rec)
+
+
+def test_sharded_estimator_pipelined_chunks(nccl_world1):
+    """Batches of 32 through the pipeline (two launches per batch, records
+    written by the fit kernel into the send buffer, gathers every 2 batches
+    on the side stream) plus a fused ragged tail, vs one batched estimate."""
+    specs = synth.bench_specs(20, 640, 480, seed=8)
+    base = torch.from_numpy(np.stack([synth.render(s, 600 + k) for k, (_, s) in enumerate(specs)])).cuda()
+    frames = base[[k % 20 for k in range(100)]].contiguous()
+    se = ShardedEstimator(100, 480, 640, chunk=32, gather_every=2)
+    assert not se.engine.fused and se.tail_engine.fused
+    got = se.run(lambda a, b: frames[a:b], frames_ready=True)
+    want = eb.ContentAreaEngine(480, 640, 100).run(frames)
+    torch.cuda.synchronize()
+    assert se.gathers == 2
+    assert torch.equal(got, want)
