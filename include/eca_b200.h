@@ -229,9 +229,13 @@ int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const double* cand_sco
             int batch, int n_cand, const EcaParams* params, const int16_t* triplets,
             int exhaustive, EcaFitRecord* out, void* stream);
 
-/* estimate() for a batch in ONE launch (estimator.py:55-74): strip scoring,
- * candidates, filter, RANSAC.  `counters` = batch int32 zeros (left zeroed on
- * return).  The candidate outputs double as the fitter's input staging. */
+/* estimate() for a small batch (the latency path; estimator.py:55-74): strip
+ * scoring with the survivors rescored in FP64 by the same warp, candidates,
+ * then filter + RANSAC in a fit kernel launched programmatically behind it.
+ * `counters` = max(batch, 64) int32 zeros (scratch: left zeroed on return).
+ * The candidate outputs double as the fitter's input.  (ECA_LATENCY_STRIP=1
+ * in the environment: the older single launch, a block-per-strip kernel
+ * whose last CTA per frame fits it.) */
 int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                              int64_t row_stride, const int32_t* strip_rows,
                              const int32_t* band_rows, int n_strips,

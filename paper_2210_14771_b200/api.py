@@ -584,7 +584,7 @@ class _FrameEstimator:
         self.p_params = ctypes.byref(self.params)
         with _on(device):
             self.trip = _dev_triplets(seed, cfg.ransac_attempts, 2 * s, device)
-            self.cnt = torch.zeros(1, dtype=torch.int32, device=device)
+            self.cnt = torch.zeros(64, dtype=torch.int32, device=device)
             self.xs = torch.empty((1, 2 * s), dtype=torch.int32, device=device)
             self.ys = torch.empty_like(self.xs)
             self.sc = torch.empty((1, 2 * s), dtype=torch.float64, device=device)
@@ -599,24 +599,30 @@ class _FrameEstimator:
         self.lock = threading.Lock()
 
     def __call__(self, frame) -> ContentArea:
+        if torch.cuda.current_device() == self.dev.index:   # (the device switch costs microseconds)
+            with self.lock:
+                return self._run(frame)
         with self.lock, _on(self.dev):
-            if isinstance(frame, torch.Tensor) and frame.is_cuda:
-                t = frame if frame.device == self.dev else frame.to(self.dev)
-                if t.stride(2) != 1 or t.stride(1) != 3 or t.stride(0) < 3 * self.w:
-                    t = t.contiguous()
-                ptr, rs, band = ctypes.c_void_p(t.data_ptr()), t.stride(0), None
-            else:
-                a = frame.numpy() if isinstance(frame, torch.Tensor) else frame
-                np.take(a, self.row_idx, axis=0, out=self.bands_np)
-                ptr, rs, band = ctypes.c_void_p(self.bands_host.data_ptr()), 3 * self.w, self.c_band
-            stream = torch.cuda.current_stream(self.dev)
-            _lib.check(self.fn(ptr, 1, 0, rs, self.c_rows, band, self.s, self.p_params, *self.args,
-                               ctypes.c_void_p(stream.cuda_stream)), "eca_estimate_handcrafted")
-            stream.synchronize()
-            r = self.rec_np[0]
-            if int(r.view(np.int32)[9]) == _lib.ACCEPTED:
-                return CircularArea(Circle(float(r[0]), float(r[1]), float(r[2])), float(r[3]))
-            return FULL_FRAME
+            return self._run(frame)
+
+    def _run(self, frame) -> ContentArea:
+        if isinstance(frame, torch.Tensor) and frame.is_cuda:
+            t = frame if frame.device == self.dev else frame.to(self.dev)
+            if t.stride(2) != 1 or t.stride(1) != 3 or t.stride(0) < 3 * self.w:
+                t = t.contiguous()
+            ptr, rs, band = ctypes.c_void_p(t.data_ptr()), t.stride(0), None
+        else:
+            a = frame.numpy() if isinstance(frame, torch.Tensor) else frame
+            np.take(a, self.row_idx, axis=0, out=self.bands_np)
+            ptr, rs, band = ctypes.c_void_p(self.bands_host.data_ptr()), 3 * self.w, self.c_band
+        stream = torch.cuda.current_stream(self.dev)
+        _lib.check(self.fn(ptr, 1, 0, rs, self.c_rows, band, self.s, self.p_params, *self.args,
+                           ctypes.c_void_p(stream.cuda_stream)), "eca_estimate_handcrafted")
+        stream.synchronize()
+        r = self.rec_np[0]
+        if int(r.view(np.int32)[9]) == _lib.ACCEPTED:
+            return CircularArea(Circle(float(r[0]), float(r[1]), float(r[2])), float(r[3]))
+        return FULL_FRAME
 
 
 _FRAME_ESTIMATORS: dict = {}
@@ -636,12 +642,17 @@ def estimate(frame, variant: EstimatorVariant = HANDCRAFTED, cfg: EcaConfig | No
     if seed < 0:
         raise ValueError("expected non-negative integer seed")
     _check_config(cfg)
-    if device is None and isinstance(frame, torch.Tensor) and frame.is_cuda:
-        device = frame.device
-    dev = _device(device)
-    key = (height, width, cfg, seed, dev)
+    if device is None:   # the frame's device, else the current one
+        if isinstance(frame, torch.Tensor) and frame.is_cuda:
+            device = frame.device.index
+        else:
+            if not torch.cuda.is_available():
+                _device(None)   # raises: no GPU, no CPU fallback
+            device = torch.cuda.current_device()
+    key = (height, width, cfg, seed, device)
     est = _FRAME_ESTIMATORS.get(key)
     if est is None:
+        dev = _device(device if not isinstance(device, int) else torch.device("cuda", device))
         if len(_FRAME_ESTIMATORS) > 32:
             _FRAME_ESTIMATORS.clear()
         est = _FRAME_ESTIMATORS[key] = _FrameEstimator(height, width, cfg, seed, dev)

@@ -56,6 +56,11 @@ bool smem_optin(K kern, int bytes = 227 * 1024) {
 
 int check_launch() { return cudaGetLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA; }
 
+bool getenv_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && std::atoi(v) != 0;
+}
+
 bool tracing() {
   static const bool on = std::getenv("ECA_TRACE") != nullptr;
   return on;
@@ -138,9 +143,9 @@ int64_t points_workspace(int batch, int n_strips) {
   return 256 + slots_bytes(n_hr) + n_hr * 4;
 }
 
-template <int NS, bool kChunked>
+template <int NS, bool kChunked, bool kInWarp = false>
 int launch_points_t(PointsJob PJ, cudaStream_t stream, bool overlap, bool share) {
-  auto kern = bounds_kernel<NS, kChunked>;
+  auto kern = bounds_kernel<NS, kChunked, kInWarp>;
   StripJob& J = PJ.J;
   const int W = J.p.width;
   const int split = (W + 1) / 2;
@@ -682,13 +687,37 @@ extern "C" int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_
   if (rc) return rc;
   if (!triplets || !counters || !out || !out_x || !out_y || !out_score) return ECA_ERR_ARG;
   if (check_fit_params(params)) return ECA_ERR_ARG;
+  if (batch == 0) return ECA_OK;
   J.out_x = out_x;
   J.out_y = out_y;
   J.out_score = out_score;
+  cudaStream_t st = as_stream(stream);
+  if (!getenv_flag("ECA_LATENCY_STRIP")) {
+    // warp per half row, survivors rescored in the same warp (candidates
+    // out), then the fit kernel as a programmatic dependent launch: its CTAs
+    // are resident before the candidates are done.  `counters` is the item
+    // ticket block (>= 64 int32, left zeroed).
+    PointsJob PJ = points_job(J, counters);
+    rc = launch_points_t<1, false, true>(PJ, st, false, false);
+    if (rc) return rc;
+    FitJob F;
+    std::memset(&F, 0, sizeof(F));
+    F.x = out_x;
+    F.y = out_y;
+    F.s = out_score;
+    F.n_cand = 2 * n_strips;
+    F.p = J.p;
+    F.trip = triplets;
+    F.out = out;
+    F.wait_prev = 1;
+    return launch_fit(F, batch, st, /*overlap=*/true);
+  }
+  // one launch: the block-per-strip kernel whose last CTA per frame fits it
+  // (`counters`: batch int32 zeros)
   J.triplets = triplets;
   J.counters = counters;
   J.out_fit = out;
-  return launch_strips<false, true>(J, as_stream(stream));
+  return launch_strips<false, true>(J, st);
 }
 
 extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_stride,

@@ -198,7 +198,9 @@ ECA_DEV bool guard_release(int32_t* ticket, int units) {
 #endif
 // kChunked: zero-copy mode (ECA_BOUNDS_ZERO_COPY), a separate instantiation so
 // the device-resident kernel carries none of its code
-template <int NS, bool kChunked>
+// kInWarp (small batches, the latency path): each warp also rescoring its
+// half row's survivors in FP64 and writing the candidate (no survivor slots)
+template <int NS, bool kChunked, bool kInWarp = false>
 __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_constant__ PointsJob PJ) {
   const StripJob& J = PJ.J;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -666,7 +668,34 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     // kernel's rescore stage); resolve the half row here if it has more than
     // kSlots.  The next item's TMA starts as soon as the stage is read.
     const int hrow = item;
-    if (!flushed && n_list <= kSlots) {
+    if (kInWarp && !flushed && n_list <= kSlots) {
+      // one lane per survivor: the 3x3 sums to registers, refill the stage,
+      // then the FP64 score under the next item's TMA
+      int sx = 0, spre = 0, sl[3] = {0, 0, 0}, sm[3] = {0, 0, 0}, sr[3] = {0, 0, 0};
+      if (lane < n_list) {
+        const uint32_t v = list[lane];
+        sx = int(v & 0xffffu);
+        spre = int(v >> 16);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          sl[r] = px_sum(st, rb[r] + 3 * (sx - 1));
+          sm[r] = px_sum(st, rb[r] + 3 * sx);
+          sr[r] = px_sum(st, rb[r] + 3 * (sx + 1));
+        }
+      }
+      advance();
+      if (lane < n_list) {
+        const double sc = exact_score(sl, sm, sr, spre, sx, y, cxf, cyf, J.p);
+        if (better(sc, sx, best.s, best.x, !half)) best = Best{sc, sx};
+      }
+      best = warp_best(best, !half);
+      if (lane == 0) {
+        const size_t slot = size_t(frame) * 2 * S + (half ? S : 0) + strip;
+        J.out_x[slot] = best.x;
+        J.out_y[slot] = y;
+        J.out_score[slot] = best.s;
+      }
+    } else if (!flushed && n_list <= kSlots) {
       if (lane < n_list) {
         const uint32_t v = list[lane];
         const int x = int(v & 0xffffu);
@@ -693,7 +722,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
         J.out_x[slot] = best.x;
         J.out_y[slot] = y;
         J.out_score[slot] = best.s;
-        PJ.counts[hrow] = -1;
+        if (!kInWarp) PJ.counts[hrow] = -1;
       }
     }
 #endif

@@ -44,7 +44,7 @@ class ContentAreaEngine:
         self.params = self.cfg.device_params(width, height)
         d = self.device
         self.trip = api._dev_triplets(seed, self.cfg.ransac_attempts, 2 * s, d)
-        self.counters = torch.zeros(batch, dtype=torch.int32, device=d)
+        self.counters = torch.zeros(max(batch, 64), dtype=torch.int32, device=d)
         self.xs = torch.empty((batch, 2 * s), dtype=torch.int32, device=d)
         self.ys = torch.empty_like(self.xs)
         self.sc = torch.empty((batch, 2 * s), dtype=torch.float64, device=d)
