@@ -408,6 +408,7 @@ ECA_DEV void rescore_frame(const FitJob& J, int b, uint8_t* smem) {
       if (lane >= d) incl += v;
     }
     const int off = base + incl - n;
+    ECA_CHECK(n <= kSlots && off + n <= nc * kSlots);
     for (int k = 0; k < n; ++k) ent[off + k] = uint16_t((hk << 3) | k);
     if (hk < nc) {
       cx[hk] = off;   // parked until the winners are taken

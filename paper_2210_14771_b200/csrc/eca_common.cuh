@@ -9,6 +9,22 @@
 
 #define ECA_DEV __device__ __forceinline__
 
+// ECA_CHECKED builds (tools/checked.sh): device-side bounds checks at the
+// kernels' computed indices; a violation traps (the launch fails with an
+// error) instead of corrupting memory silently.  compute-sanitizer is not
+// available on the GPU pool, so this plus tests/test_gpu_guard.py (canary
+// zones, launch-shape determinism) stands in for memcheck / racecheck.
+#ifdef ECA_CHECKED
+#define ECA_CHECK(cond)        \
+  do {                         \
+    if (!(cond)) __trap();     \
+  } while (0)
+#else
+#define ECA_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace eca {
 
 // ---------------------------------------------------------------- smem / TMA

@@ -263,6 +263,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
       q.yy = mul_rn(q.y, q.y);
       q.xz = mul_rn(q.x, q.z);
       q.yz = mul_rn(q.y, q.z);
+      ECA_CHECK(pos < n_cand);
       pt[pos] = q;
       ps[pos] = s;
     }
@@ -292,6 +293,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
         i1 = t[1];
         i2 = t[2];
       }
+      ECA_CHECK(i0 >= 0 && i0 < n && i1 >= 0 && i1 < n && i2 >= 0 && i2 < n);
       c = circumcircle(pt[i0].x, pt[i0].y, pt[i1].x, pt[i1].y, pt[i2].x,
                        pt[i2].y);
     }

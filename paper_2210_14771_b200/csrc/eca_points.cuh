@@ -405,6 +405,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
         __syncwarp();
         if (keep) {
           const int pos = out + __popc(bm & lt_mask);
+          ECA_CHECK(pos < kWListCap);
           list[pos] = v;
           ulist[pos] = u;
         }
@@ -424,6 +425,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
       if (n_list + tot > kWListCap) flush();
       if (surv) {
         const int pos = n_list + __popc(bm & lt_mask);
+        ECA_CHECK(pos < kWListCap && ce.x >= lo && ce.x <= hi);
         list[pos] = uint32_t(ce.x) | (uint32_t(ce.pre) << 16);
         ulist[pos] = ce.U;
       }
@@ -523,6 +525,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
       float u = 0.0f;
       if (qmax > 0)
         u = fminf(t_term(qmax, tk) * hi_f, 1.0f) * fminf(d_term(ex, tk) * hi_f, 1.0f);
+      ECA_CHECK(k < kWMaxChunks);
       ut_s[k * 32 + lane] = __float2half_ru(u);
       ex_s[k * 32 + lane] = uint16_t(ex);
       // every later column has preceding sum >= carry, so its score is below
@@ -576,6 +579,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
           }
         }
         const unsigned bm = __ballot_sync(kFull, s);
+        ECA_CHECK(n_sel + __popc(bm) <= kWMaxChunks * 32);
         if (s) sel_s[n_sel + __popc(bm & lt_mask)] = uint16_t((k << 5) | lane);
         n_sel += __popc(bm);
       }
@@ -709,6 +713,7 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
           sl.r[r] = uint16_t(px_sum(st, rb[r] + 3 * (x + 1)));
         }
         sl.pad = 0;
+        ECA_CHECK(hrow < n_items && lane < kSlots && x >= slo && x <= shi);
         PJ.slots[size_t(hrow) * kSlots + lane] = sl;
       }
       if (lane == 0) PJ.counts[hrow] = n_list;
