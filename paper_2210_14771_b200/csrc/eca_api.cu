@@ -554,6 +554,7 @@ extern "C" int eca_points_handcrafted(const uint8_t* frames, int batch, int64_t 
                                       const int32_t* band_rows, int n_strips,
                                       const EcaParams* params, int32_t* out_x, int32_t* out_y,
                                       double* out_score, void* workspace, void* stream) {
+  ECA_RANGE("eca_points_handcrafted");
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
                              n_strips, params);
@@ -572,6 +573,7 @@ extern "C" int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t 
                                       const EcaParams* params, int32_t* out_x, int32_t* out_y,
                                       double* out_score, void* workspace, int flags,
                                       void* stream) {
+  ECA_RANGE("eca_bounds_handcrafted");
   if (flags & ~(ECA_BOUNDS_OVERLAP_PREVIOUS | ECA_BOUNDS_SHARE_SMS | ECA_BOUNDS_ZERO_COPY))
     return ECA_ERR_ARG;
   StripJob J;
@@ -589,6 +591,7 @@ extern "C" int eca_bounds_handcrafted(const uint8_t* frames, int batch, int64_t 
 extern "C" int eca_rescore_handcrafted(int batch, const int32_t* strip_rows, int n_strips,
                                        const EcaParams* params, int32_t* out_x, int32_t* out_y,
                                        double* out_score, void* workspace, void* stream) {
+  ECA_RANGE("eca_rescore_handcrafted");
   if (!strip_rows || !params || !out_x || !out_y || !out_score || !workspace || batch < 0)
     return ECA_ERR_ARG;
   if (n_strips < 1 || n_strips > ECA_MAX_STRIPS) return ECA_ERR_UNSUPPORTED;
@@ -613,6 +616,7 @@ extern "C" int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int6
                                           const EcaParams* params, double* out_scores,
                                           int32_t* out_x, int32_t* out_y, double* out_score,
                                           void* stream) {
+  ECA_RANGE("eca_score_rows_handcrafted");
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
                              n_strips, params);
@@ -659,6 +663,7 @@ int launch_fit(const FitJob& J, int batch, cudaStream_t stream, bool overlap = f
 extern "C" int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const double* cand_score,
                        int batch, int n_cand, const EcaParams* params, const int16_t* triplets,
                        int exhaustive, EcaFitRecord* out, void* stream) {
+  ECA_RANGE("eca_fit");
   if (batch < 0 || n_cand < 0 || n_cand > 2 * ECA_MAX_STRIPS || !params) return ECA_ERR_ARG;
   if (batch == 0) return ECA_OK;
   if (!cand_x || !cand_y || !cand_score || !out || (!exhaustive && !triplets)) return ECA_ERR_ARG;
@@ -682,6 +687,7 @@ extern "C" int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_
                                         const EcaParams* params, const int16_t* triplets,
                                         int32_t* counters, int32_t* out_x, int32_t* out_y,
                                         double* out_score, EcaFitRecord* out, void* stream) {
+  ECA_RANGE("eca_estimate_handcrafted");
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
                              n_strips, params);
@@ -724,6 +730,7 @@ extern "C" int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_
 extern "C" int eca_h2d_bands(const uint8_t* host, int batch, int64_t host_frame_stride,
                              int64_t host_row_stride, const int32_t* first_rows, int n_bands,
                              int rows_per_band, int width, uint8_t* dev, void* stream) {
+  ECA_RANGE("eca_h2d_bands");
   if (batch < 0 || n_bands < 0 || rows_per_band < 1 || width < 1) return ECA_ERR_ARG;
   if (batch == 0 || n_bands == 0) return ECA_OK;
   if (!host || !first_rows || !dev || host_row_stride < 3LL * width) return ECA_ERR_ARG;
@@ -805,6 +812,7 @@ extern "C" int eca_pipeline_bytes(int batch, int n_strips, int64_t* out_bytes) {
 extern "C" int eca_pipeline_create(int batch, int height, int width, const int32_t* strip_rows,
                                    int n_strips, const EcaParams* params, const int16_t* triplets,
                                    void* scratch, int64_t scratch_bytes, EcaPipeline** out) {
+  ECA_RANGE("eca_pipeline_create");
   if (!out || !scratch || !triplets || batch < 1) return ECA_ERR_ARG;
   *out = nullptr;
   if (!params || params->width != width || params->height != height) return ECA_ERR_ARG;
@@ -848,6 +856,7 @@ extern "C" int eca_pipeline_create(int batch, int height, int width, const int32
 extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t frame_stride,
                                  int64_t row_stride, int flags, EcaFitRecord* host_records,
                                  void* stream, EcaFitRecord** out_records) {
+  ECA_RANGE("eca_pipeline_step");
   if (!P || !frames || !out_records || row_stride < 3LL * P->J.p.width || frame_stride < 0)
     return ECA_ERR_ARG;
   if (flags & ~(ECA_BOUNDS_ZERO_COPY | ECA_PIPE_FRAMES_READY)) return ECA_ERR_ARG;
@@ -890,6 +899,7 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
 extern "C" int eca_pipeline_run(EcaPipeline* P, const uint8_t* pool, int64_t batch_stride,
                                 int n_slots, int first_slot, int n_steps, int64_t frame_stride,
                                 int64_t row_stride, int flags, void* stream) {
+  ECA_RANGE("eca_pipeline_run");
   if (!P || !pool || n_slots < 1 || first_slot < 0 || n_steps < 0 || batch_stride < 0)
     return ECA_ERR_ARG;
   EcaFitRecord* out = nullptr;
@@ -916,6 +926,7 @@ extern "C" int eca_pipeline_reset(EcaPipeline* P) {
 }
 
 extern "C" int eca_pipeline_fence(EcaPipeline* P, void* stream) {
+  ECA_RANGE("eca_pipeline_fence");
   if (!P) return ECA_ERR_ARG;
   if (P->last < 0) return ECA_OK;
   cudaStream_t st = as_stream(stream);
@@ -933,6 +944,7 @@ extern "C" int eca_pipeline_side_stream(EcaPipeline* P, void** out_stream) {
 }
 
 extern "C" int eca_pipeline_destroy(EcaPipeline* P) {
+  ECA_RANGE("eca_pipeline_destroy");
   if (!P) return ECA_OK;
   if (P->last_stream || P->last >= 0) cudaStreamSynchronize(P->last_stream);
   cudaEventDestroy(P->ev_fence);
@@ -948,6 +960,7 @@ extern "C" int eca_estimate_batch_handcrafted(const uint8_t* frames, int batch,
                                               int32_t* out_x, int32_t* out_y, double* out_score,
                                               EcaFitRecord* out, EcaFitRecord* host_out,
                                               int flags, void* stream) {
+  ECA_RANGE("eca_estimate_batch_handcrafted");
   if (flags & ~(ECA_BOUNDS_ZERO_COPY | ECA_PIPE_FRAMES_READY)) return ECA_ERR_ARG;
   StripJob J;
   int rc = prepare_strip_job(J, frames, batch, frame_stride, row_stride, strip_rows, band_rows,
@@ -1056,6 +1069,7 @@ __global__ void selftest_tables(const EcaParams p, float pad, double* out) {
 }  // namespace
 
 extern "C" int eca_prefilter_selftest(const EcaParams* params, double* dev_out, void* stream) {
+  ECA_RANGE("eca_prefilter_selftest");
   if (!params || !dev_out) return ECA_ERR_ARG;
   static const uint8_t dummy[16] = {};
   const int32_t row = 3;

@@ -774,6 +774,7 @@ extern "C" int eca_points_learned_ex(const uint8_t* frames, int batch, int64_t f
                                      const float* weights, const double* norm, int flags,
                                      float* out_probs, int32_t* out_x, int32_t* out_y,
                                      double* out_score, void* stream) {
+  ECA_RANGE("eca_points_learned_ex");
   if ((flags & ~(ECA_LEARNED_TCGEN05 | ECA_LEARNED_SIMT)) ||
       (flags & (ECA_LEARNED_TCGEN05 | ECA_LEARNED_SIMT)) == (ECA_LEARNED_TCGEN05 | ECA_LEARNED_SIMT))
     return ECA_ERR_ARG;
@@ -847,6 +848,7 @@ extern "C" int eca_points_learned(const uint8_t* frames, int batch, int64_t fram
                                   int height, int width, const float* weights, const double* norm,
                                   float* out_probs, int32_t* out_x, int32_t* out_y,
                                   double* out_score, void* stream) {
+  ECA_RANGE("eca_points_learned");
   return eca_points_learned_ex(frames, batch, frame_stride, row_stride, strip_rows, band_rows,
                                n_strips, height, width, weights, norm, 0, out_probs, out_x, out_y,
                                out_score, stream);

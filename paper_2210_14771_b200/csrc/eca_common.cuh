@@ -9,6 +9,24 @@
 
 #define ECA_DEV __device__ __forceinline__
 
+// NVTX ranges around the C-ABI entry points (header-only NVTX3: a no-op
+// unless a tool such as nsys / ncu --nvtx is attached); one domain "eca".
+#include <nvtx3/nvToolsExt.h>
+struct EcaRange {
+  explicit EcaRange(const char* name) {
+    static nvtxDomainHandle_t dom = nvtxDomainCreateA("eca");
+    nvtxEventAttributes_t a = {};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    nvtxDomainRangePushEx(dom_ = dom, &a);
+  }
+  ~EcaRange() { nvtxDomainRangePop(dom_); }
+  nvtxDomainHandle_t dom_;
+};
+#define ECA_RANGE(name) EcaRange eca_range_(name)
+
 // ECA_CHECKED builds (tools/checked.sh): device-side bounds checks at the
 // kernels' computed indices; a violation traps (the launch fails with an
 // error) instead of corrupting memory silently.  compute-sanitizer is not

@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(256) crop_copy_kernel(const uint8_t* frames, i
 
 extern "C" int eca_draw_mask(const EcaFitRecord* fits, int batch, int height, int width,
                              uint8_t* out, int64_t out_frame_stride, void* stream) {
+  ECA_RANGE("eca_draw_mask");
   if (batch < 0 || height < 1 || width < 1 || out_frame_stride < int64_t(height) * width)
     return ECA_ERR_ARG;
   if (batch == 0) return ECA_OK;
@@ -213,6 +214,7 @@ extern "C" int eca_draw_mask(const EcaFitRecord* fits, int batch, int height, in
 
 extern "C" int eca_crop_bounds(const EcaFitRecord* fits, int batch, int height, int width,
                                int32_t* out_bounds, void* stream) {
+  ECA_RANGE("eca_crop_bounds");
   if (batch < 0 || height < 1 || width < 1) return ECA_ERR_ARG;
   if (batch == 0) return ECA_OK;
   if (!fits || !out_bounds) return ECA_ERR_ARG;
@@ -224,6 +226,7 @@ extern "C" int eca_crop_bounds(const EcaFitRecord* fits, int batch, int height, 
 extern "C" int eca_crop_copy(const uint8_t* frames, int batch, int64_t frame_stride,
                              int64_t row_stride, const int32_t* bounds, const int64_t* out_offsets,
                              uint8_t* out, int max_rows, void* stream) {
+  ECA_RANGE("eca_crop_copy");
   if (batch < 0 || max_rows < 0) return ECA_ERR_ARG;
   if (batch == 0 || max_rows == 0) return ECA_OK;
   if (!frames || !bounds || !out_offsets || !out) return ECA_ERR_ARG;
