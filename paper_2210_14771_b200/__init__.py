@@ -36,7 +36,7 @@ from .api import (
     validate_frame,
 )
 from .engine import ContentAreaEngine
-from .params import EcaConfig, apply_overrides, config_default, load_config, save_config
+from .params import EcaConfig, config_default
 from .shapes import (
     FULL_FRAME,
     Circle,

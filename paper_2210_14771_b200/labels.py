@@ -1,7 +1,8 @@
 """GPU pseudo-labelling: the paper's PseudoECA generator.
 
 Drop-in for ``eca.dataset.pseudo_label`` (dataset.py:190-225) and the
-annotation record it returns (dataset.py:36-60, CSV form :63-81).  The
+annotation record it returns (dataset.py:36-60; its CSV file form, :63-81,
+is host-side dataset tooling and out of scope).  The
 reference decodes and estimates one frame at a time; here worker processes
 decode the images and hand back only the strip rows the scorer reads, while
 the GPU estimates the previous chunk, and each chunk of same-sized frames is
@@ -12,8 +13,6 @@ with the same seed per frame, the same frame numbering, stride and skipping.
 
 from __future__ import annotations
 
-import csv
-import io
 import logging
 import os
 import multiprocessing as mp
@@ -33,8 +32,6 @@ from .shapes import Circle, CircularArea
 
 LOGGER = logging.getLogger("paper_2210_14771_b200.labels")
 IMAGE_EXTENSIONS = {".png", ".jpg", ".jpeg", ".bmp"}   # dataset.py:29
-CSV_FIELDS = ("sample_id", "source", "video_no", "frame_no", "area_type", "cx", "cy", "r",
-              "image_path")
 
 
 class Source(Enum):   # dataset.py:44-47
@@ -62,22 +59,6 @@ def load_image(path) -> np.ndarray:
 
 def save_image(frame: np.ndarray, path) -> None:
     Image.fromarray(frame, mode="RGB").save(path)
-
-
-def dumps_annotations(annotations) -> str:
-    """The reference's flat CSV (dataset.py:63-77)."""
-    buf = io.StringIO()
-    w = csv.writer(buf, lineterminator="\n")
-    w.writerow(CSV_FIELDS)
-    for a in annotations:
-        geo = ("full", "", "", "") if a.area is None else \
-            ("circle", repr(a.area.cx), repr(a.area.cy), repr(a.area.r))
-        w.writerow((a.sample_id, a.source.value, a.video_no, a.frame_no, *geo, a.image_path))
-    return buf.getvalue()
-
-
-def save_annotations(annotations, path) -> None:
-    Path(path).write_text(dumps_annotations(annotations), encoding="utf-8")
 
 
 def _decode_bands(args):
@@ -113,11 +94,16 @@ _POOL: dict = {}
 
 
 def _decode_pool(workers: int) -> ProcessPoolExecutor:
-    """The decode workers, started once per process and reused by later calls
-    (forking a large CUDA process costs more than decoding a few frames)."""
+    """The decode workers, started once per process and reused by later calls.
+    Forkserver, not fork: this process has CUDA and torch threads running, and
+    a fork would copy their locks; the server is a clean single-threaded
+    process that imports this module once, so workers start fast and never
+    initialise CUDA (they only decode and compute strip rows)."""
     pool = _POOL.get(workers)
     if pool is None:
-        pool = ProcessPoolExecutor(workers, mp_context=mp.get_context("fork"))
+        ctx = mp.get_context("forkserver")
+        ctx.set_forkserver_preload([__name__])
+        pool = ProcessPoolExecutor(workers, mp_context=ctx)
         _POOL[workers] = pool
     return pool
 

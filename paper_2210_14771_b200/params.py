@@ -9,10 +9,8 @@ kernel receives by value.
 from __future__ import annotations
 
 import ctypes
-import dataclasses
 import math
 from dataclasses import dataclass
-from pathlib import Path
 
 _POSITIVE = ("gradient_threshold", "angle_threshold_deg", "intensity_threshold",
              "min_point_score", "inlier_distance_px", "min_circle_score",
@@ -99,57 +97,3 @@ class EcaParams(ctypes.Structure):
 
 def config_default() -> EcaConfig:
     return EcaConfig()
-
-
-_TYPES = {f.name: f.type for f in dataclasses.fields(EcaConfig)}
-
-
-def _parse(name: str, text: str):
-    if name not in _TYPES:
-        raise ValueError(f"unknown config field {name!r}")
-    text = text.strip()
-    kind = _TYPES[name]
-    if kind == "bool":
-        low = text.lower()
-        if low in ("true", "1", "yes"):
-            return True
-        if low in ("false", "0", "no"):
-            return False
-        raise ValueError(f"bad boolean for {name}: {text!r}")
-    return int(text) if kind == "int" else float(text)
-
-
-def apply_overrides(cfg: EcaConfig, overrides: list[str]) -> EcaConfig:
-    """``name=value`` overrides (config.py:137-146)."""
-    vals = {}
-    for item in overrides:
-        if "=" not in item:
-            raise ValueError(f"override must look like name=value, got {item!r}")
-        k, _, v = item.partition("=")
-        vals[k.strip()] = _parse(k.strip(), v)
-    return dataclasses.replace(cfg, **vals)
-
-
-def save_config(cfg: EcaConfig, path) -> None:
-    """Flat ``name = value`` file; floats via repr so they round-trip exactly."""
-    lines = ["# content-area estimation parameters"]
-    for f in dataclasses.fields(EcaConfig):
-        v = getattr(cfg, f.name)
-        lines.append(f"{f.name} = {('true' if v else 'false') if isinstance(v, bool) else repr(v)}")
-    Path(path).write_text("\n".join(lines) + "\n", encoding="utf-8")
-
-
-def load_config(path, base: EcaConfig | None = None) -> EcaConfig:
-    vals = {}
-    for no, raw in enumerate(Path(path).read_text(encoding="utf-8").splitlines(), 1):
-        line = raw.split("#", 1)[0].strip()
-        if not line:
-            continue
-        if "=" not in line:
-            raise ValueError(f"line {no}: expected 'name = value', got {raw!r}")
-        k, _, v = line.partition("=")
-        try:
-            vals[k.strip()] = _parse(k.strip(), v)
-        except ValueError as exc:
-            raise ValueError(f"line {no}: {exc}") from None
-    return dataclasses.replace(base or config_default(), **vals)

@@ -54,10 +54,3 @@ def test_pseudo_label_matches_reference(frame_dir, case, chunk, caplog):
         assert (a.area is None) == (area is None), (a, area)
         if area is not None:
             assert np.abs(np.array([a.area.cx, a.area.cy, a.area.r]) - area).max() <= 1e-3
-    rows = [r.split(",") for r in labels.dumps_annotations(got).splitlines()]
-    ref = [r.split(",") for r in want["csv"].splitlines()]
-    assert rows[0] == ref[0] and len(rows) == len(ref)
-    for r, q in zip(rows[1:], ref[1:]):
-        assert r[:5] + r[8:] == q[:5] + q[8:]
-        if r[4] == "circle":
-            assert max(abs(float(x) - float(y)) for x, y in zip(r[5:8], q[5:8])) <= 1e-3
