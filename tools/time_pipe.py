@@ -99,3 +99,22 @@ for _ in range(300):
     ts.append(a.elapsed_time(b) * 1e3)
 print(f"latency final-stage kernel B=1: p50 {np.percentile(ts, 50):.1f} us")
 assert torch.equal(e.rec, eb.ContentAreaEngine(H, W, 1, device=dev).run(frame))
+# native K-step call (bench path), 20 steps, after an idle pause vs warm
+for pause in (0.0, 0.2):
+    r = []
+    for rep in range(3):
+        eng.run_stream(pool, 0, 5)
+        eng.fence()
+        torch.cuda.synchronize()
+        time.sleep(pause)
+        if pause:
+            eng.run_stream(pool, 0, 5) if rep == 2 else None   # rep 2: warm-up right before
+            torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        eng.run_stream(pool, 5, 20)
+        eng.fence()
+        b.record(st)
+        torch.cuda.synchronize()
+        r.append(a.elapsed_time(b) / 20 * 1e3)
+    print(f"run_stream 20 steps, pause {pause}: " + ", ".join(f"{x:.1f}" for x in r) + " us/step")
