@@ -80,7 +80,7 @@ ECA_DEV bool lsq_solve(const double* mo, int cnt, double& a_out, double& b_out, 
     v[0] = piv == 1 ? v1 : (piv == 2 ? v2 : v0);
     v[1] = piv == 1 ? v0 : v1;
     v[2] = piv == 2 ? v0 : v2;
-    const double rp = div_rn(1.0, m[0][0]);
+    const double rp = __drcp_rn(m[0][0]);   // = 1.0 / pivot, correctly rounded
 #pragma unroll
     for (int i = 1; i < 3; ++i) {
       m[i][0] = mul_rn(m[i][0], rp);
@@ -100,7 +100,7 @@ ECA_DEV bool lsq_solve(const double* mo, int cnt, double& a_out, double& b_out, 
     const double v1 = v[1], v2 = v[2];
     v[1] = sw ? v2 : v1;
     v[2] = sw ? v1 : v2;
-    const double rp = div_rn(1.0, m[1][1]);
+    const double rp = __drcp_rn(m[1][1]);
     m[2][1] = mul_rn(m[2][1], rp);
     m[2][2] = sub_rn(m[2][2], mul_rn(m[2][1], m[1][2]));
   }
@@ -180,6 +180,8 @@ ECA_DEV Ring ring_of(const Circ& c, double tol) {
 // products the masked least squares sums.
 struct FitPt {
   double x, y, z, xx, xy, yy, xz, yz;
+  float xf, yf;   // x, y rounded to FP32 (the inlier screen)
+  double pad_;
 };
 
 struct FitScratchW {
@@ -187,17 +189,52 @@ struct FitScratchW {
   double ps[2 * ECA_MAX_STRIPS];
 };
 
+// The inlier screen in FP32 (the decisions of is_inlier, exactly): d^2 of a
+// point to the lane's circle is formed from FP32 copies of the coordinates.
+// With B >= every |coordinate| of the points and of the centre, that FP32 d^2
+// is within 44 * 2^-24 * B^2 < 2.7e-6 B^2 of the exact d^2 (two roundings of
+// the inputs and of each operation), so the FP64 ring thresholds are widened
+// by E = 4e-6 B^2 and rounded outward to FP32: "in" / "out" there implies
+// "in" / "out" of the FP64 screen (ring_of), the rest takes the exact test.
+// FP32 runs at twice the FP64 rate with half the dependency latency.
+struct RingF {
+  float in_lo, in_hi, out_lo, out_hi, cx, cy;
+};
+
+ECA_DEV RingF ring_f(const Ring& g, const Circ& c, double bmax) {
+  const double b = fmax(bmax, fmax(fabs(c.cx), fabs(c.cy)));
+  const double e = 4e-6 * b * b;
+  RingF f;
+  f.in_hi = __double2float_rd(g.in_hi - e);
+  f.in_lo = __double2float_ru(g.in_lo + e);
+  f.out_hi = __double2float_ru(g.out_hi + e);
+  f.out_lo = __double2float_rd(g.out_lo - e);
+  f.cx = float(c.cx);
+  f.cy = float(c.cy);
+  return f;
+}
+
+ECA_DEV RingF ringf_dead() {   // matches no point
+  RingF f;
+  f.in_lo = 1.0f;
+  f.in_hi = -1.0f;
+  f.out_lo = -1.0f;
+  f.out_hi = -1.0f;
+  f.cx = f.cy = 0.0f;
+  return f;
+}
+
 // Inlier bits of candidates k0 .. k0+kn-1 (kn <= 32) against the lane's
-// circle: the d^2 screen for every candidate first, with no vote inside the
-// loop, so consecutive candidates' FP64 chains overlap; the rare candidates in
+// circle: the FP32 d^2 screen for every candidate first, with no vote inside
+// the loop, so consecutive candidates' chains overlap; the rare candidates in
 // the screen's band then take the exact test (the decisions of is_inlier).
-ECA_DEV uint32_t inlier_bits(const FitPt* pt, int k0, int kn, const Circ& c, const Ring& g,
+ECA_DEV uint32_t inlier_bits(const FitPt* pt, int k0, int kn, const Circ& c, const RingF& g,
                              double tol) {
   uint32_t in_m = 0, amb_m = 0;
 #pragma unroll 8
   for (int j = 0; j < kn; ++j) {
-    const double dx = pt[k0 + j].x - c.cx, dy = pt[k0 + j].y - c.cy;
-    const double d2 = fma(dx, dx, dy * dy);
+    const float dx = pt[k0 + j].xf - g.cx, dy = pt[k0 + j].yf - g.cy;
+    const float d2 = fmaf(dx, dx, dy * dy);
     const bool in = d2 <= g.in_hi && d2 >= g.in_lo;
     const bool amb = !in && !(d2 > g.out_hi || d2 < g.out_lo);
     in_m |= uint32_t(in) << j;
@@ -239,6 +276,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
   const int W = p.width, H = p.height;
   FIT_STAMP(0);
   int n = 0;
+  double bmax = 0.0;   // largest |coordinate| of the kept points (the FP32 screen's margin)
   for (int base = 0; base < n_cand; base += 32) {   // filter_candidates, order-preserving
     const int i = base + lane;
     bool keep = false;
@@ -263,12 +301,18 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
       q.yy = mul_rn(q.y, q.y);
       q.xz = mul_rn(q.x, q.z);
       q.yz = mul_rn(q.y, q.z);
+      q.xf = float(q.x);
+      q.yf = float(q.y);
+      q.pad_ = 0.0;
+      bmax = fmax(bmax, fmax(fabs(q.x), fabs(q.y)));
       ECA_CHECK(pos < n_cand);
       pt[pos] = q;
       ps[pos] = s;
     }
     n += __popc(bal);
   }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) bmax = fmax(bmax, __shfl_xor_sync(kFull, bmax, d));
   __syncwarp();
   FIT_STAMP(1);
   if (n < 3) {
@@ -302,7 +346,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
     // loop, dead hypotheses with an empty ring.  Outliers contribute fma(0, v, s)
     // = s + (+-0) = s exactly (the sums start at +0.0, so no -0.0 appears).
     for (int it = 0; it < p.ransac_iterations && __any_sync(kFull, c.alive); ++it) {
-      const Ring g = c.alive ? ring_of(c, tol) : ring_dead();
+      const RingF g = c.alive ? ring_f(ring_of(c, tol), c, bmax) : ringf_dead();
       double mo[kMom - 1] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
       for (int k0 = 0; k0 < n; k0 += 32) {
         const int kn = min(32, n - k0);
@@ -320,8 +364,8 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
           mo[5] = __fma_rn(w, P.yy, mo[5]);
           mo[6] = __fma_rn(w, P.xz, mo[6]);
           mo[7] = __fma_rn(w, P.yz, mo[7]);
-          mo[8] = add_rn(mo[8], w);
         }
+        mo[8] += double(__popc(in_m));   // the member count: exact integers
       }
       double na, nb, nr;
       if (c.alive) {
@@ -338,7 +382,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
     double score = 0.0;
     int inl = 0;
     {
-      const Ring g = c.alive ? ring_of(c, tol) : ring_dead();
+      const RingF g = c.alive ? ring_f(ring_of(c, tol), c, bmax) : ringf_dead();
       for (int k0 = 0; k0 < n; k0 += 32) {
         const int kn = min(32, n - k0);
         const uint32_t in_m = inlier_bits(pt, k0, kn, c, g, tol);

@@ -85,6 +85,16 @@ ECA_DEV float rcpf(float x) {
   return y;
 }
 
+// v / 3.0 correctly rounded for an RGB sum v in [0, 765]: q0 = v * RN(1/3)
+// plus one FMA correction equals the IEEE quotient for every such v
+// (exhaustive check: tools/div3_check.c, tests/test_host_lib.py), three
+// instructions instead of a full FP64 division.
+ECA_DEV double div3(int v) {
+  const double third = 1.0 / 3.0;
+  const double q0 = __dmul_rn(double(v), third);
+  return __fma_rn(__fma_rn(-q0, 3.0, double(v)), third, q0);
+}
+
 // handcrafted.py:164-200 for one interior column in numpy's evaluation order.
 // l/m/r: integer RGB sums at x-1, x, x+1 of rows h-1, h, h+1.
 ECA_DEV double exact_score(const int l[3], const int m[3], const int r[3], int pre_sum, int x,
@@ -92,9 +102,10 @@ ECA_DEV double exact_score(const int l[3], const int m[3], const int r[3], int p
   double gl[3], gm[3], gr[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    gl[k] = div_rn(double(l[k]), 3.0);
-    gm[k] = div_rn(double(m[k]), 3.0);
-    gr[k] = div_rn(double(r[k]), 3.0);
+    ECA_CHECK(l[k] >= 0 && l[k] <= 765 && m[k] >= 0 && m[k] <= 765 && r[k] >= 0 && r[k] <= 765);
+    gl[k] = div3(l[k]);
+    gm[k] = div3(m[k]);
+    gr[k] = div3(r[k]);
   }
   const double gx =
       add_rn(add_rn(sub_rn(gr[0], gl[0]), mul_rn(2.0, sub_rn(gr[1], gl[1]))), sub_rn(gr[2], gl[2]));
@@ -109,7 +120,7 @@ ECA_DEV double exact_score(const int l[3], const int m[3], const int r[3], int p
   const double t =
       tanh(div_rn(__dsqrt_rn(add_rn(mul_rn(gx, gx), mul_rn(gy, gy))), p.gradient_threshold));
   const double a = div_rn(2.0, add_rn(1.0, exp(mul_rn(2.0, ang))));
-  const double pre = div_rn(double(pre_sum), 3.0);
+  const double pre = div3(pre_sum);
   const double d = div_rn(2.0, add_rn(1.0, exp(div_rn(mul_rn(2.0, pre), p.intensity_threshold))));
   return mul_rn(mul_rn(t, a), d);
 }

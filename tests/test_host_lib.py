@@ -182,3 +182,18 @@ def test_validate_frame_rejects_frames_outside_the_kernel_envelope():
         api._check_config(EcaConfig(strip_count=_lib.MAX_STRIPS + 1))
     with pytest.raises(ValueError, match="ransac_attempts"):
         api._check_config(EcaConfig(ransac_attempts=_lib.MAX_ATTEMPTS + 1))
+
+
+def test_division_by_three_is_exact(tmp_path):
+    """exact_score divides RGB sums by 3 with a multiply + one FMA correction
+    (eca_strip.cuh: div3); tools/div3_check.c checks every sum 0..765 against
+    the IEEE quotient (compiled without FMA contraction)."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    exe = tmp_path / "div3"
+    src = Path(__file__).resolve().parents[1] / "tools" / "div3_check.c"
+    subprocess.run([gcc, "-O2", "-ffp-contract=off", str(src), "-o", str(exe), "-lm"], check=True)
+    assert subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.strip() == "bad=0"
