@@ -239,10 +239,17 @@ def run_ours(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # (ECA_DIST_BACKEND=gloo: a functional dry run of the N > 1 path with every
+    # rank on the box's GPUs round-robin; the measured runs use NCCL, one GPU per rank)
+    backend = os.environ.get("ECA_DIST_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     base = base_frames()
     want = oracle_records(base) if rank == 0 else None
@@ -267,7 +274,7 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local_dev) as clocks:
         # the W warm-up steps again right before the timed region: the sampler's
         # start-up pause leaves the GPU idle, and the first launches after an
         # idle period run slow
@@ -493,9 +500,9 @@ def c5_leg(eb, dev, base, rank: int, world: int) -> dict:
     ms_t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
     per_rank = [float(ms_t.item())]
     if world > 1:
-        gathered = torch.empty(world, dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(gathered, ms_t)
-        per_rank = gathered.cpu().tolist()
+        parts = [torch.empty_like(ms_t) for _ in range(world)]
+        dist.all_gather(parts, ms_t)
+        per_rank = [float(p.item()) for p in parts]
     ms = max(per_rank)
     st = table.view(torch.int32).view(C5_FRAMES, 10)[:, 9]
     del pool
