@@ -632,7 +632,10 @@ extern "C" int eca_score_rows_handcrafted(const uint8_t* frames, int batch, int6
 namespace {
 // overlap: programmatic dependent launch (then J.wait_prev must be set when
 // the candidates come from the kernel before it in the stream)
-int launch_fit(const FitJob& J, int batch, cudaStream_t stream, bool overlap = false) {
+// spread: no launch follows that must wait for this one's residency (the last
+// step of a stream): one frame per CTA, over every SM
+int launch_fit(const FitJob& J, int batch, cudaStream_t stream, bool overlap = false,
+               bool spread = false) {
   // frames (warps) per CTA: few, wide CTAs find room in a draining bounds
   // kernel sooner than many small ones (the next programmatic launch waits
   // until every CTA of this one is resident)
@@ -641,7 +644,7 @@ int launch_fit(const FitJob& J, int batch, cudaStream_t stream, bool overlap = f
     return v ? std::atoi(v) : 0;
   }();
   const size_t per = fit_smem_layout(J.n_cand, J.counts != nullptr).total;
-  int fpb = fpb_env > 0 ? fpb_env : (overlap ? 8 : 1);
+  int fpb = fpb_env > 0 ? fpb_env : (overlap && !spread ? 8 : 1);
   if (fpb > 8) fpb = 8;
   while (fpb > 1 && per * fpb > 96 * 1024) fpb /= 2;
   cudaLaunchConfig_t cfg = {};
@@ -853,10 +856,24 @@ extern "C" int eca_pipeline_create(int batch, int height, int width, const int32
   return ECA_OK;
 }
 
+namespace {
+int pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t frame_stride, int64_t row_stride,
+                  int flags, EcaFitRecord* host_records, void* stream, EcaFitRecord** out_records,
+                  bool last);
+}
+
 extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t frame_stride,
                                  int64_t row_stride, int flags, EcaFitRecord* host_records,
                                  void* stream, EcaFitRecord** out_records) {
   ECA_RANGE("eca_pipeline_step");
+  return pipeline_step(P, frames, frame_stride, row_stride, flags, host_records, stream,
+                       out_records, false);
+}
+
+namespace {
+int pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t frame_stride, int64_t row_stride,
+                  int flags, EcaFitRecord* host_records, void* stream, EcaFitRecord** out_records,
+                  bool last) {
   if (!P || !frames || !out_records || row_stride < 3LL * P->J.p.width || frame_stride < 0)
     return ECA_ERR_ARG;
   if (flags & ~(ECA_BOUNDS_ZERO_COPY | ECA_PIPE_FRAMES_READY)) return ECA_ERR_ARG;
@@ -887,7 +904,7 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   F.guard = PJ.ticket;
   F.dbg_seq = P->step;
   F.wait_prev = 1;   // its survivors come from the bounds kernel just before
-  rc = launch_fit(F, P->batch, st, /*overlap=*/true);
+  rc = launch_fit(F, P->batch, st, /*overlap=*/true, /*spread=*/last);
   if (rc) return rc;
   P->last = s;
   P->last_stream = st;
@@ -895,6 +912,7 @@ extern "C" int eca_pipeline_step(EcaPipeline* P, const uint8_t* frames, int64_t 
   *out_records = P->rec[s];
   return ECA_OK;
 }
+}  // namespace
 
 extern "C" int eca_pipeline_run(EcaPipeline* P, const uint8_t* pool, int64_t batch_stride,
                                 int n_slots, int first_slot, int n_steps, int64_t frame_stride,
@@ -905,8 +923,9 @@ extern "C" int eca_pipeline_run(EcaPipeline* P, const uint8_t* pool, int64_t bat
   EcaFitRecord* out = nullptr;
   for (int j = 0; j < n_steps; ++j) {
     const int slot = int((int64_t(first_slot) + j) % n_slots);
-    const int rc = eca_pipeline_step(P, pool + slot * batch_stride, frame_stride, row_stride, flags,
-                                     nullptr, stream, &out);
+    // the last step's fits run alone: spread them over every SM
+    const int rc = pipeline_step(P, pool + slot * batch_stride, frame_stride, row_stride, flags,
+                                 nullptr, stream, &out, j + 1 == n_steps);
     if (rc) return rc;
   }
   return ECA_OK;
