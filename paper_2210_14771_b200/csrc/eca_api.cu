@@ -1005,7 +1005,7 @@ extern "C" int eca_debug_timeline(unsigned long long* out) {
 #endif
 #ifdef ECA_FIT_TIMES
 extern "C" int eca_debug_fit_times(unsigned long long* out, int n) {
-  return cudaMemcpyFromSymbol(out, g_fit_times, sizeof(unsigned long long) * 8 * n) == cudaSuccess ? 0
+  return cudaMemcpyFromSymbol(out, g_fit_times, sizeof(unsigned long long) * 16 * n) == cudaSuccess ? 0
                                                                                                 : -2;
 }
 #endif

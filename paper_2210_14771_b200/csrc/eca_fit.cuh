@@ -253,11 +253,11 @@ ECA_DEV Ring ring_dead() {   // matches no point (hypothesis no longer alive)
 }
 
 #ifdef ECA_FIT_TIMES   // diagnostic builds: per-frame phase clocks (tools/fit_times.py)
-__device__ unsigned long long g_fit_times[8 * 4096];
+__device__ unsigned long long g_fit_times[16 * 4096];
 #define FIT_STAMP(k)                                                        \
   do {                                                                      \
     if ((threadIdx.x & 31) == 0 && blockIdx.x < 4096)                       \
-      g_fit_times[8 * blockIdx.x + (k)] = clock64();                        \
+      g_fit_times[16 * blockIdx.x + (k)] = clock64();                       \
   } while (0)
 #else
 #define FIT_STAMP(k) \
@@ -351,6 +351,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
       for (int k0 = 0; k0 < n; k0 += 32) {
         const int kn = min(32, n - k0);
         const uint32_t in_m = inlier_bits(pt, k0, kn, c, g, tol);
+        if (it == 1) FIT_STAMP(8);
 #pragma unroll 4
         for (int j = 0; j < kn; ++j) {
           const FitPt& P = pt[k0 + j];
@@ -367,6 +368,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
         }
         mo[8] += double(__popc(in_m));   // the member count: exact integers
       }
+      if (it == 1) FIT_STAMP(9);
       double na, nb, nr;
       if (c.alive) {
         if (lsq_solve(mo, int(mo[8]), na, nb, nr)) {

@@ -31,15 +31,17 @@ for rep in range(3):
     b.record()
     torch.cuda.synchronize()
     print(f"fit kernel {a.elapsed_time(b) * 1e3:.1f} us")
-out = (ctypes.c_ulonglong * (8 * B))()
+out = (ctypes.c_ulonglong * (16 * B))()
 fn = lib.eca_debug_fit_times
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 assert fn(ctypes.cast(out, ctypes.c_void_p), B) == 0
-t = np.array(out, dtype=np.int64).reshape(B, 8)
-d = np.diff(t, axis=1)
+t = np.array(out, dtype=np.int64).reshape(B, 16)[:, :10]
+d = np.diff(t[:, :8], axis=1)
 names = ["filter", "circum", "iter1", "iter2", "iter3", "final", "vote"]
 for i, n in enumerate(names):
     print(f"{n:8s} median {np.median(d[:, i]):8.0f} clk  p90 {np.percentile(d[:, i], 90):8.0f}")
+print(f"iter2 split: screen {np.median(t[:, 8] - t[:, 3]):.0f}  moments {np.median(t[:, 9] - t[:, 8]):.0f}  "
+      f"lsq {np.median(t[:, 4] - t[:, 9]):.0f} clk")
 print(f"total    median {np.median(t[:, 7] - t[:, 0]):8.0f} clk")
 # the FP64 rescore stage alone (one lane per survivor slot)
 for rep in range(3):
