@@ -876,7 +876,10 @@ def train_leg(eb, dev) -> dict:
                       "forward + BCE + backward + update)",
             "value": round(epochs * TRAIN_M / dt, 1), "unit": "samples/s",
             "ms_per_step": round(1e3 * dt / steps, 4), "steps": steps, "epochs": epochs,
-            "launches_per_step": 16, "dtype": "f32", "data": "synthetic normal strips",
+            "launches_per_step": 16 if os.environ.get("ECA_TRAIN_SIMT") == "1" else 14,
+            "kernels": "SIMT FP32 (ECA_TRAIN_SIMT=1)" if os.environ.get("ECA_TRAIN_SIMT") == "1" else
+                       "tcgen05 3xTF32 conv forward / dgrad / wgrad (eca_train_tc.cuh)",
+            "dtype": "f32", "data": "synthetic normal strips",
             "method": "wall clock of edgenet.train over 4 epochs of 2048 strips resident in HBM: epoch 1 "
                       "eager, epoch 2 captured as a CUDA graph, epochs 3-4 graph replays"}
 

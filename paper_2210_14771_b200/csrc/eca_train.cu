@@ -22,7 +22,13 @@
 // logits / gradients agree to FP32 rounding, not bitwise.
 #include <math.h>
 
+#include <cstdlib>
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "eca_common.cuh"
+#include "eca_train_tc.cuh"
 
 using namespace eca;
 
@@ -33,8 +39,14 @@ constexpr int kOffW0 = 0, kOffB0 = 360, kOffW1 = 368, kOffB1 = 1520, kOffW2 = 15
 static_assert(kNetN == ECA_NET_FLOATS, "weight layout");
 constexpr int kSeg = 128;   // output columns per weight-gradient segment
 
+// tensor-core weight-gradient partials: [kWgCtas][R][CO] per layer
+constexpr size_t kTcPart0 = size_t(ttc::kWgCtas) * ttc::WgCfg<5, 8, 3>::R * 8;
+constexpr size_t kTcPart1 = size_t(ttc::kWgCtas) * ttc::WgCfg<8, 16, 3>::R * 16;
+constexpr size_t kTcPart2 = size_t(ttc::kWgCtas) * ttc::WgCfg<16, 32, 3>::R * 32;
+constexpr size_t kTcPart3 = size_t(ttc::kWgCtas) * ttc::WgCfg<32, 1, 1>::R * 1;
+
 struct TrainWs {   // workspace layout (floats unless noted)
-  size_t a1, a2, a3, logit, d3, d2, d1, dlog, wpart, lpart, total;
+  size_t a1, a2, a3, logit, d3, d2, d1, dlog, wpart, lpart, tcpart, total;
   int nseg3, nseg2, nseg1, nseg0, nlblk;
 };
 
@@ -65,6 +77,7 @@ TrainWs train_ws(int m, int h, int w) {
   L.wpart = o; o = up256(o + 4 * parts);
   L.nlblk = int((p3 + kLossThreads - 1) / kLossThreads);
   L.lpart = o; o = up256(o + 8 * size_t(L.nlblk));
+  L.tcpart = o; o = up256(o + 4 * (kTcPart0 + kTcPart1 + kTcPart2 + kTcPart3));
   L.total = o;
   return L;
 }
@@ -303,6 +316,91 @@ int check_dims(int m, int h, int w) {
   return ECA_OK;
 }
 
+// the SIMT kernels above instead of the tensor-core ones (comparison runs)
+bool train_simt() {
+  static const bool v = [] {
+    const char* e = std::getenv("ECA_TRAIN_SIMT");
+    return e && *e && *e != '0';
+  }();
+  return v;
+}
+
+// dynamic shared-memory opt-in of a kernel on the current device for `bytes`
+// (the most any launch of it uses), once per (kernel, device), and the number
+// of its 128-thread CTAs one SM holds at that size times the SM count; 0 if
+// the attribute could not be set
+int optin(const void* kern, int bytes) {
+  struct Entry {
+    const void* kern;
+    int dev, slots;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.kern == kern && d.dev == dev) return d.slots;
+  int per_sm = 0, sms = 0;
+  const bool ok = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess &&
+                  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess &&
+                  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ttc::kThreads, bytes) ==
+                      cudaSuccess &&
+                  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess;
+  done.push_back({kern, dev, ok ? (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148) : 0});
+  return done.back().slots;
+}
+
+template <int CI, int CO, bool kHead>
+bool launch_fwd_tc(const float* x, const int32_t* idx, int m, int hi, int wi, const float* net, int ow,
+                   int ob, float* y, float* logit, cudaStream_t st) {
+  using C = ttc::FwdCfg<CI, CO>;
+  auto k = ttc::tc_conv_fwd<CI, CO, kHead>;
+  const int slots = optin(reinterpret_cast<const void*>(k), C::SMEM);
+  if (!slots) return false;
+  const int64_t tiles = int64_t(m) * (hi - 2) * ((wi - 2 + ttc::kTOut - 1) / ttc::kTOut);
+  k<<<unsigned(tiles < slots ? tiles : slots), ttc::kThreads, C::SMEM, st>>>(
+      x, idx, m, hi, wi, net + ow, net + ob, kHead ? net + kOffW3 : nullptr, y, logit);
+  return true;
+}
+
+template <int CI, int CO>
+bool launch_dgrad_tc(const float* dy, const float* xin, int m, int hi, int wi, const float* wk, float* dx,
+                     cudaStream_t st) {
+  using C = ttc::DgCfg<CI, CO>;
+  auto k = ttc::tc_conv_dgrad<CI, CO>;
+  const int smem = C::smem(hi - 2);
+  const int slots = optin(reinterpret_cast<const void*>(k), C::smem(3));
+  if (!slots) return false;
+  // CTAs per SM at this launch's (smaller) size
+  int per_sm = 0, sms = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, ttc::kThreads, smem) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return false;
+  const int64_t cap = int64_t(per_sm > 0 ? per_sm : 1) * sms;
+  const int64_t tiles = int64_t(m) * hi * ((wi + ttc::kTOut - 1) / ttc::kTOut);
+  k<<<unsigned(tiles < cap ? tiles : cap), ttc::kThreads, smem, st>>>(dy, xin, m, hi, wi, wk,
+                                                                     C::a_region(hi - 2), dx);
+  return true;
+}
+
+// returns the number of partials (CTAs), 0 on failure
+template <int CI, int CO, int KS>
+int launch_wgrad_tc(const float* dy, const float* x, const int32_t* idx, int m, int hi, int wi, float* part,
+                    cudaStream_t st) {
+  using C = ttc::WgCfg<CI, CO, KS>;
+  auto k = ttc::tc_conv_wgrad<CI, CO, KS>;
+  const int slots = optin(reinterpret_cast<const void*>(k), C::SMEM);
+  if (!slots) return 0;
+  const int wo = wi - KS + 1;
+  const int64_t units = int64_t(m) * (hi - KS + 1) * ((wo + ttc::kWgK - 1) / ttc::kWgK);
+  const int cap = slots < ttc::kWgCtas ? slots : ttc::kWgCtas;   // one wave
+  const int g = int(units < cap ? units : cap);
+  k<<<g, ttc::kThreads, C::SMEM, st>>>(dy, x, idx, m, hi, wi, part);
+  return g;
+}
+
 }  // namespace
 
 extern "C" {
@@ -326,14 +424,21 @@ int eca_edgenet_forward(const float* x, const int32_t* index, int m, int h, int 
   float* a3 = reinterpret_cast<float*>(ws + L.a3);
   float* logit = reinterpret_cast<float*>(ws + L.logit);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  conv3_fwd<5, 8, 1><<<dim3(blocks(int64_t(m) * (h - 2) * (w - 2), 128), 1), 128, 0, st>>>(
-      x, index, m, h, w, net + kOffW0, net + kOffB0, a1);
-  conv3_fwd<8, 16, 2><<<dim3(blocks(int64_t(m) * (h - 4) * (w - 4), 128), 2), 128, 0, st>>>(
-      a1, nullptr, m, h - 2, w - 2, net + kOffW1, net + kOffB1, a2);
-  conv3_fwd<16, 32, 4><<<dim3(blocks(int64_t(m) * (h - 6) * (w - 6), 128), 4), 128, 0, st>>>(
-      a2, nullptr, m, h - 4, w - 4, net + kOffW2, net + kOffB2, a3);
   const int64_t plane = int64_t(h - 6) * (w - 6);
-  head_fwd<<<blocks(m * plane, 128), 128, 0, st>>>(a3, plane, m, net, logit);
+  if (!train_simt()) {   // tcgen05: three conv launches, the head fused into the last
+    if (!launch_fwd_tc<5, 8, false>(x, index, m, h, w, net, kOffW0, kOffB0, a1, nullptr, st) ||
+        !launch_fwd_tc<8, 16, false>(a1, nullptr, m, h - 2, w - 2, net, kOffW1, kOffB1, a2, nullptr, st) ||
+        !launch_fwd_tc<16, 32, true>(a2, nullptr, m, h - 4, w - 4, net, kOffW2, kOffB2, a3, logit, st))
+      return ECA_ERR_CUDA;
+  } else {
+    conv3_fwd<5, 8, 1><<<dim3(blocks(int64_t(m) * (h - 2) * (w - 2), 128), 1), 128, 0, st>>>(
+        x, index, m, h, w, net + kOffW0, net + kOffB0, a1);
+    conv3_fwd<8, 16, 2><<<dim3(blocks(int64_t(m) * (h - 4) * (w - 4), 128), 2), 128, 0, st>>>(
+        a1, nullptr, m, h - 2, w - 2, net + kOffW1, net + kOffB1, a2);
+    conv3_fwd<16, 32, 4><<<dim3(blocks(int64_t(m) * (h - 6) * (w - 6), 128), 4), 128, 0, st>>>(
+        a2, nullptr, m, h - 4, w - 4, net + kOffW2, net + kOffB2, a3);
+    head_fwd<<<blocks(m * plane, 128), 128, 0, st>>>(a3, plane, m, net, logit);
+  }
   if (out_logits)
     cudaMemcpyAsync(out_logits, logit, sizeof(float) * size_t(m * plane), cudaMemcpyDeviceToDevice, st);
   return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
@@ -354,6 +459,33 @@ int eca_edgenet_backward(const float* x, const float* targets, const int32_t* in
   loss_kernel<<<L.nlblk, kLossThreads, 0, st>>>(f(L.logit), targets, index, m, plane, f(L.dlog), lpart);
   loss_final<<<1, 256, 0, st>>>(lpart, L.nlblk, n, out_loss, diverged);
   if (!out_grads) return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;   // loss only
+  if (!train_simt()) {   // tcgen05 weight / input gradients, one fixed-order reduction
+    float* tp0 = f(L.tcpart);
+    float* tp1 = tp0 + kTcPart0;
+    float* tp2 = tp1 + kTcPart1;
+    float* tp3 = tp2 + kTcPart2;
+    ttc::WgReduceJob R{};
+    R.l[3] = {tp3, ttc::WgCfg<32, 1, 1>::R, 1,
+              launch_wgrad_tc<32, 1, 1>(f(L.dlog), f(L.a3), nullptr, m, h - 6, w - 6, tp3, st),
+              out_grads + kOffW3, out_grads + kOffB3};
+    head_dgrad<<<blocks(n * 32, 256), 256, 0, st>>>(f(L.dlog), f(L.a3), plane, m, net, f(L.d3));
+    R.l[2] = {tp2, ttc::WgCfg<16, 32, 3>::R, 32,
+              launch_wgrad_tc<16, 32, 3>(f(L.d3), f(L.a2), nullptr, m, h - 4, w - 4, tp2, st),
+              out_grads + kOffW2, out_grads + kOffB2};
+    if (!launch_dgrad_tc<16, 32>(f(L.d3), f(L.a2), m, h - 4, w - 4, net + kOffW2, f(L.d2), st))
+      return ECA_ERR_CUDA;
+    R.l[1] = {tp1, ttc::WgCfg<8, 16, 3>::R, 16,
+              launch_wgrad_tc<8, 16, 3>(f(L.d2), f(L.a1), nullptr, m, h - 2, w - 2, tp1, st),
+              out_grads + kOffW1, out_grads + kOffB1};
+    if (!launch_dgrad_tc<8, 16>(f(L.d2), f(L.a1), m, h - 2, w - 2, net + kOffW1, f(L.d1), st))
+      return ECA_ERR_CUDA;
+    R.l[0] = {tp0, ttc::WgCfg<5, 8, 3>::R, 8, launch_wgrad_tc<5, 8, 3>(f(L.d1), x, index, m, h, w, tp0, st),
+              out_grads + kOffW0, out_grads + kOffB0};
+    for (const auto& l : R.l)
+      if (l.G == 0) return ECA_ERR_CUDA;
+    ttc::tc_wgrad_reduce<<<dim3(blocks(ttc::WgCfg<16, 32, 3>::R * 32, 32), 4), dim3(32, ttc::kRedG), 0, st>>>(R);
+    return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
+  }
   // head (1x1, 32 -> 1)
   float* part = f(L.wpart);
   float* p3 = part;
