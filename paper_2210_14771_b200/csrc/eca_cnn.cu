@@ -718,20 +718,28 @@ extern "C" int eca_points_learned_ex(const uint8_t* frames, int batch, int64_t f
   const bool tc = (flags & ECA_LEARNED_SIMT) == 0;   // tcgen05 unless the SIMT kernel is asked for
   // per device: shared-memory opt-in and occupancy (checked)
   static std::once_flag once[64];
-  static int per_sm_d[64], per_sm_tc_d[64], sms_d[64];
+  static int per_sm_d[64], per_sm_tc_d[64], sms_d[64], tc_smem_d[64];
   static bool ok_d[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return ECA_ERR_CUDA;
   std::call_once(once[dev], [dev] {
-    int a = 0, b = 0, c = 0;
+    int a = 0, b = 0, c = 0, optin_max = 0;
+    // cnn_kernel_tc holds all 512 TMEM columns: its CTA takes the whole
+    // shared memory too, so the block scheduler cannot co-locate another
+    // TMEM-using CTA with it (the scheduler does not account TMEM)
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, cnn_kernel_tc);
+    cudaDeviceGetAttribute(&optin_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    tc_smem_d[dev] = optin_max - int(fa.sharedSizeBytes);
+    if (tc_smem_d[dev] < int(sizeof(CnnSmemTc))) tc_smem_d[dev] = int(sizeof(CnnSmemTc));
     ok_d[dev] = cudaFuncSetAttribute(cnn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(sizeof(CnnSmem))) == cudaSuccess &&
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, cnn_kernel, 256, sizeof(CnnSmem)) ==
                     cudaSuccess &&
                 cudaFuncSetAttribute(cnn_kernel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(sizeof(CnnSmemTc))) == cudaSuccess &&
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cnn_kernel_tc, 512,
-                                                              sizeof(CnnSmemTc)) == cudaSuccess &&
+                                     tc_smem_d[dev]) == cudaSuccess &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cnn_kernel_tc, 512, tc_smem_d[dev]) ==
+                    cudaSuccess &&
                 cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess;
     per_sm_d[dev] = a > 0 ? a : 1;
     per_sm_tc_d[dev] = b > 0 ? b : 1;
@@ -743,7 +751,7 @@ extern "C" int eca_points_learned_ex(const uint8_t* frames, int batch, int64_t f
   const int64_t cap = int64_t(sms) * (tc ? per_sm_tc : per_sm);
   const int grid = int(tiles < cap ? tiles : cap);
   if (tc)
-    cnn_kernel_tc<<<grid, 512, sizeof(CnnSmemTc), st>>>(J);
+    cnn_kernel_tc<<<grid, 512, tc_smem_d[dev], st>>>(J);
   else
     cnn_kernel<<<grid, 256, sizeof(CnnSmem), st>>>(J);
   select_kernel<<<dim3(n_strips, batch), 256, 0, st>>>(out_probs, n_strips, width, nullptr, out_x,

@@ -5,21 +5,26 @@
 // RGBXY rows), targets [*][1][h-6][W-6]; a batch is a list of sample indices
 // into them (the epoch permutation), gathered inside the first kernels.
 //
-//  forward    conv3_fwd (3x3 valid conv + bias + ReLU, one thread per output
-//             position, all output channels in registers, weights in shared
-//             memory) x3, head_fwd (1x1 conv) -> logits; activations stay in
-//             the workspace (the reference's caches; ReLU masks are y > 0).
-//  backward   loss_kernel: stable BCE terms in FP64 (edgenet.py:236-241) and
-//             dlogits = (sigmoid(z) - t) / N in FP32 (:315); head_dgrad; per 3x3
-//             layer conv3_dgrad (dx = full correlation with the flipped
-//             kernel, times the previous layer's ReLU mask) and conv_wgrad
-//             (per-row-segment partial dW / db in shared memory, then a
-//             fixed-order reduction: deterministic, no float atomics).
+// Default: the convolutions on the tensor cores (eca_train_tc.cuh, tcgen05
+// 3xTF32; 11 launches per SGD step):
+//  forward    tc_conv_fwd x3 (3x3 valid conv + bias + ReLU; the last one also
+//             computes the 1x1 head's logits); activations stay in the
+//             workspace (the reference's caches; ReLU masks are y > 0).
+//  backward   loss_head_kernel: stable BCE terms in FP64 (edgenet.py:236-241),
+//             dlogits = (sigmoid(z) - t) / N in FP32 (:315), the head's input
+//             gradient and block partials of its weight gradient; loss_final;
+//             per 3x3 layer tc_conv_wgrad (partials per CTA) and tc_conv_dgrad
+//             (x the previous layer's ReLU mask; not for layer 0);
+//             tc_wgrad_reduce sums all partials in a fixed order
+//             (deterministic, no float atomics).
 //  sgd        w = w - fl32(lr) * g without contraction (:327-328), skipped
 //             once a non-finite loss was seen (the reference raises before
 //             that update), so an epoch runs without host round trips.
-// Accumulations are sequential FMA; the reference's sgemm reassociates, so
-// logits / gradients agree to FP32 rounding, not bitwise.
+// ECA_TRAIN_SIMT=1: the CUDA-core kernels below (conv3_fwd / head_fwd,
+// loss_kernel, head_dgrad, conv3_dgrad, conv_wgrad + wgrad_reduce; sequential
+// FMA, per-row-segment weight-gradient partials); kept for comparison.
+// The reference's sgemm reassociates, so logits / gradients agree to FP32
+// rounding, not bitwise.
 #include <math.h>
 
 #include <cstdlib>
@@ -43,10 +48,9 @@ constexpr int kSeg = 128;   // output columns per weight-gradient segment
 constexpr size_t kTcPart0 = size_t(ttc::kWgCtas) * ttc::WgCfg<5, 8, 3>::R * 8;
 constexpr size_t kTcPart1 = size_t(ttc::kWgCtas) * ttc::WgCfg<8, 16, 3>::R * 16;
 constexpr size_t kTcPart2 = size_t(ttc::kWgCtas) * ttc::WgCfg<16, 32, 3>::R * 32;
-constexpr size_t kTcPart3 = size_t(ttc::kWgCtas) * ttc::WgCfg<32, 1, 1>::R * 1;
 
 struct TrainWs {   // workspace layout (floats unless noted)
-  size_t a1, a2, a3, logit, d3, d2, d1, dlog, wpart, lpart, tcpart, total;
+  size_t a1, a2, a3, logit, d3, d2, d1, dlog, wpart, lpart, tcpart, hpart, total;
   int nseg3, nseg2, nseg1, nseg0, nlblk;
 };
 
@@ -77,7 +81,8 @@ TrainWs train_ws(int m, int h, int w) {
   L.wpart = o; o = up256(o + 4 * parts);
   L.nlblk = int((p3 + kLossThreads - 1) / kLossThreads);
   L.lpart = o; o = up256(o + 8 * size_t(L.nlblk));
-  L.tcpart = o; o = up256(o + 4 * (kTcPart0 + kTcPart1 + kTcPart2 + kTcPart3));
+  L.tcpart = o; o = up256(o + 4 * (kTcPart0 + kTcPart1 + kTcPart2));
+  L.hpart = o; o = up256(o + 4 * 33 * size_t(L.nlblk));
   L.total = o;
   return L;
 }
@@ -182,6 +187,71 @@ __global__ void loss_final(const double* lpart, int nblk, int64_t n, double* out
     const double loss = red[0] / double(n);
     *out_loss = loss;
     if (!isfinite(loss) && flag) *flag = 1;
+  }
+}
+
+// the loss kernel fused with the 1x1 head's backward (tensor-core path): per
+// position the BCE term, dlogit g, the head's input gradient
+// d3[c] = g * w3[c] * (a3[c] > 0), and per block the partial head gradients
+// sum g * a3[c] (r = c) and sum g (r = 32), summed in a fixed order (xor tree
+// within each warp, then the warps in order); hpart[block][33] is reduced by
+// tc_wgrad_reduce like the conv layers' partials
+__global__ void __launch_bounds__(kLossThreads) loss_head_kernel(
+    const float* __restrict__ logit, const float* __restrict__ tgt, const int32_t* __restrict__ idx, int m,
+    int64_t plane, const float* __restrict__ a3, const float* __restrict__ net, float* __restrict__ dlog,
+    float* __restrict__ d3, double* __restrict__ lpart, float* __restrict__ hpart) {
+  const int64_t n = int64_t(m) * plane;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  double term = 0.0;
+  float g = 0.f, av[32];
+  if (p < n) {
+    const int64_t b = p / plane, q = p % plane;
+    const float t = tgt[(idx ? int64_t(idx[b]) : b) * plane + q];
+    const float z = logit[p];
+    const float* a = a3 + b * 32 * plane + q;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) av[c] = a[c * plane];
+    const double zd = double(z), td = double(t);
+    term = add_rn(sub_rn(fmax(zd, 0.0), mul_rn(zd, td)), log1p(exp(-fabs(zd))));
+    float sg;   // _sigmoid (edgenet.py:227-233), FP32
+    if (z >= 0.f) {
+      sg = 1.0f / (1.0f + expf(-z));
+    } else {
+      const float e = expf(z);
+      sg = e / (1.0f + e);
+    }
+    g = __fdiv_rn(__fsub_rn(sg, t), float(n));
+    dlog[p] = g;
+    float* d = d3 + b * 32 * plane + q;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      d[c * plane] = (g * net[kOffW3 + c]) * float(av[c] > 0.f);   // dx * mask (inf * 0 = NaN, as numpy)
+  } else {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) av[c] = 0.f;
+  }
+  __shared__ double red[kLossThreads];
+  __shared__ float hred[kLossThreads / 32][33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 33; ++c) {
+    float v = c < 32 ? g * av[c] : g;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) hred[wid][c] = v;
+  }
+  red[threadIdx.x] = term;
+  __syncthreads();
+  for (int o = kLossThreads / 2; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) lpart[blockIdx.x] = red[0];
+  if (threadIdx.x < 33) {
+    float v = hred[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < kLossThreads / 32; ++w) v += hred[w][threadIdx.x];
+    hpart[int64_t(blockIdx.x) * 33 + threadIdx.x] = v;
   }
 }
 
@@ -325,30 +395,51 @@ bool train_simt() {
   return v;
 }
 
-// dynamic shared-memory opt-in of a kernel on the current device for `bytes`
-// (the most any launch of it uses), once per (kernel, device), and the number
-// of its 128-thread CTAs one SM holds at that size times the SM count; 0 if
-// the attribute could not be set
-int optin(const void* kern, int bytes) {
+// Launch plan of a tensor-core training kernel on the current device: the
+// dynamic shared memory to request and the CTAs one wave holds.  The block
+// scheduler does not account TMEM: CTAs it co-locates -- of one kernel, or of
+// kernels on concurrent streams -- must not ask for more than the SM's 512
+// columns together (oversubscribing faults; measured).  So every kernel's
+// shared memory is padded until its share of the SM's shared memory is at
+// least its share of the TMEM columns: any set of CTAs that fits the shared
+// memory then fits the TMEM.
+struct TcPlan {
+  int dyn, slots;
+};
+TcPlan tc_plan(const void* kern, int need, int cols) {
   struct Entry {
     const void* kern;
-    int dev, slots;
+    int dev, need;
+    TcPlan plan;
   };
   static std::mutex mu;
   static std::vector<Entry> done;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return {0, 0};
   std::lock_guard<std::mutex> lock(mu);
   for (const auto& d : done)
-    if (d.kern == kern && d.dev == dev) return d.slots;
-  int per_sm = 0, sms = 0;
-  const bool ok = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess &&
-                  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess &&
-                  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ttc::kThreads, bytes) ==
-                      cudaSuccess &&
-                  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess;
-  done.push_back({kern, dev, ok ? (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148) : 0});
-  return done.back().slots;
+    if (d.kern == kern && d.dev == dev && d.need == need) return d.plan;
+  TcPlan p{0, 0};
+  cudaFuncAttributes fa{};
+  int sm_smem = 0, reserved = 0, optin_max = 0, sms = 0, per_sm = 0;
+  if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&optin_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) {
+    const int64_t share = (int64_t(cols) * sm_smem + 511) / 512;   // per-CTA footprint for `cols`
+    int dyn = int(share - int64_t(fa.sharedSizeBytes) - reserved);
+    if (dyn < need) dyn = need;
+    if (dyn > optin_max - int(fa.sharedSizeBytes)) dyn = optin_max - int(fa.sharedSizeBytes);
+    if (dyn >= need &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) == cudaSuccess &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ttc::kThreads, dyn) == cudaSuccess &&
+        per_sm >= 1 && per_sm * cols <= 512)
+      p = {dyn, per_sm * sms};
+  }
+  done.push_back({kern, dev, need, p});
+  return p;
 }
 
 template <int CI, int CO, bool kHead>
@@ -356,10 +447,10 @@ bool launch_fwd_tc(const float* x, const int32_t* idx, int m, int hi, int wi, co
                    int ob, float* y, float* logit, cudaStream_t st) {
   using C = ttc::FwdCfg<CI, CO>;
   auto k = ttc::tc_conv_fwd<CI, CO, kHead>;
-  const int slots = optin(reinterpret_cast<const void*>(k), C::SMEM);
-  if (!slots) return false;
+  const TcPlan p = tc_plan(reinterpret_cast<const void*>(k), C::SMEM, C::COLS);
+  if (!p.slots) return false;
   const int64_t tiles = int64_t(m) * (hi - 2) * ((wi - 2 + ttc::kTOut - 1) / ttc::kTOut);
-  k<<<unsigned(tiles < slots ? tiles : slots), ttc::kThreads, C::SMEM, st>>>(
+  k<<<unsigned(tiles < p.slots ? tiles : p.slots), ttc::kThreads, p.dyn, st>>>(
       x, idx, m, hi, wi, net + ow, net + ob, kHead ? net + kOffW3 : nullptr, y, logit);
   return true;
 }
@@ -369,18 +460,11 @@ bool launch_dgrad_tc(const float* dy, const float* xin, int m, int hi, int wi, c
                      cudaStream_t st) {
   using C = ttc::DgCfg<CI, CO>;
   auto k = ttc::tc_conv_dgrad<CI, CO>;
-  const int smem = C::smem(hi - 2);
-  const int slots = optin(reinterpret_cast<const void*>(k), C::smem(3));
-  if (!slots) return false;
-  // CTAs per SM at this launch's (smaller) size
-  int per_sm = 0, sms = 0, dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, ttc::kThreads, smem) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return false;
-  const int64_t cap = int64_t(per_sm > 0 ? per_sm : 1) * sms;
+  const TcPlan p = tc_plan(reinterpret_cast<const void*>(k), C::smem(hi - 2), C::COLS);
+  if (!p.slots) return false;
+  const int64_t cap = p.slots;
   const int64_t tiles = int64_t(m) * hi * ((wi + ttc::kTOut - 1) / ttc::kTOut);
-  k<<<unsigned(tiles < cap ? tiles : cap), ttc::kThreads, smem, st>>>(dy, xin, m, hi, wi, wk,
+  k<<<unsigned(tiles < cap ? tiles : cap), ttc::kThreads, p.dyn, st>>>(dy, xin, m, hi, wi, wk,
                                                                      C::a_region(hi - 2), dx);
   return true;
 }
@@ -391,13 +475,13 @@ int launch_wgrad_tc(const float* dy, const float* x, const int32_t* idx, int m, 
                     cudaStream_t st) {
   using C = ttc::WgCfg<CI, CO, KS>;
   auto k = ttc::tc_conv_wgrad<CI, CO, KS>;
-  const int slots = optin(reinterpret_cast<const void*>(k), C::SMEM);
-  if (!slots) return 0;
+  const TcPlan p = tc_plan(reinterpret_cast<const void*>(k), C::SMEM, C::COLS);
+  if (!p.slots) return 0;
   const int wo = wi - KS + 1;
   const int64_t units = int64_t(m) * (hi - KS + 1) * ((wo + ttc::kWgK - 1) / ttc::kWgK);
-  const int cap = slots < ttc::kWgCtas ? slots : ttc::kWgCtas;   // one wave
+  const int cap = p.slots < ttc::kWgCtas ? p.slots : ttc::kWgCtas;   // one wave
   const int g = int(units < cap ? units : cap);
-  k<<<g, ttc::kThreads, C::SMEM, st>>>(dy, x, idx, m, hi, wi, part);
+  k<<<g, ttc::kThreads, p.dyn, st>>>(dy, x, idx, m, hi, wi, part);
   return g;
 }
 
@@ -456,19 +540,20 @@ int eca_edgenet_backward(const float* x, const float* targets, const int32_t* in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t plane = int64_t(h - 6) * (w - 6), n = int64_t(m) * plane;
   double* lpart = reinterpret_cast<double*>(ws + L.lpart);
-  loss_kernel<<<L.nlblk, kLossThreads, 0, st>>>(f(L.logit), targets, index, m, plane, f(L.dlog), lpart);
+  const bool tc = out_grads && !train_simt();
+  if (tc)
+    loss_head_kernel<<<L.nlblk, kLossThreads, 0, st>>>(f(L.logit), targets, index, m, plane, f(L.a3), net,
+                                                       f(L.dlog), f(L.d3), lpart, f(L.hpart));
+  else
+    loss_kernel<<<L.nlblk, kLossThreads, 0, st>>>(f(L.logit), targets, index, m, plane, f(L.dlog), lpart);
   loss_final<<<1, 256, 0, st>>>(lpart, L.nlblk, n, out_loss, diverged);
   if (!out_grads) return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;   // loss only
-  if (!train_simt()) {   // tcgen05 weight / input gradients, one fixed-order reduction
+  if (tc) {   // tcgen05 weight / input gradients, one fixed-order reduction
     float* tp0 = f(L.tcpart);
     float* tp1 = tp0 + kTcPart0;
     float* tp2 = tp1 + kTcPart1;
-    float* tp3 = tp2 + kTcPart2;
     ttc::WgReduceJob R{};
-    R.l[3] = {tp3, ttc::WgCfg<32, 1, 1>::R, 1,
-              launch_wgrad_tc<32, 1, 1>(f(L.dlog), f(L.a3), nullptr, m, h - 6, w - 6, tp3, st),
-              out_grads + kOffW3, out_grads + kOffB3};
-    head_dgrad<<<blocks(n * 32, 256), 256, 0, st>>>(f(L.dlog), f(L.a3), plane, m, net, f(L.d3));
+    R.l[3] = {f(L.hpart), 33, 1, L.nlblk, out_grads + kOffW3, out_grads + kOffB3};
     R.l[2] = {tp2, ttc::WgCfg<16, 32, 3>::R, 32,
               launch_wgrad_tc<16, 32, 3>(f(L.d3), f(L.a2), nullptr, m, h - 4, w - 4, tp2, st),
               out_grads + kOffW2, out_grads + kOffB2};

@@ -95,7 +95,12 @@ ECA_DEV void mma_terms(uint32_t tmem, uint32_t a, int astride, int sboa, uint32_
 constexpr int up8(int c) { return (c + 7) / 8 * 8; }
 constexpr int up16(int c) { return (c + 15) / 16 * 16; }
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
-constexpr int tmem_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+#ifndef ECA_TMEM_ALL
+#define ECA_TMEM_ALL 0
+#endif
+constexpr int tmem_cols(int n) {
+  return ECA_TMEM_ALL ? 512 : n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512;
+}
 
 ECA_DEV void tmem_alloc(uint32_t* slot, int cols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(slot)),
@@ -132,7 +137,11 @@ struct FwdCfg {
   static constexpr int B_BYTES = N * KP * 4;
   static constexpr int A_REGION = cmax(3 * kP * A_BYTES, 2 * CO * kXb * 4);   // + exchange after the MMAs
   static constexpr int SMEM = A_REGION + 3 * kP * B_BYTES;
-  static constexpr int COLS = tmem_cols(3 * N);   // one accumulator per ky
+  // accumulators: one per ky (N = 96), or ky 0-1 and ky 2 (N = 48: 128 TMEM
+  // columns, so four CTAs fit an SM's TMEM)
+  static constexpr int NACC = N > 48 ? 3 : 2;
+  static constexpr int COLS = tmem_cols(NACC * N);
+  static constexpr int acc(int ky) { return NACC == 3 ? ky : (ky < 2 ? 0 : 1); }
 };
 
 // x: [*][CI][hi][wi] (sample idx[b] when idx) -> y: [m][CO][hi-2][wi-2].
@@ -209,29 +218,37 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
 #pragma unroll
         for (int ks = 0; ks < C::KP / 8; ++ks) {
           const uint32_t a = a0 + ky * kP * C::A_BYTES + ks * 256, bb = b0 + ky * kP * C::B_BYTES + ks * 256;
-          mma_terms(tmem + ky * C::N, a, C::A_BYTES, C::SBO, bb, C::B_BYTES, C::SBO, idesc, ks == 0);
+          mma_terms(tmem + C::acc(ky) * C::N, a, C::A_BYTES, C::SBO, bb, C::B_BYTES, C::SBO, idesc,
+                    ks == 0 && (C::NACC == 3 || ky != 1));
         }
       mma_commit(bar_s);
     }
     mma_wait(bar_s, phase);
     phase ^= 1u;
-    // epilogue: thread m = TMEM lane m.  The three ky accumulators are summed
-    // in FP32 with round-to-nearest; D0 stays in registers, D1 / D2 go to the
+    // epilogue: thread m = TMEM lane m.  The accumulators are summed in FP32
+    // with round-to-nearest; D0 stays in registers, D1 / D2 go to the
     // exchange (the A operands are dead: the MMAs completed)
     float d0[CO];
 #pragma unroll
     for (int o4 = 0; o4 < CO; o4 += 4) {
-      float v[3][3][4];   // [ky][kx][o]
+      float v[C::NACC][3][4];   // [accumulator][kx][o]
 #pragma unroll
-      for (int ky = 0; ky < 3; ++ky)
+      for (int a = 0; a < C::NACC; ++a)
 #pragma unroll
-        for (int kx = 0; kx < 3; ++kx) tmem_ld<4>(lrow + ky * C::N + kx * C::NB + o4, v[ky][kx]);
+        for (int kx = 0; kx < 3; ++kx) tmem_ld<4>(lrow + a * C::N + kx * C::NB + o4, v[a][kx]);
       tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        d0[o4 + j] = (v[0][0][j] + v[1][0][j]) + v[2][0][j];
-        xb[(o4 + j) * kXb + m] = (v[0][1][j] + v[1][1][j]) + v[2][1][j];
-        xb[(CO + o4 + j) * kXb + m] = (v[0][2][j] + v[1][2][j]) + v[2][2][j];
+        float s0 = v[0][0][j], s1 = v[0][1][j], s2 = v[0][2][j];
+#pragma unroll
+        for (int a = 1; a < C::NACC; ++a) {
+          s0 += v[a][0][j];
+          s1 += v[a][1][j];
+          s2 += v[a][2][j];
+        }
+        d0[o4 + j] = s0;
+        xb[(o4 + j) * kXb + m] = s1;
+        xb[(CO + o4 + j) * kXb + m] = s2;
       }
     }
     __syncthreads();
@@ -566,7 +583,8 @@ __global__ void __launch_bounds__(kThreads) tc_conv_wgrad(const float* __restric
   tmem_release(tmem, C::COLS);
 }
 
-// gradients from the partials of all layers, summed in a fixed order: layer
+// gradients from the per-CTA partials of all layers ([G][R][CO]; the head's
+// are the loss kernel's per-block sums), summed in a fixed order: layer
 // blockIdx.y, 32 outputs per block (OIHW order then the biases); group
 // threadIdx.y sums partials g = y, y + 8, ... (4 independent chains), then the
 // 8 group sums are added in group order
@@ -594,7 +612,9 @@ __global__ void __launch_bounds__(32 * kRedG) tc_wgrad_reduce(const __grid_const
     for (; g + 3 * kRedG < L.G; g += 4 * kRedG)
 #pragma unroll
       for (int q = 0; q < 4; ++q) s4[q] += p[(g + q * kRedG) * stride];
-    for (int q = 0; g < L.G; g += kRedG, ++q) s4[q] += p[g * stride];
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      if (g + q * kRedG < L.G) s4[q] += p[(g + q * kRedG) * stride];
   }
   red[g0][threadIdx.x] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
   __syncthreads();
