@@ -853,14 +853,49 @@ def _train_data(m: int):
     return x, t
 
 
+def train_graph_step_us(eb, dev, xd, td, reps: int = 10) -> float:
+    """Device time of one SGD step (forward + loss + backward + update, batch
+    8): an epoch of 256 steps captured as one CUDA graph through the trainer's
+    own calls, replayed `reps` times between CUDA events."""
+    import ctypes
+    import torch
+    from paper_2210_14771_b200 import training as tr
+    n, b = TRAIN_M, TRAIN_BATCH
+    trn = tr._Trainer(eb.EdgeNet(eb.ChannelStats((100.0,) * 3, (50.0,) * 3), seed=0), 7, WIDTH, b, dev)
+    order = torch.from_numpy(np.random.default_rng(0).permutation(n).astype(np.int32)).to(dev)
+    losses = torch.zeros(n // b, dtype=torch.float64, device=dev)
+
+    def epoch():
+        for k in range(n // b):
+            idx = ctypes.c_void_p(order.data_ptr() + 4 * k * b)
+            trn.forward(xd, idx, b)
+            trn.backward(xd, td, idx, b, losses[k:k + 1])
+            trn.sgd(1e-4)
+
+    epoch()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        epoch()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return 1e3 * e0.elapsed_time(e1) / (reps * (n // b))
+
+
 def train_leg(eb, dev) -> dict:
     """§8f-4: EdgeNet SGD training (edgenet.train) over 2048 synthetic RGBXY
     strips (5 x 7 x 1920, the learned variant's input) in batches of 8,
-    forward + BCE + backward + update on the GPU; wall clock of the public
-    call with the strips resident in HBM, synchronised.  Each call runs its
-    first epoch eagerly and captures the second as a CUDA graph, so the
-    steady per-step time is also given: the difference of a 16-epoch and a
-    4-epoch call (graph replays only) over the 12 x 256 extra steps."""
+    forward + BCE + backward + update on the GPU.  value: wall clock of the
+    public call over 16 epochs with the strips resident in HBM (its first
+    epoch runs eagerly, the second is captured as a CUDA graph, the rest
+    replay it); device_us_per_step: one step of a replayed epoch graph, CUDA
+    events."""
     import torch
     from paper_2210_14771_b200 import training as tr
     x, t = _train_data(TRAIN_M)
@@ -868,31 +903,30 @@ def train_leg(eb, dev) -> dict:
     net = eb.EdgeNet(eb.ChannelStats((100.0,) * 3, (50.0,) * 3), seed=0)
     tr.train(net, (xd[:64], td[:64]), None, tr.TrainConfig(learning_rate=0.001, batch_size=TRAIN_BATCH,
                                                             max_epochs=4))   # warm-up
-    wall = {}
-    for epochs in (4, 16):
-        cfg = tr.TrainConfig(learning_rate=0.001, batch_size=TRAIN_BATCH, max_epochs=epochs)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        tr.train(eb.EdgeNet(eb.ChannelStats((100.0,) * 3, (50.0,) * 3), seed=0), (xd, td), None, cfg)
-        torch.cuda.synchronize()
-        wall[epochs] = time.perf_counter() - t0
+    epochs = 16
+    cfg = tr.TrainConfig(learning_rate=0.001, batch_size=TRAIN_BATCH, max_epochs=epochs)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tr.train(eb.EdgeNet(eb.ChannelStats((100.0,) * 3, (50.0,) * 3), seed=0), (xd, td), None, cfg)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    dev_us = train_graph_step_us(eb, dev, xd, td)
     per_epoch = TRAIN_M // TRAIN_BATCH
-    steady = (wall[16] - wall[4]) / (12 * per_epoch)
     simt = os.environ.get("ECA_TRAIN_SIMT") == "1"
     return {"metric": "EdgeNet training samples/s (§8f-4: SGD epochs, batch 8 strips of 5x7x1920, "
                       "forward + BCE + backward + update)",
-            "value": round(16 * TRAIN_M / wall[16], 1), "unit": "samples/s",
-            "ms_per_step": round(1e3 * wall[16] / (16 * per_epoch), 4),
-            "steady_us_per_step": round(1e6 * steady, 1),
-            "steady_samples_per_s": round(TRAIN_BATCH / steady, 1),
-            "steps": 16 * per_epoch, "epochs": 16,
-            "launches_per_step": 16 if simt else 11,
+            "value": round(epochs * TRAIN_M / wall, 1), "unit": "samples/s",
+            "ms_per_step": round(1e3 * wall / (epochs * per_epoch), 4),
+            "device_us_per_step": round(dev_us, 1),
+            "device_samples_per_s": round(TRAIN_BATCH / dev_us * 1e6, 1),
+            "steps": epochs * per_epoch, "epochs": epochs,
+            "launches_per_step": 16 if simt else 12,
             "kernels": "SIMT FP32 (ECA_TRAIN_SIMT=1)" if simt else
                        "tcgen05 3xTF32 conv forward / dgrad / wgrad (eca_train_tc.cuh)",
             "dtype": "f32", "data": "synthetic normal strips",
-            "method": "wall clock of edgenet.train over 16 epochs of 2048 strips resident in HBM (epoch 1 "
-                      "eager, epoch 2 captured as a CUDA graph, then replays); steady = (16-epoch - 4-epoch "
-                      "wall) / (12 x 256 steps)"}
+            "method": "value: wall clock of edgenet.train over 16 epochs of 2048 strips resident in HBM "
+                      "(epoch 1 eager, epoch 2 captured as a CUDA graph, then replays); device: CUDA events "
+                      "around 10 replays of a captured 256-step epoch"}
 
 
 _CPU_TRAIN = None

@@ -27,6 +27,7 @@
 // rounding, not bitwise.
 #include <math.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <utility>
@@ -50,7 +51,7 @@ constexpr size_t kTcPart1 = size_t(ttc::kWgCtas) * ttc::WgCfg<8, 16, 3>::R * 16;
 constexpr size_t kTcPart2 = size_t(ttc::kWgCtas) * ttc::WgCfg<16, 32, 3>::R * 32;
 
 struct TrainWs {   // workspace layout (floats unless noted)
-  size_t a1, a2, a3, logit, d3, d2, d1, dlog, wpart, lpart, tcpart, hpart, total;
+  size_t a1, a2, a3, logit, d3, d2, d1, dlog, wpart, lpart, tcpart, hpart, bimg[5], total;
   int nseg3, nseg2, nseg1, nseg0, nlblk;
 };
 
@@ -83,6 +84,12 @@ TrainWs train_ws(int m, int h, int w) {
   L.lpart = o; o = up256(o + 8 * size_t(L.nlblk));
   L.tcpart = o; o = up256(o + 4 * (kTcPart0 + kTcPart1 + kTcPart2));
   L.hpart = o; o = up256(o + 4 * 33 * size_t(L.nlblk));
+  const size_t img[5] = {ttc::FwdCfg<5, 8>::BIMG, ttc::FwdCfg<8, 16>::BIMG, ttc::FwdCfg<16, 32>::BIMG,
+                         ttc::DgCfg<16, 32>::BIMG, ttc::DgCfg<8, 16>::BIMG};
+  for (int k = 0; k < 5; ++k) {
+    L.bimg[k] = o;
+    o = up256(o + img[k]);
+  }
   L.total = o;
   return L;
 }
@@ -431,40 +438,51 @@ TcPlan tc_plan(const void* kern, int need, int cols) {
     int dyn = int(share - int64_t(fa.sharedSizeBytes) - reserved);
     if (dyn < need) dyn = need;
     if (dyn > optin_max - int(fa.sharedSizeBytes)) dyn = optin_max - int(fa.sharedSizeBytes);
+    // CTAs per SM from the shared memory, registers and threads (the
+    // occupancy API answered 1 for these kernels where ncu shows 2-3
+    // resident; only the grid size depends on this, the TMEM bound comes
+    // from the padding above)
+    const int foot = dyn + int(fa.sharedSizeBytes) + reserved;
+    const int regs = (fa.numRegs + 7) / 8 * 8 * ttc::kThreads;
+    per_sm = sm_smem / foot;
+    if (regs > 0 && 65536 / regs < per_sm) per_sm = 65536 / regs;
+    if (2048 / ttc::kThreads < per_sm) per_sm = 2048 / ttc::kThreads;
     if (dyn >= need &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) == cudaSuccess &&
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ttc::kThreads, dyn) == cudaSuccess &&
         per_sm >= 1 && per_sm * cols <= 512)
       p = {dyn, per_sm * sms};
   }
+  if (std::getenv("ECA_TRAIN_PLAN_LOG"))
+    std::fprintf(stderr, "tc_plan %p need %d cols %d: static %zu dyn %d per_sm %d slots %d\n", kern, need, cols,
+                 size_t(fa.sharedSizeBytes), p.dyn, per_sm, p.slots);
   done.push_back({kern, dev, need, p});
   return p;
 }
 
 template <int CI, int CO, bool kHead>
-bool launch_fwd_tc(const float* x, const int32_t* idx, int m, int hi, int wi, const float* net, int ow,
-                   int ob, float* y, float* logit, cudaStream_t st) {
+bool launch_fwd_tc(const float* x, const int32_t* idx, int m, int hi, int wi, const float* net,
+                   const uint8_t* bimg, int ob, float* y, float* logit, cudaStream_t st) {
   using C = ttc::FwdCfg<CI, CO>;
   auto k = ttc::tc_conv_fwd<CI, CO, kHead>;
   const TcPlan p = tc_plan(reinterpret_cast<const void*>(k), C::SMEM, C::COLS);
   if (!p.slots) return false;
   const int64_t tiles = int64_t(m) * (hi - 2) * ((wi - 2 + ttc::kTOut - 1) / ttc::kTOut);
   k<<<unsigned(tiles < p.slots ? tiles : p.slots), ttc::kThreads, p.dyn, st>>>(
-      x, idx, m, hi, wi, net + ow, net + ob, kHead ? net + kOffW3 : nullptr, y, logit);
+      x, idx, m, hi, wi, bimg, net + ob, kHead ? net + kOffW3 : nullptr, y, logit);
   return true;
 }
 
 template <int CI, int CO>
-bool launch_dgrad_tc(const float* dy, const float* xin, int m, int hi, int wi, const float* wk, float* dx,
-                     cudaStream_t st) {
+bool launch_dgrad_tc(const float* dy, const float* xin, int m, int hi, int wi, const uint8_t* bimg,
+                     float* dx, cudaStream_t st) {
   using C = ttc::DgCfg<CI, CO>;
   auto k = ttc::tc_conv_dgrad<CI, CO>;
   const TcPlan p = tc_plan(reinterpret_cast<const void*>(k), C::smem(hi - 2), C::COLS);
   if (!p.slots) return false;
   const int64_t cap = p.slots;
   const int64_t tiles = int64_t(m) * hi * ((wi + ttc::kTOut - 1) / ttc::kTOut);
-  k<<<unsigned(tiles < cap ? tiles : cap), ttc::kThreads, p.dyn, st>>>(dy, xin, m, hi, wi, wk,
+  k<<<unsigned(tiles < cap ? tiles : cap), ttc::kThreads, p.dyn, st>>>(dy, xin, m, hi, wi, bimg,
                                                                      C::a_region(hi - 2), dx);
   return true;
 }
@@ -479,9 +497,10 @@ int launch_wgrad_tc(const float* dy, const float* x, const int32_t* idx, int m, 
   if (!p.slots) return 0;
   const int wo = wi - KS + 1;
   const int64_t units = int64_t(m) * (hi - KS + 1) * ((wo + ttc::kWgK - 1) / ttc::kWgK);
-  const int cap = p.slots < ttc::kWgCtas ? p.slots : ttc::kWgCtas;   // one wave
+  const int per_tile = p.slots / C::MT;   // one wave of (unit range, M tile) CTAs
+  const int cap = per_tile < ttc::kWgCtas ? per_tile : ttc::kWgCtas;
   const int g = int(units < cap ? units : cap);
-  k<<<g, ttc::kThreads, p.dyn, st>>>(dy, x, idx, m, hi, wi, part);
+  k<<<dim3(g, C::MT), ttc::kThreads, p.dyn, st>>>(dy, x, idx, m, hi, wi, part);
   return g;
 }
 
@@ -510,9 +529,14 @@ int eca_edgenet_forward(const float* x, const int32_t* index, int m, int h, int 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t plane = int64_t(h - 6) * (w - 6);
   if (!train_simt()) {   // tcgen05: three conv launches, the head fused into the last
-    if (!launch_fwd_tc<5, 8, false>(x, index, m, h, w, net, kOffW0, kOffB0, a1, nullptr, st) ||
-        !launch_fwd_tc<8, 16, false>(a1, nullptr, m, h - 2, w - 2, net, kOffW1, kOffB1, a2, nullptr, st) ||
-        !launch_fwd_tc<16, 32, true>(a2, nullptr, m, h - 4, w - 4, net, kOffW2, kOffB2, a3, logit, st))
+    const ttc::PackJob P{net + kOffW0, net + kOffW1, net + kOffW2, ws + L.bimg[0], ws + L.bimg[1],
+                         ws + L.bimg[2], ws + L.bimg[3], ws + L.bimg[4]};
+    ttc::tc_pack_weights<<<dim3((ttc::kPackMax + ttc::kPackThreads - 1) / ttc::kPackThreads, 5),
+                           ttc::kPackThreads, 0, st>>>(P);
+    if (!launch_fwd_tc<5, 8, false>(x, index, m, h, w, net, ws + L.bimg[0], kOffB0, a1, nullptr, st) ||
+        !launch_fwd_tc<8, 16, false>(a1, nullptr, m, h - 2, w - 2, net, ws + L.bimg[1], kOffB1, a2, nullptr,
+                                     st) ||
+        !launch_fwd_tc<16, 32, true>(a2, nullptr, m, h - 4, w - 4, net, ws + L.bimg[2], kOffB2, a3, logit, st))
       return ECA_ERR_CUDA;
   } else {
     conv3_fwd<5, 8, 1><<<dim3(blocks(int64_t(m) * (h - 2) * (w - 2), 128), 1), 128, 0, st>>>(
@@ -557,12 +581,14 @@ int eca_edgenet_backward(const float* x, const float* targets, const int32_t* in
     R.l[2] = {tp2, ttc::WgCfg<16, 32, 3>::R, 32,
               launch_wgrad_tc<16, 32, 3>(f(L.d3), f(L.a2), nullptr, m, h - 4, w - 4, tp2, st),
               out_grads + kOffW2, out_grads + kOffB2};
-    if (!launch_dgrad_tc<16, 32>(f(L.d3), f(L.a2), m, h - 4, w - 4, net + kOffW2, f(L.d2), st))
+    // the packed B operands of the forward on the same weights (backward
+    // always follows its forward in this workspace)
+    if (!launch_dgrad_tc<16, 32>(f(L.d3), f(L.a2), m, h - 4, w - 4, ws + L.bimg[3], f(L.d2), st))
       return ECA_ERR_CUDA;
     R.l[1] = {tp1, ttc::WgCfg<8, 16, 3>::R, 16,
               launch_wgrad_tc<8, 16, 3>(f(L.d2), f(L.a1), nullptr, m, h - 2, w - 2, tp1, st),
               out_grads + kOffW1, out_grads + kOffB1};
-    if (!launch_dgrad_tc<8, 16>(f(L.d2), f(L.a1), m, h - 2, w - 2, net + kOffW1, f(L.d1), st))
+    if (!launch_dgrad_tc<8, 16>(f(L.d2), f(L.a1), m, h - 2, w - 2, ws + L.bimg[4], f(L.d1), st))
       return ECA_ERR_CUDA;
     R.l[0] = {tp0, ttc::WgCfg<5, 8, 3>::R, 8, launch_wgrad_tc<5, 8, 3>(f(L.d1), x, index, m, h, w, tp0, st),
               out_grads + kOffW0, out_grads + kOffB0};

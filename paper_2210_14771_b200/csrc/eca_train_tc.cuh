@@ -126,6 +126,12 @@ ECA_DEV void tmem_release(uint32_t tmem, int cols) {
   if (threadIdx.x < 32) tmem_free(tmem, cols);
 }
 
+// 16-byte copy of `bytes` (a multiple of 16) by the CTA's threads
+ECA_DEV void copy16(uint8_t* dst, const uint8_t* src, int bytes) {
+  for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+}
+
 // ------------------------------------------------------------------ forward --
 template <int CI, int CO>
 struct FwdCfg {
@@ -137,6 +143,7 @@ struct FwdCfg {
   static constexpr int B_BYTES = N * KP * 4;
   static constexpr int A_REGION = cmax(3 * kP * A_BYTES, 2 * CO * kXb * 4);   // + exchange after the MMAs
   static constexpr int SMEM = A_REGION + 3 * kP * B_BYTES;
+  static constexpr int BIMG = 3 * kP * B_BYTES;  // the packed B operands (tc_pack_weights)
   // accumulators: one per ky (N = 96), or ky 0-1 and ky 2 (N = 48: 128 TMEM
   // columns, so four CTAs fit an SM's TMEM)
   static constexpr int NACC = N > 48 ? 3 : 2;
@@ -151,7 +158,7 @@ struct FwdCfg {
 template <int CI, int CO, bool kHead>
 __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict__ x,
                                                         const int32_t* __restrict__ idx, int m_, int hi,
-                                                        int wi, const float* __restrict__ wk,
+                                                        int wi, const uint8_t* __restrict__ bimg,
                                                         const float* __restrict__ bias,
                                                         const float* __restrict__ head, float* __restrict__ y,
                                                         float* __restrict__ logit) {
@@ -172,13 +179,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
     mbar_init(&bar, 1);
     fence_barrier_init();
   }
-  // B[ky]: row n = kx * NB + o, K = c  (w is OIHW)
-  for (int i = tid; i < 3 * C::N * C::KP; i += kThreads) {
-    const int c = i % C::KP, n = (i / C::KP) % C::N, ky = i / (C::KP * C::N);
-    const int kx = n / C::NB, o = n % C::NB;
-    const float v = (o < CO && c < CI) ? wk[((o * CI + c) * 3 + ky) * 3 + kx] : 0.f;
-    st_pieces1(B + ky * kP * C::B_BYTES, C::B_BYTES, kmaj_off(n, c, C::SBO), v);
-  }
+  copy16(B, bimg, C::BIMG);   // B[ky]: row n = kx * NB + o, K = c (pack_b_fwd)
   if (tid < CO) sbias[tid] = bias[tid];
   if (kHead) {
     if (tid < 32) sw3[tid] = head[tid];
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tslot, bar_s = smem_addr(&bar);
   const uint32_t lrow = tmem + (uint32_t(32 * warp) << 16);
-  const int64_t plane = int64_t(ho) * wo;
+  const int plane = ho * wo, iplane = hi * wi;   // < 2^31 (check_dims)
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int tx = tile % ntx, oy = (tile / ntx) % ho, b = tile / (ntx * ho);
@@ -196,12 +197,12 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
     const int s = idx ? idx[b] : b;
     {   // A[ky]: input row oy + ky, positions x0 + m (zero past the row), K = channels
       const bool in = x0 + m < wi;
-      const float* xs = x + (int64_t(s) * CI * hi + oy) * wi + x0 + m;
+      const float* xs = x + int64_t(s) * CI * iplane + oy * wi + x0 + m;
       float v[3][C::KP];
 #pragma unroll
       for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
-        for (int c = 0; c < C::KP; ++c) v[ky][c] = (in && c < CI) ? xs[(int64_t(c) * hi + ky) * wi] : 0.f;
+        for (int c = 0; c < C::KP; ++c) v[ky][c] = (in && c < CI) ? xs[c * iplane + ky * wi] : 0.f;
 #pragma unroll
       for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
     __syncthreads();
     const int ox = x0 + m;
     if (m < kTOut && ox < wo) {
-      float* yo = y + int64_t(b) * CO * plane + int64_t(oy) * wo + ox;
+      float* yo = y + int64_t(b) * CO * plane + oy * wo + ox;
       float z = 0.f;
 #pragma unroll
       for (int o = 0; o < CO; ++o) {
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
         yo[o * plane] = v;
         if (kHead) z = fmaf(sw3[o], v, z);
       }
-      if (kHead) logit[int64_t(b) * plane + int64_t(oy) * wo + ox] = z + sb3;
+      if (kHead) logit[int64_t(b) * plane + oy * wo + ox] = z + sb3;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();   // exchange reads done before the next tile's A (same bytes)
@@ -282,9 +283,10 @@ struct DgCfg {
   static constexpr int A_BYTES = kT * KP * 4;
   static constexpr int B_BYTES = N * KP * 4;
   static constexpr int XB = 2 * CI * kXb * 4;
-  static constexpr int NACC = KP / 8;            // one accumulator per K step
+  static constexpr int NACC = KP / 8 < 2 ? KP / 8 : 2;   // K steps alternate between two accumulators
   static constexpr int COLS = tmem_cols(NACC * N);
   // ky rows of dy that exist for some output row: min(3, ho) A slots
+  static constexpr int BIMG = 3 * kP * B_BYTES;  // the packed B operands (tc_pack_weights)
   static int a_region(int ho) { return cmax((ho < 3 ? ho : 3) * kP * A_BYTES, XB); }
   static int smem(int ho) { return a_region(ho) + 3 * kP * B_BYTES; }
 };
@@ -294,8 +296,8 @@ struct DgCfg {
 template <int CI, int CO>
 __global__ void __launch_bounds__(kThreads) tc_conv_dgrad(const float* __restrict__ dy,
                                                           const float* __restrict__ xin, int m_, int hi,
-                                                          int wi, const float* __restrict__ wk, int a_region,
-                                                          float* __restrict__ dx) {
+                                                          int wi, const uint8_t* __restrict__ bimg,
+                                                          int a_region, float* __restrict__ dx) {
   using C = DgCfg<CI, CO>;
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t bar;
@@ -311,17 +313,12 @@ __global__ void __launch_bounds__(kThreads) tc_conv_dgrad(const float* __restric
     mbar_init(&bar, 1);
     fence_barrier_init();
   }
-  for (int i = tid; i < 3 * C::N * C::KP; i += kThreads) {   // B[ky]: row n = kx * NB + c, K = o
-    const int o = i % C::KP, n = (i / C::KP) % C::N, ky = i / (C::KP * C::N);
-    const int kx = n / C::NB, c = n % C::NB;
-    const float v = c < CI ? wk[((o * CI + c) * 3 + ky) * 3 + kx] : 0.f;
-    st_pieces1(B + ky * kP * C::B_BYTES, C::B_BYTES, kmaj_off(n, o, C::SBO), v);
-  }
+  copy16(B, bimg, C::BIMG);   // B[ky]: row n = kx * NB + c, K = o (pack_b_dgrad)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tslot, bar_s = smem_addr(&bar);
   const uint32_t lrow = tmem + (uint32_t(32 * warp) << 16);
-  const int64_t plane = int64_t(hi) * wi, dplane = int64_t(ho) * wo;
+  const int plane = hi * wi, dplane = ho * wo;   // < 2^31 (check_dims)
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int tx = tile % ntx, yr = (tile / ntx) % hi, b = tile / (ntx * hi);
@@ -331,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_dgrad(const float* __restric
       const int p = x0 - 2 + m;
       const bool in = p >= 0 && p < wo;
       for (int ky = ky0; ky <= ky1; ++ky) {
-        const float* ds = dy + (int64_t(b) * CO * ho + (yr - ky)) * wo + p;
+        const float* ds = dy + int64_t(b) * CO * dplane + (yr - ky) * wo + p;
         uint8_t* ak = A + (ky - ky0) * kP * C::A_BYTES;
         float v[CO];
 #pragma unroll
@@ -350,17 +347,18 @@ __global__ void __launch_bounds__(kThreads) tc_conv_dgrad(const float* __restric
         for (int ks = 0; ks < C::KP / 8; ++ks) {
           const uint32_t a = a0 + (ky - ky0) * kP * C::A_BYTES + ks * 256;
           const uint32_t bb = b0 + ky * kP * C::B_BYTES + ks * 256;
-          mma_terms(tmem + ks * C::N, a, C::A_BYTES, C::SBO, bb, C::B_BYTES, C::SBO, idesc, ky == ky0);
+          mma_terms(tmem + (ks % C::NACC) * C::N, a, C::A_BYTES, C::SBO, bb, C::B_BYTES, C::SBO, idesc,
+                    ky == ky0 && ks < C::NACC);
         }
       mma_commit(bar_s);
     }
     mma_wait(bar_s, phase);
     phase ^= 1u;
-    // the K-step accumulators summed in FP32 (round-to-nearest)
+    // the accumulators summed in FP32 (round-to-nearest)
     float d2[CI];
 #pragma unroll
     for (int c4 = 0; c4 < CI; c4 += 4) {
-      float v[C::NACC][3][4];   // [ks][kx][c]
+      float v[C::NACC][3][4];   // [accumulator][kx][c]
 #pragma unroll
       for (int ks = 0; ks < C::NACC; ++ks)
 #pragma unroll
@@ -383,7 +381,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_dgrad(const float* __restric
     __syncthreads();
     const int xo = x0 + m;
     if (m < kTOut && xo < wi) {
-      const int64_t q0 = int64_t(b) * CI * plane + int64_t(yr) * wi + xo;
+      const int64_t q0 = int64_t(b) * CI * plane + yr * wi + xo;
 #pragma unroll
       for (int c = 0; c < CI; ++c) {
         const float v = (d2[c] + xb[c * kXb + m + 1]) + xb[(CI + c) * kXb + m + 2];
@@ -396,6 +394,48 @@ __global__ void __launch_bounds__(kThreads) tc_conv_dgrad(const float* __restric
   tmem_release(tmem, C::COLS);
 }
 
+// ------------------------------------------------------- packed B operands --
+// The conv kernels' B operands (weights as K-major TF32 pieces) are built once
+// per forward by tc_pack_weights into the workspace, in their shared-memory
+// layout, and copied by every CTA (instead of each CTA rebuilding them).
+// forward: B[ky][piece] row n = kx * NB + o, K = c; dgrad: row n = kx * NB + c, K = o.
+template <int CI, int CO>
+ECA_DEV void pack_b_fwd(uint8_t* dst, const float* __restrict__ wk, int i) {
+  using C = FwdCfg<CI, CO>;
+  if (i >= 3 * C::N * C::KP) return;
+  const int c = i % C::KP, n = (i / C::KP) % C::N, ky = i / (C::KP * C::N);
+  const int kx = n / C::NB, o = n % C::NB;
+  const float v = (o < CO && c < CI) ? wk[((o * CI + c) * 3 + ky) * 3 + kx] : 0.f;
+  st_pieces1(dst + ky * kP * C::B_BYTES, C::B_BYTES, kmaj_off(n, c, C::SBO), v);
+}
+template <int CI, int CO>
+ECA_DEV void pack_b_dgrad(uint8_t* dst, const float* __restrict__ wk, int i) {
+  using C = DgCfg<CI, CO>;
+  if (i >= 3 * C::N * C::KP) return;
+  const int o = i % C::KP, n = (i / C::KP) % C::N, ky = i / (C::KP * C::N);
+  const int kx = n / C::NB, c = n % C::NB;
+  const float v = c < CI ? wk[((o * CI + c) * 3 + ky) * 3 + kx] : 0.f;
+  st_pieces1(dst + ky * kP * C::B_BYTES, C::B_BYTES, kmaj_off(n, o, C::SBO), v);
+}
+struct PackJob {
+  const float *w0, *w1, *w2;   // OIHW kernels of the three 3x3 layers
+  uint8_t *f0, *f1, *f2, *d2, *d1;
+};
+constexpr int kPackThreads = 256;
+// blockIdx.y: forward 0, 1, 2, dgrad 2, 1; one element per thread
+__global__ void __launch_bounds__(kPackThreads) tc_pack_weights(const __grid_constant__ PackJob J) {
+  const int i = blockIdx.x * kPackThreads + threadIdx.x;
+  switch (blockIdx.y) {
+    case 0: pack_b_fwd<5, 8>(J.f0, J.w0, i); break;
+    case 1: pack_b_fwd<8, 16>(J.f1, J.w1, i); break;
+    case 2: pack_b_fwd<16, 32>(J.f2, J.w2, i); break;
+    case 3: pack_b_dgrad<16, 32>(J.d2, J.w2, i); break;
+    default: pack_b_dgrad<8, 16>(J.d1, J.w1, i); break;
+  }
+}
+constexpr int kPackMax = cmax(cmax(3 * FwdCfg<16, 32>::N * FwdCfg<16, 32>::KP, 3 * DgCfg<16, 32>::N * 32),
+                              3 * FwdCfg<5, 8>::N * FwdCfg<5, 8>::KP);
+
 // -------------------------------------------------------------------- wgrad --
 template <int CI, int CO, int KS>
 struct WgCfg {
@@ -404,7 +444,7 @@ struct WgCfg {
   static constexpr int NB = up16(CO);
   static constexpr int NKS = kWgK / 8;           // K steps per unit
   static constexpr int SBO = kWgK / 4 * 128;     // K = 32 positions
-  static constexpr int A_BYTES = MT * kT * kWgK * 4;
+  static constexpr int A_BYTES = kT * kWgK * 4;  // one M tile per CTA (blockIdx.y)
   static constexpr int B_BYTES = NB * kWgK * 4;
   static constexpr int STAGE = kP * A_BYTES + kP * B_BYTES;
   static constexpr int XW = kWgK + KS - 1;       // raw x columns of a unit
@@ -412,12 +452,12 @@ struct WgCfg {
   static constexpr int NX = (XR + kThreads - 1) / kThreads;                  // per thread
   static constexpr int NDC = (NB + 15) / 16;    // dy chunk rows per thread
   static constexpr int SMEM = 2 * STAGE + XR * 4;
-  static constexpr int ACC = NKS * MT * NB;      // TMEM columns of one unit: an accumulator per K step
+  static constexpr int ACC = NKS * NB;           // TMEM columns of one unit: an accumulator per K step
   static constexpr int COLS = tmem_cols(2 * ACC);
   static_assert(2 * ACC <= 512, "TMEM");
 };
 
-// partial[g][r][o] = sum over CTA g's units of x_row(r) . dy_row(o); a unit is
+// partial[g][o][r] = sum over CTA g's units of x_row(r) . dy_row(o); a unit is
 // (b, oy, 32 output columns); dy: [m][CO][hi-KS+1][wi-KS+1], x: [*][CI][hi][wi].
 // Per unit: the raw x rows (c, oy + ky) and the dy chunks were prefetched into
 // registers during the previous unit (coalesced); x goes through shared memory
@@ -433,7 +473,8 @@ __global__ void __launch_bounds__(kThreads) tc_conv_wgrad(const float* __restric
                                                           const int32_t* __restrict__ idx, int m_,
                                                           int hi, int wi, float* __restrict__ part) {
   using C = WgCfg<CI, CO, KS>;
-  constexpr int NA = (C::R + 15) / 16;   // A chunk rows per thread
+  const int mt = blockIdx.y, row0 = mt * kT;   // this CTA's M tile: rows row0 ..
+  constexpr int NA = (C::R < kT ? C::R + 15 : kT) / 16;   // A chunk rows per thread
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ uint32_t tslot;
@@ -461,40 +502,36 @@ __global__ void __launch_bounds__(kThreads) tc_conv_wgrad(const float* __restric
   int asrc[NA], adst[NA];   // A chunk: source in xr, destination in the operand
 #pragma unroll
   for (int q = 0; q < NA; ++q) {
-    const int r = rbase + 16 * q;
+    const int r = row0 + rbase + 16 * q;
     asrc[q] = r < C::R - 1 ? (r / (KS * KS)) * KS * C::XW + ((r / KS) % KS) * C::XW + r % KS + j4 : -1;
-    adst[q] = r < C::R ? kmaj_off(r, j4, C::SBO) : -1;
+    adst[q] = r < C::R ? kmaj_off(r - row0, j4, C::SBO) : -1;
   }
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tslot;
   const uint32_t lrow = tmem + (uint32_t(32 * warp) << 16);
-  float acc[C::MT][CO];
+  float acc[CO];
 #pragma unroll
-  for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-    for (int o = 0; o < CO; ++o) acc[mt][o] = 0.f;
+  for (int o = 0; o < CO; ++o) acc[o] = 0.f;
   // unit k's accumulators (buffer k & 1) -> registers, after its MMAs completed
   const auto drain = [&](int k) {
     mma_wait(smem_addr(&bars[k & 1]), uint32_t(k >> 1) & 1u);
     const uint32_t base = lrow + (k & 1) * C::ACC;
 #pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt)
+    for (int o4 = 0; o4 < CO; o4 += 4) {
+      float v[C::NKS][4];
 #pragma unroll
-      for (int o4 = 0; o4 < CO; o4 += 4) {
-        float v[C::NKS][4];
+      for (int ks = 0; ks < C::NKS; ++ks) tmem_ld<4>(base + ks * C::NB + o4, v[ks]);
+      tmem_ld_wait();
 #pragma unroll
-        for (int ks = 0; ks < C::NKS; ++ks) tmem_ld<4>(base + (ks * C::MT + mt) * C::NB + o4, v[ks]);
-        tmem_ld_wait();
+      for (int j = 0; j < 4; ++j) {
+        if (o4 + j >= CO) break;
+        float s = v[0][j];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (o4 + j >= CO) break;
-          float s = v[0][j];
-#pragma unroll
-          for (int ks = 1; ks < C::NKS; ++ks) s += v[ks][j];
-          acc[mt][o4 + j] += s;
-        }
+        for (int ks = 1; ks < C::NKS; ++ks) s += v[ks][j];
+        acc[o4 + j] += s;
       }
+    }
   };
   // the unit to fetch next, stepped without divisions
   int fxc = u0 % nxc, foy = (u0 / nxc) % ho, fb = u0 / (nxc * ho);
@@ -560,34 +597,27 @@ __global__ void __launch_bounds__(kThreads) tc_conv_wgrad(const float* __restric
       constexpr uint32_t idesc = idesc_tf32(C::NB);
 #pragma unroll
       for (int ks = 0; ks < C::NKS; ++ks)
-#pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) {
-          const uint32_t a = a0 + mt * (kT / 8) * C::SBO + ks * 256, bb = b0 + ks * 256;
-          mma_terms(tmem + st * C::ACC + (ks * C::MT + mt) * C::NB, a, C::A_BYTES, C::SBO, bb, C::B_BYTES,
-                    C::SBO, idesc, true);
-        }
+        mma_terms(tmem + st * C::ACC + ks * C::NB, a0 + ks * 256, C::A_BYTES, C::SBO, b0 + ks * 256, C::B_BYTES,
+                  C::SBO, idesc, true);
       mma_commit(smem_addr(&bars[st]));
     }
   }
   if (nu >= 2) drain(nu - 2);
   if (nu >= 1) drain(nu - 1);
   const int lane_row = 32 * warp + (tid & 31);
-  float* pg = part + int64_t(blockIdx.x) * C::R * CO;
+  float* pg = part + int64_t(blockIdx.x) * C::R * CO;   // [G][CO][R]: a warp's stores are contiguous
+  const int r = row0 + lane_row;
+  if (r < C::R)
 #pragma unroll
-  for (int mt = 0; mt < C::MT; ++mt) {
-    const int r = mt * kT + lane_row;
-    if (r < C::R)
-#pragma unroll
-      for (int o = 0; o < CO; ++o) pg[r * CO + o] = acc[mt][o];
-  }
+    for (int o = 0; o < CO; ++o) pg[o * C::R + r] = acc[o];
   tmem_release(tmem, C::COLS);
 }
 
-// gradients from the per-CTA partials of all layers ([G][R][CO]; the head's
+// gradients from the per-CTA partials of all layers ([G][CO][R]; the head's
 // are the loss kernel's per-block sums), summed in a fixed order: layer
 // blockIdx.y, 32 outputs per block (OIHW order then the biases); group
-// threadIdx.y sums partials g = y, y + 8, ... (4 independent chains), then the
-// 8 group sums are added in group order
+// threadIdx.y sums partials g = y, y + 32, ... (4 independent chains), then
+// the 32 group sums are added in group order
 struct WgLayer {
   const float* part;
   int R, CO, G;
@@ -596,7 +626,7 @@ struct WgLayer {
 struct WgReduceJob {
   WgLayer l[4];
 };
-constexpr int kRedG = 8;
+constexpr int kRedG = 32;
 __global__ void __launch_bounds__(32 * kRedG) tc_wgrad_reduce(const __grid_constant__ WgReduceJob J) {
   __shared__ float red[kRedG][32];
   const WgLayer& L = J.l[blockIdx.y];
@@ -607,7 +637,7 @@ __global__ void __launch_bounds__(32 * kRedG) tc_wgrad_reduce(const __grid_const
   const int64_t stride = int64_t(L.R) * L.CO;
   float s4[4] = {0.f, 0.f, 0.f, 0.f};
   if (i < n) {
-    const float* p = L.part + r * L.CO + o;
+    const float* p = L.part + o * L.R + r;
     int g = g0;
     for (; g + 3 * kRedG < L.G; g += 4 * kRedG)
 #pragma unroll
