@@ -322,10 +322,13 @@ int eca_hausdorff_points(const double* a, int na, const double* b, int nb, void*
  * sample indices of this batch, each < the number of samples in x / targets
  * (device int32; null: samples 0..m-1).  net: ECA_NET_FLOATS
  * packed weights (kernel0, bias0, ..., kernel3, bias3 in reference order).
- * forward keeps the activations in the workspace (the reference's caches);
- * backward (after forward on the same batch) writes the mean stable BCE loss
+ * forward keeps the activations (the reference's caches) and the packed
+ * tensor-core weight operands in the workspace; backward (after forward on
+ * the same batch, weights and workspace) writes the mean stable BCE loss
  * (FP64), the packed gradients (out_grads null: the loss only), and sets
- * *diverged = 1 on a non-finite loss (diverged may be null).
+ * *diverged = 1 on a non-finite loss (diverged may be null).  The
+ * convolutions run on tcgen05 (3xTF32, eca_train_tc.cuh); ECA_TRAIN_SIMT=1
+ * selects the CUDA-core kernels.
  * eca_sgd_step: net -= fl32(lr) * grads, skipped while *diverged != 0. */
 int eca_train_workspace_bytes(int m, int h, int w, int64_t* bytes);
 int eca_edgenet_forward(const float* x, const int32_t* index, int m, int h, int w, const float* net,
