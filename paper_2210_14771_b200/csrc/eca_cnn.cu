@@ -250,12 +250,13 @@ __global__ void __launch_bounds__(256, 2) cnn_kernel(const __grid_constant__ Cnn
 // layout (8-row x 16-byte core matrices), split hi/lo for 3xTF32
 // (hi*hi + hi*lo + lo*hi: FP32-level error, tools/umma_test.cu).  128 MMA
 // positions give 122 valid outputs per tile (the 3x3 halo of three layers).
-//   layer 0: per output row one N = 48 chain: 3 ky x 3 split terms, 45 MMAs
+//   layer 0: per output row one N = 32 chain (the three 8-row kx blocks
+//            adjacent): 3 ky x 3 split terms, 45 MMAs
 //   layer 1: per output row one N = 48 MMA chain (the 3 kx weight blocks
 //            stacked as rows of B): 3 ky x 3 split terms, 27 MMAs
 //   layer 2: one N = 96 chain: 3 ky x 2 K-steps x 3 terms, 18 MMAs
 // TMEM: 256 columns per group, reused by the three layers in turn (layer 0
-// [0, 240), layer 1 [0, 144), layer 2 [0, 96)).
+// [0, 160), layer 1 [0, 144), layer 2 [0, 96)).
 constexpr int kTP = 128, kTOut = kTP - 6;   // 3 layers x 2 columns of halo
 constexpr int kSbo1 = 2 * 128, kSbo2 = 4 * 128;       // K = 8 / 16 channels
 constexpr int kA1 = 16 * kSbo1, kA2 = 16 * kSbo2;     // one row operand (128 positions)
@@ -304,14 +305,15 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   const float* wg = J.weights;
 
   // ---- weights -> smem as K-major hi/lo operands [hi/lo][ky][kx][out][in];
-  // layer 0's 8 x 5 blocks zero-padded to 16 x 8 ----
+  // layer 0: per ky one 32 x 8 operand, rows kx * 8 + o (the three 8-output
+  // kx blocks adjacent, rows 24..31 and input lanes 5..7 zero) ----
   for (int i = tid; i < 2 * 9 * kWt1 / 4; i += nt) reinterpret_cast<float*>(&s.b0[0][0][0][0])[i] = 0.f;
   __syncthreads();
   for (int i = tid; i < kW0; i += nt) {   // i = ((o*5 + c)*3 + ky)*3 + kx
     const int o = i / 45, c = (i / 9) % 5, ky = (i % 9) / 3, kx = i % 3;
     const float v = wg[i], hi = tf32_rna(v);
-    *reinterpret_cast<float*>(s.b0[0][ky][kx] + kmaj_off(o, c, kSbo1)) = hi;
-    *reinterpret_cast<float*>(s.b0[1][ky][kx] + kmaj_off(o, c, kSbo1)) = tf32_rna(v - hi);
+    *reinterpret_cast<float*>(s.b0[0][ky][0] + kmaj_off(kx * 8 + o, c, kSbo1)) = hi;
+    *reinterpret_cast<float*>(s.b0[1][ky][0] + kmaj_off(kx * 8 + o, c, kSbo1)) = tf32_rna(v - hi);
   }
   for (int i = tid; i < kW1; i += nt) {   // i = ((o*8 + c)*3 + ky)*3 + kx
     const int o = i / 72, c = (i / 9) % 8, ky = (i % 9) / 3, kx = i % 3;
@@ -439,12 +441,12 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
   publish_group(grp);
 
   // ---- layer 0 (tensor cores): D0[r][kx] = sum_ky a0[r + ky] . b0[ky][kx],
-  // N = 48 (three zero-padded 16-row kx blocks) ----
+  // N = 32 (three adjacent 8-row kx blocks + 8 zero rows) ----
   if (gw < 5 && lane == 0) {   // output row r = gw
-    constexpr uint32_t id0 = idesc_tf32(48);
+    constexpr uint32_t id0 = idesc_tf32(32);
     const int r = gw;
     for (int ky = 0; ky < 3; ++ky)
-      mma3(tmem + uint32_t(r * 48), saddr(a0(r + ky, 0)), saddr(a0(r + ky, 1)), kSbo1,
+      mma3(tmem + uint32_t(r * 32), saddr(a0(r + ky, 0)), saddr(a0(r + ky, 1)), kSbo1,
            saddr(s.b0[0][ky][0]), saddr(s.b0[1][ky][0]), kSbo1, id0, ky == 0);
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0)
                  : "memory");
@@ -461,7 +463,7 @@ __global__ void __launch_bounds__(512, 1) cnn_kernel_tc(const __grid_constant__ 
 #pragma unroll
     for (int r = 0; r < 5; ++r)
 #pragma unroll
-      for (int kx = 0; kx < 3; ++kx) tmem_ld<4>(lane_base + uint32_t(r * 48 + kx * 16 + 4 * ch), d[r][kx]);
+      for (int kx = 0; kx < 3; ++kx) tmem_ld<4>(lane_base + uint32_t(r * 32 + kx * 8 + 4 * ch), d[r][kx]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     float* xch = G.xch;   // [r][q][lane][kx-1][8]
     if (lane < 2) {
