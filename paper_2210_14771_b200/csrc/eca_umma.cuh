@@ -35,8 +35,10 @@ ECA_DEV void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, u
 ECA_DEV void mma3(uint32_t tmem, uint32_t a_hi, uint32_t a_lo, int sboa, uint32_t b_hi, uint32_t b_lo,
                   int sbob, uint32_t idesc, bool first) {
   mma_tf32(tmem, umma_desc(a_hi, sboa), umma_desc(b_hi, sbob), idesc, first ? 0u : 1u);
+#ifndef ECA_EXPERIMENT_MMA1   // timing experiment only: wrong numerics
   mma_tf32(tmem, umma_desc(a_hi, sboa), umma_desc(b_lo, sbob), idesc, 1u);
   mma_tf32(tmem, umma_desc(a_lo, sboa), umma_desc(b_hi, sbob), idesc, 1u);
+#endif
 }
 ECA_DEV void st_hilo(uint8_t* hi, uint8_t* lo, int off, float4 v) {
   float4 h, l;
