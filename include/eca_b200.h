@@ -233,9 +233,12 @@ int eca_fit(const int32_t* cand_x, const int32_t* cand_y, const double* cand_sco
  * scoring with the survivors rescored in FP64 by the same warp, candidates,
  * then filter + RANSAC in a fit kernel launched programmatically behind it.
  * `counters` = max(batch, 64) int32 zeros (scratch: left zeroed on return).
- * The candidate outputs double as the fitter's input.  (ECA_LATENCY_STRIP=1
- * in the environment: the older single launch, a block-per-strip kernel
- * whose last CTA per frame fits it.) */
+ * The candidate outputs double as the fitter's input.  `out` may be mapped
+ * pinned host memory: each record's status word is written last, after a
+ * system-scope fence, so a host that set it to a value outside EcaStatus can
+ * poll it instead of synchronising the stream.  (ECA_LATENCY_STRIP=1 in the
+ * environment: the older single launch, a block-per-strip kernel whose last
+ * CTA per frame fits it; no ordered store.) */
 int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_t frame_stride,
                              int64_t row_stride, const int32_t* strip_rows,
                              const int32_t* band_rows, int n_strips,

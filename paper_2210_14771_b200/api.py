@@ -569,7 +569,9 @@ class _FrameEstimator:
     """estimate() of ONE handcrafted frame of a fixed (H, W, cfg, seed, device),
     everything preallocated: one fused launch (strip scoring -> candidates ->
     filter -> RANSAC, eca_estimate_handcrafted) whose fit writes the record
-    straight into pinned host memory, then a stream synchronisation.  Host
+    straight into pinned host memory, status word last; the host polls that
+    word (a bounded spin, then a stream synchronisation that also raises any
+    kernel error) instead of waking from a synchronisation.  Host
     frames: the 3 rows of every strip are copied into a pinned buffer that the
     kernel reads over PCIe (no H2D copy, no full-frame transfer).  A lock
     serialises callers (the buffers are shared)."""
@@ -590,6 +592,7 @@ class _FrameEstimator:
             self.sc = torch.empty((1, 2 * s), dtype=torch.float64, device=device)
         self.rec_host = torch.zeros((1, 5), dtype=torch.float64).pin_memory()
         self.rec_np = self.rec_host.numpy()
+        self.rec_i32 = self.rec_np.view(np.int32).reshape(-1)   # [9]: the status word
         self.bands_host = torch.empty((3 * s, width, 3), dtype=torch.uint8).pin_memory()
         self.bands_np = self.bands_host.numpy()
         self.row_idx = np.array([r + d for r in self.rows for d in (-1, 0, 1)], dtype=np.intp)
@@ -615,14 +618,36 @@ class _FrameEstimator:
             a = frame.numpy() if isinstance(frame, torch.Tensor) else frame
             np.take(a, self.row_idx, axis=0, out=self.bands_np)
             ptr, rs, band = ctypes.c_void_p(self.bands_host.data_ptr()), 3 * self.w, self.c_band
-        stream = torch.cuda.current_stream(self.dev)
+        raw = _raw_stream(self.dev)
+        st32 = self.rec_i32
+        st32[9] = _PENDING
         _lib.check(self.fn(ptr, 1, 0, rs, self.c_rows, band, self.s, self.p_params, *self.args,
-                           ctypes.c_void_p(stream.cuda_stream)), "eca_estimate_handcrafted")
-        stream.synchronize()
+                           ctypes.c_void_p(raw)), "eca_estimate_handcrafted")
+        spins = 0
+        while st32[9] == _PENDING:
+            spins += 1
+            if spins & 0x3FF == 0 and spins > _SPIN_LIMIT:
+                torch.cuda.current_stream(self.dev).synchronize()   # raises a kernel error
+                if st32[9] == _PENDING:
+                    raise _lib.EcaError("eca_estimate_handcrafted: the record was not written")
         r = self.rec_np[0]
-        if int(r.view(np.int32)[9]) == _lib.ACCEPTED:
+        if int(st32[9]) == _lib.ACCEPTED:
             return CircularArea(Circle(float(r[0]), float(r[1]), float(r[2])), float(r[3]))
         return FULL_FRAME
+
+
+_PENDING = -0x7FFFFFFF        # a status value outside EcaStatus: "not written yet"
+_SPIN_LIMIT = 1 << 16          # polls of the status word before a stream synchronisation
+try:                           # the current stream's raw handle without a Stream object
+    _RAW_STREAM = torch._C._cuda_getCurrentRawStream
+except AttributeError:         # pragma: no cover
+    _RAW_STREAM = None
+
+
+def _raw_stream(dev: torch.device) -> int:
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(dev.index)
+    return torch.cuda.current_stream(dev).cuda_stream
 
 
 _FRAME_ESTIMATORS: dict = {}

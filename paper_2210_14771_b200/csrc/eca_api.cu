@@ -337,6 +337,7 @@ struct FitJob {
   const int16_t* trip;
   EcaFitRecord* out;
   EcaFitRecord* host_out;   // optional mapped pinned copy of the records
+  int ordered;              // out: status word last, after a system-scope fence
   int32_t* guard;           // set-reuse guard ticket block (pipelines) or null
   int wait_prev;            // griddepcontrol.wait: the inputs come from the
                             // kernel before this one (programmatic launch)
@@ -495,10 +496,11 @@ __global__ void __launch_bounds__(256) fit_kernel(const __grid_constant__ FitJob
       fit_warp<false>(reinterpret_cast<const int32_t*>(mine + L.cx),
                       reinterpret_cast<const int32_t*>(mine + L.cy),
                       reinterpret_cast<const double*>(mine + L.cs), J.n_cand, J.p, J.trip,
-                      J.exhaustive, pt, ps, J.out + b);
+                      J.exhaustive, pt, ps, J.out + b, J.ordered != 0);
     } else {
       const size_t o = size_t(b) * J.n_cand;
-      fit_warp(J.x + o, J.y + o, J.s + o, J.n_cand, J.p, J.trip, J.exhaustive, pt, ps, J.out + b);
+      fit_warp(J.x + o, J.y + o, J.s + o, J.n_cand, J.p, J.trip, J.exhaustive, pt, ps, J.out + b,
+               J.ordered != 0);
     }
     if (J.host_out && lane == 0) J.host_out[b] = J.out[b];
   }
@@ -719,6 +721,7 @@ extern "C" int eca_estimate_handcrafted(const uint8_t* frames, int batch, int64_
     F.p = J.p;
     F.trip = triplets;
     F.out = out;
+    F.ordered = 1;   // `out` may be mapped pinned memory the caller polls
     F.wait_prev = 1;
     return launch_fit(F, batch, st, /*overlap=*/true);
   }

@@ -268,10 +268,28 @@ __device__ unsigned long long g_fit_times[16 * 4096];
 // pt / ps: shared scratch for n_cand points (FitScratchW, or n_cand-sized).
 // kCG: the candidates are in global memory, written by other CTAs of the same
 // kernel (L2 loads); otherwise any memory this warp wrote (e.g. shared).
+// the record store; ordered: every field, a system-scope fence, then the
+// status word -- a host polling mapped pinned memory for the status sees the
+// complete record (the single-frame latency path)
+ECA_DEV void store_record(EcaFitRecord* out, const EcaFitRecord& rec, bool ordered) {
+  if (!ordered) {
+    *out = rec;
+    return;
+  }
+  volatile EcaFitRecord* v = out;
+  v->cx = rec.cx;
+  v->cy = rec.cy;
+  v->r = rec.r;
+  v->score = rec.score;
+  v->inliers = rec.inliers;
+  __threadfence_system();
+  v->status = rec.status;
+}
+
 template <bool kCG = true>
 ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double* cand_s,
                       int n_cand, const EcaParams& p, const int16_t* trip, int exhaustive,
-                      FitPt* pt, double* ps, EcaFitRecord* out) {
+                      FitPt* pt, double* ps, EcaFitRecord* out, bool ordered = false) {
   const int lane = threadIdx.x & 31;
   const int W = p.width, H = p.height;
   FIT_STAMP(0);
@@ -316,7 +334,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
   __syncwarp();
   FIT_STAMP(1);
   if (n < 3) {
-    if (lane == 0) *out = EcaFitRecord{0.0, 0.0, 0.0, 0.0, 0, ECA_NO_CANDIDATES};
+    if (lane == 0) store_record(out, EcaFitRecord{0.0, 0.0, 0.0, 0.0, 0, ECA_NO_CANDIDATES}, ordered);
     __syncwarp();
     return;
   }
@@ -431,7 +449,7 @@ ECA_DEV void fit_warp(const int32_t* cand_x, const int32_t* cand_y, const double
       rec.score = best_s;
       rec.inliers = best_inl;
     }
-    *out = rec;
+    store_record(out, rec, ordered);
   }
   FIT_STAMP(7);
   __syncwarp();

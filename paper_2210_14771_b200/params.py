@@ -95,5 +95,13 @@ class EcaParams(ctypes.Structure):
     ]
 
 
+_DEFAULT: EcaConfig | None = None
+
+
 def config_default() -> EcaConfig:
-    return EcaConfig()
+    """The default configuration (config.py:76-77).  EcaConfig is frozen, so
+    one shared instance is returned (built once: construction validates)."""
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = EcaConfig()
+    return _DEFAULT
