@@ -497,7 +497,12 @@ int launch_wgrad_tc(const float* dy, const float* x, const int32_t* idx, int m, 
   if (!p.slots) return 0;
   const int wo = wi - KS + 1;
   const int64_t units = int64_t(m) * (hi - KS + 1) * ((wo + ttc::kWgK - 1) / ttc::kWgK);
-  const int per_tile = p.slots / C::MT;   // one wave of (unit range, M tile) CTAs
+  int per_tile = p.slots / C::MT;   // one wave of (unit range, M tile) CTAs
+  static const int force_g = [] {   // diagnostics: ECA_WG_CTAS=<weight-gradient CTAs per M tile>
+    const char* e = std::getenv("ECA_WG_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force_g > 0 && force_g < per_tile) per_tile = force_g;
   const int cap = per_tile < ttc::kWgCtas ? per_tile : ttc::kWgCtas;
   const int g = int(units < cap ? units : cap);
   k<<<dim3(g, C::MT), ttc::kThreads, p.dyn, st>>>(dy, x, idx, m, hi, wi, part);

@@ -113,3 +113,60 @@ def test_training_rejects_bad_input():
         tr.train(net, (np.zeros((0, 5, 7, 20), np.float32), np.zeros((0, 1, 1, 14), np.float32)), None)
     with pytest.raises(ValueError, match="receptive field"):
         tr.forward_logits(net, np.zeros((1, 5, 6, 20), np.float32))
+
+
+def test_gradients_many_tiles_per_cta():
+    """64 strips x 1920: every persistent conv CTA loops over several tiles
+    and every weight-gradient CTA over several 32-column units (ragged row
+    ends included), against the oracle.  Inputs, weights and biases are
+    non-negative / positive so no pre-activation is near 0: at this size a
+    value within FP32 rounding of 0 can get different ReLU masks on the two
+    sides (a near-tie: one flipped unit moves a gradient element by a whole
+    term, K7); this test is about the tiling, not ties."""
+    from paper_2210_14771_b200.stripnet import ConvLayer
+
+    rng = np.random.default_rng(17)
+    x = np.abs(rng.normal(0.0, 1.0, (64, 5, 7, 1920))).astype(np.float32)
+    t = rng.uniform(0.0, 1.0, (64, 1, 1, 1914)).astype(np.float32)
+    net = _net(seed=5)
+    net.layers = [ConvLayer(np.abs(l.kernel), np.full_like(l.bias, 0.1)) if i < 3 else l
+                  for i, l in enumerate(net.layers)]
+    layers = [(l.kernel, l.bias) for l in net.layers]
+    want_logits, _ = orc.forward_logits(x, layers)
+    assert np.abs(tr.forward_logits(net, x) - want_logits).max() <= 1e-5 * max(1.0, np.abs(want_logits).max())
+    loss, grads = tr.gradients(net, x, t)
+    want_loss, want_grads, _ = orc.train_step(x, t, layers, 0.0)
+    assert loss == pytest.approx(want_loss, rel=1e-6)
+    _grad_close(_pack(grads), _pack(want_grads))
+
+
+def test_concurrent_streams_match_sequential():
+    """Two trainers stepping on two streams at once (their tensor-core CTAs
+    share SMs: the shared-memory padding must keep their TMEM allocations
+    within 512 columns per SM) give the results of running them one after
+    the other."""
+    import torch
+
+    rng = np.random.default_rng(23)
+    dev = torch.device("cuda", 0)
+    xs = [torch.from_numpy(rng.normal(0.0, 1.0, (16, 5, 7, 1920)).astype(np.float32)).to(dev) for _ in range(2)]
+    ts = [torch.from_numpy(rng.uniform(0.0, 1.0, (16, 1, 1, 1914)).astype(np.float32)).to(dev) for _ in range(2)]
+
+    def run(concurrent: bool):
+        trainers = [tr._Trainer(_net(seed=k), 7, 1920, 16, dev) for k in range(2)]
+        losses = [torch.zeros(8, dtype=torch.float64, device=dev) for _ in range(2)]
+        streams = [torch.cuda.Stream(dev) for _ in range(2)]
+        torch.cuda.synchronize()
+        for step in range(8):
+            for k in range(2):
+                with torch.cuda.stream(streams[k] if concurrent else streams[0]):
+                    trainers[k].forward(xs[k], None, 16)
+                    trainers[k].backward(xs[k], ts[k], None, 16, losses[k][step:step + 1])
+                    trainers[k].sgd(0.05)
+        torch.cuda.synchronize()
+        return [t.weights.cpu().numpy() for t in trainers], [l.cpu().numpy() for l in losses]
+
+    w_seq, l_seq = run(False)
+    w_con, l_con = run(True)
+    for a, b in zip(w_seq + l_seq, w_con + l_con):
+        assert np.array_equal(a, b)

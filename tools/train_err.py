@@ -15,7 +15,10 @@ from oracle import eca_oracle as orc  # noqa: E402
 from paper_2210_14771_b200 import training as tr  # noqa: E402
 
 tag = "simt" if os.environ.get("ECA_TRAIN_SIMT") == "1" else "tc"
-for (h, w, m) in [(7, 40, 4), (7, 1920, 8), (11, 300, 2)]:
+shapes = [(7, 40, 4), (7, 1920, 8), (11, 300, 2)]
+if len(sys.argv) > 1:   # h,w,m triples: python tools/train_err.py 7,1920,64
+    shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
+for (h, w, m) in shapes:
     rng = np.random.default_rng(h * w + m)
     x = rng.normal(0.0, 1.0, (m, 5, h, w)).astype(np.float32)
     t = rng.uniform(0.0, 1.0, (m, 1, h - 6, w - 6)).astype(np.float32)
