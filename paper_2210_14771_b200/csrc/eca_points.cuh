@@ -120,6 +120,17 @@ ECA_DEV void issue_item_half(const PointsJob& PJ, int item, uint8_t* stage, uint
   }
 }
 
+#ifndef ECA_COLD_FLUSH
+#define ECA_COLD_FLUSH 1
+#endif
+// the FP64 score of a list entry outside the kernel body (the overflow path
+// runs on a few percent of half rows; inlined, its ~700 FP64 instructions sit
+// between the hot blocks)
+__device__ __noinline__ double score_entry_cold(uint32_t v, const uint8_t* st, const int* rb, int y, double cxf,
+                                                double cyf, const EcaParams& p, int& x) {
+  return score_entry(v, st, rb, y, cxf, cyf, p, x);
+}
+
 // RGB sums of the 10 pixels x0-1 .. x0+8 of one staged row; B = smem byte of
 // pixel x0.  `al`: B % 8 == 0 (warp-uniform), else funnel-shifted word loads.
 ECA_DEV void load10(const uint8_t* st, int B, bool al, int s[10]) {
@@ -387,7 +398,11 @@ __global__ void __maxnreg__(ECA_BOUNDS_MAXREG) bounds_kernel(const __grid_consta
     auto flush = [&]() {   // rare: score the pending survivors in this warp
       for (int k = lane; k < n_list; k += 32) {
         int x;
+#if ECA_COLD_FLUSH
+        const double s = score_entry_cold(list[k], st, rb, y, cxf, cyf, J.p, x);
+#else
         const double s = score_entry(list[k], st, rb, y, cxf, cyf, J.p, x);
+#endif
         if (better(s, x, best.s, best.x, !half)) best = Best{s, x};
       }
       n_list = 0;
