@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
       for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
         for (int c = 0; c < C::KP; ++c) v[ky][c] = (in && c < CI) ? xs[c * iplane + ky * wi] : 0.f;
+      ECA_CHECK(s >= 0 && oy + 2 < hi && x0 < wi);
 #pragma unroll
       for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
     __syncthreads();
     const int ox = x0 + m;
     if (m < kTOut && ox < wo) {
+      ECA_CHECK(b < m_ && oy < ho);
       float* yo = y + int64_t(b) * CO * plane + oy * wo + ox;
       float z = 0.f;
 #pragma unroll
@@ -324,6 +326,8 @@ __global__ void __launch_bounds__(kThreads) tc_conv_dgrad(const float* __restric
     const int tx = tile % ntx, yr = (tile / ntx) % hi, b = tile / (ntx * hi);
     const int x0 = tx * kTOut;
     const int ky0 = yr - ho + 1 > 0 ? yr - ho + 1 : 0, ky1 = yr < 2 ? yr : 2;   // 0 <= yr - ky < ho
+    // the slots used fit the A region sized for min(3, ho) rows
+    ECA_CHECK(ky1 >= ky0 && (ky1 - ky0 + 1) * kP * C::A_BYTES <= a_region && b < m_);
     {   // A[slot]: dy row yr - ky, positions x0 - 2 + m (zero outside the row)
       const int p = x0 - 2 + m;
       const bool in = p >= 0 && p < wo;
@@ -505,6 +509,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_wgrad(const float* __restric
     const int r = row0 + rbase + 16 * q;
     asrc[q] = r < C::R - 1 ? (r / (KS * KS)) * KS * C::XW + ((r / KS) % KS) * C::XW + r % KS + j4 : -1;
     adst[q] = r < C::R ? kmaj_off(r - row0, j4, C::SBO) : -1;
+    ECA_CHECK(asrc[q] + 3 < C::XR && adst[q] + 16 <= C::A_BYTES && (r - row0 < kT || adst[q] < 0));
   }
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -539,6 +544,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_wgrad(const float* __restric
   int fx0 = 0;
   const auto fetch = [&]() {
     const int x0 = fxc * kWgK, s = idx ? idx[fb] : fb;
+    ECA_CHECK(fb < m_ && foy < ho && s >= 0);
     const float* xs = x + (int64_t(s) * CI * hi + foy) * wi + x0;
 #pragma unroll
     for (int q = 0; q < C::NX; ++q) px[q] = x0 + xcol[q] < wi ? xs[xoff[q]] : 0.f;
@@ -607,6 +613,7 @@ __global__ void __launch_bounds__(kThreads) tc_conv_wgrad(const float* __restric
   const int lane_row = 32 * warp + (tid & 31);
   float* pg = part + int64_t(blockIdx.x) * C::R * CO;   // [G][CO][R]: a warp's stores are contiguous
   const int r = row0 + lane_row;
+  ECA_CHECK(int(blockIdx.x) < kWgCtas);
   if (r < C::R)
 #pragma unroll
     for (int o = 0; o < CO; ++o) pg[o * C::R + r] = acc[o];
