@@ -920,7 +920,7 @@ def train_leg(eb, dev) -> dict:
             "device_us_per_step": round(dev_us, 1),
             "device_samples_per_s": round(TRAIN_BATCH / dev_us * 1e6, 1),
             "steps": epochs * per_epoch, "epochs": epochs,
-            "launches_per_step": 16 if simt else 12,
+            "launches_per_step": 16 if simt else 10,
             "kernels": "SIMT FP32 (ECA_TRAIN_SIMT=1)" if simt else
                        "tcgen05 3xTF32 conv forward / dgrad / wgrad (eca_train_tc.cuh)",
             "dtype": "f32", "data": "synthetic normal strips",

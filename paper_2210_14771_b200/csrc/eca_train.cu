@@ -6,17 +6,18 @@
 // into them (the epoch permutation), gathered inside the first kernels.
 //
 // Default: the convolutions on the tensor cores (eca_train_tc.cuh, tcgen05
-// 3xTF32; 11 launches per SGD step):
-//  forward    tc_conv_fwd x3 (3x3 valid conv + bias + ReLU; the last one also
-//             computes the 1x1 head's logits); activations stay in the
-//             workspace (the reference's caches; ReLU masks are y > 0).
+// 3xTF32; 10 launches per SGD step):
+//  forward    tc_conv_fwd x3 (3x3 valid conv + bias + ReLU; the first also
+//             packs the later kernels' weight operands, the last computes the
+//             1x1 head's logits); activations stay in the workspace (the
+//             reference's caches; ReLU masks are y > 0).
 //  backward   loss_head_kernel: stable BCE terms in FP64 (edgenet.py:236-241),
 //             dlogits = (sigmoid(z) - t) / N in FP32 (:315), the head's input
-//             gradient and block partials of its weight gradient; loss_final;
-//             per 3x3 layer tc_conv_wgrad (partials per CTA) and tc_conv_dgrad
-//             (x the previous layer's ReLU mask; not for layer 0);
-//             tc_wgrad_reduce sums all partials in a fixed order
-//             (deterministic, no float atomics).
+//             gradient and block partials of its weight gradient; per 3x3
+//             layer tc_conv_wgrad (partials per CTA) and tc_conv_dgrad (x the
+//             previous layer's ReLU mask; not for layer 0); tc_wgrad_reduce
+//             sums all partials in a fixed order (deterministic, no float
+//             atomics) and the loss (loss_final's order).
 //  sgd        w = w - fl32(lr) * g without contraction (:327-328), skipped
 //             once a non-finite loss was seen (the reference raises before
 //             that update), so an epoch runs without host round trips.
@@ -462,14 +463,16 @@ TcPlan tc_plan(const void* kern, int need, int cols) {
 
 template <int CI, int CO, bool kHead>
 bool launch_fwd_tc(const float* x, const int32_t* idx, int m, int hi, int wi, const float* net,
-                   const uint8_t* bimg, int ob, float* y, float* logit, cudaStream_t st) {
+                   const uint8_t* bimg, int ob, float* y, float* logit, cudaStream_t st,
+                   const ttc::PackJob* pack = nullptr) {
   using C = ttc::FwdCfg<CI, CO>;
   auto k = ttc::tc_conv_fwd<CI, CO, kHead>;
   const TcPlan p = tc_plan(reinterpret_cast<const void*>(k), C::SMEM, C::COLS);
   if (!p.slots) return false;
   const int64_t tiles = int64_t(m) * (hi - 2) * ((wi - 2 + ttc::kTOut - 1) / ttc::kTOut);
   k<<<unsigned(tiles < p.slots ? tiles : p.slots), ttc::kThreads, p.dyn, st>>>(
-      x, idx, m, hi, wi, bimg, net + ob, kHead ? net + kOffW3 : nullptr, y, logit);
+      x, idx, m, hi, wi, bimg, net + ob, kHead ? net + kOffW3 : nullptr, y, logit,
+      pack ? *pack : ttc::PackJob{}, pack ? 1 : 0);
   return true;
 }
 
@@ -536,9 +539,8 @@ int eca_edgenet_forward(const float* x, const int32_t* index, int m, int h, int 
   if (!train_simt()) {   // tcgen05: three conv launches, the head fused into the last
     const ttc::PackJob P{net + kOffW0, net + kOffW1, net + kOffW2, ws + L.bimg[0], ws + L.bimg[1],
                          ws + L.bimg[2], ws + L.bimg[3], ws + L.bimg[4]};
-    ttc::tc_pack_weights<<<dim3((ttc::kPackMax + ttc::kPackThreads - 1) / ttc::kPackThreads, 5),
-                           ttc::kPackThreads, 0, st>>>(P);
-    if (!launch_fwd_tc<5, 8, false>(x, index, m, h, w, net, ws + L.bimg[0], kOffB0, a1, nullptr, st) ||
+    // layer 0 builds its own weight operand and packs the other four images
+    if (!launch_fwd_tc<5, 8, false>(x, index, m, h, w, net, ws + L.bimg[0], kOffB0, a1, nullptr, st, &P) ||
         !launch_fwd_tc<8, 16, false>(a1, nullptr, m, h - 2, w - 2, net, ws + L.bimg[1], kOffB1, a2, nullptr,
                                      st) ||
         !launch_fwd_tc<16, 32, true>(a2, nullptr, m, h - 4, w - 4, net, ws + L.bimg[2], kOffB2, a3, logit, st))
@@ -575,7 +577,7 @@ int eca_edgenet_backward(const float* x, const float* targets, const int32_t* in
                                                        f(L.dlog), f(L.d3), lpart, f(L.hpart));
   else
     loss_kernel<<<L.nlblk, kLossThreads, 0, st>>>(f(L.logit), targets, index, m, plane, f(L.dlog), lpart);
-  loss_final<<<1, 256, 0, st>>>(lpart, L.nlblk, n, out_loss, diverged);
+  if (!tc) loss_final<<<1, 256, 0, st>>>(lpart, L.nlblk, n, out_loss, diverged);   // (tc: in the reduction)
   if (!out_grads) return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;   // loss only
   if (tc) {   // tcgen05 weight / input gradients, one fixed-order reduction
     float* tp0 = f(L.tcpart);
@@ -599,7 +601,12 @@ int eca_edgenet_backward(const float* x, const float* targets, const int32_t* in
               out_grads + kOffW0, out_grads + kOffB0};
     for (const auto& l : R.l)
       if (l.G == 0) return ECA_ERR_CUDA;
-    ttc::tc_wgrad_reduce<<<dim3(blocks(ttc::WgCfg<16, 32, 3>::R * 32, 32), 4), dim3(32, ttc::kRedG), 0, st>>>(R);
+    R.lpart = lpart;
+    R.nlblk = L.nlblk;
+    R.n = n;
+    R.out_loss = out_loss;
+    R.flag = diverged;
+    ttc::tc_wgrad_reduce<<<dim3(blocks(ttc::WgCfg<16, 32, 3>::R * 32, 32), 5), dim3(32, ttc::kRedG), 0, st>>>(R);
     return cudaPeekAtLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
   }
   // head (1x1, 32 -> 1)

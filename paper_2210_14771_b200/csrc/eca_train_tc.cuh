@@ -143,13 +143,77 @@ struct FwdCfg {
   static constexpr int B_BYTES = N * KP * 4;
   static constexpr int A_REGION = cmax(3 * kP * A_BYTES, 2 * CO * kXb * 4);   // + exchange after the MMAs
   static constexpr int SMEM = A_REGION + 3 * kP * B_BYTES;
-  static constexpr int BIMG = 3 * kP * B_BYTES;  // the packed B operands (tc_pack_weights)
+  static constexpr int BIMG = 3 * kP * B_BYTES;  // the packed B operands (pack_b_fwd / pack_slice)
   // accumulators: one per ky (N = 96), or ky 0-1 and ky 2 (N = 48: 128 TMEM
   // columns, so four CTAs fit an SM's TMEM)
   static constexpr int NACC = N > 48 ? 3 : 2;
   static constexpr int COLS = tmem_cols(NACC * N);
   static constexpr int acc(int ky) { return NACC == 3 ? ky : (ky < 2 ? 0 : 1); }
 };
+
+template <int CI, int CO>
+struct DgCfg {
+  static constexpr int KP = CO;                  // K: output channels (16 or 32)
+  static_assert(CO % 8 == 0, "K steps of 8");
+  static constexpr int NB = up16(CI);
+  static constexpr int N = 3 * NB;
+  static constexpr int SBO = KP / 4 * 128;
+  static constexpr int A_BYTES = kT * KP * 4;
+  static constexpr int B_BYTES = N * KP * 4;
+  static constexpr int XB = 2 * CI * kXb * 4;
+  static constexpr int NACC = KP / 8 < 2 ? KP / 8 : 2;   // K steps alternate between two accumulators
+  static constexpr int COLS = tmem_cols(NACC * N);
+  // ky rows of dy that exist for some output row: min(3, ho) A slots
+  static constexpr int BIMG = 3 * kP * B_BYTES;  // the packed B operands (pack_b_fwd / pack_slice)
+  static int a_region(int ho) { return cmax((ho < 3 ? ho : 3) * kP * A_BYTES, XB); }
+  static int smem(int ho) { return a_region(ho) + 3 * kP * B_BYTES; }
+};
+
+// ------------------------------------------------------- packed B operands --
+// The conv kernels' B operands (weights as K-major TF32 pieces) are built once
+// per forward (by the layer-0 forward's CTAs, pack_slice) into the workspace,
+// in their shared-memory layout, and copied by every CTA of the later kernels
+// (instead of each CTA rebuilding them).
+// forward: B[ky][piece] row n = kx * NB + o, K = c; dgrad: row n = kx * NB + c, K = o.
+template <int CI, int CO>
+ECA_DEV void pack_b_fwd(uint8_t* dst, const float* __restrict__ wk, int i) {
+  using C = FwdCfg<CI, CO>;
+  if (i >= 3 * C::N * C::KP) return;
+  const int c = i % C::KP, n = (i / C::KP) % C::N, ky = i / (C::KP * C::N);
+  const int kx = n / C::NB, o = n % C::NB;
+  const float v = (o < CO && c < CI) ? wk[((o * CI + c) * 3 + ky) * 3 + kx] : 0.f;
+  st_pieces1(dst + ky * kP * C::B_BYTES, C::B_BYTES, kmaj_off(n, c, C::SBO), v);
+}
+template <int CI, int CO>
+ECA_DEV void pack_b_dgrad(uint8_t* dst, const float* __restrict__ wk, int i) {
+  using C = DgCfg<CI, CO>;
+  if (i >= 3 * C::N * C::KP) return;
+  const int o = i % C::KP, n = (i / C::KP) % C::N, ky = i / (C::KP * C::N);
+  const int kx = n / C::NB, c = n % C::NB;
+  const float v = c < CI ? wk[((o * CI + c) * 3 + ky) * 3 + kx] : 0.f;
+  st_pieces1(dst + ky * kP * C::B_BYTES, C::B_BYTES, kmaj_off(n, o, C::SBO), v);
+}
+struct PackJob {
+  const float *w0, *w1, *w2;   // OIHW kernels of the three 3x3 layers
+  uint8_t *f0, *f1, *f2, *d2, *d1;
+};
+// the forward-1/2 and dgrad-2/1 images: slice `part` of `parts` of their
+// elements (the layer-0 forward kernel's CTAs write them between them, so no
+// separate packing launch is needed; stream order makes them visible to the
+// later kernels)
+ECA_DEV void pack_slice(const PackJob& J, int part, int parts) {
+  constexpr int e1 = 3 * FwdCfg<8, 16>::N * FwdCfg<8, 16>::KP, e2 = 3 * FwdCfg<16, 32>::N * FwdCfg<16, 32>::KP;
+  constexpr int e3 = 3 * DgCfg<16, 32>::N * DgCfg<16, 32>::KP, e4 = 3 * DgCfg<8, 16>::N * DgCfg<8, 16>::KP;
+  constexpr int total = e1 + e2 + e3 + e4;
+  const int lo = int(int64_t(total) * part / parts), hi = int(int64_t(total) * (part + 1) / parts);
+  for (int g = lo + int(threadIdx.x); g < hi; g += blockDim.x) {
+    if (g < e1) pack_b_fwd<8, 16>(J.f1, J.w1, g);
+    else if (g < e1 + e2) pack_b_fwd<16, 32>(J.f2, J.w2, g - e1);
+    else if (g < e1 + e2 + e3) pack_b_dgrad<16, 32>(J.d2, J.w2, g - e1 - e2);
+    else pack_b_dgrad<8, 16>(J.d1, J.w1, g - e1 - e2 - e3);
+  }
+}
+
 
 // x: [*][CI][hi][wi] (sample idx[b] when idx) -> y: [m][CO][hi-2][wi-2].
 // Persistent CTAs (B, the biases and TMEM set up once) loop over tiles (b, oy,
@@ -161,7 +225,8 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
                                                         int wi, const uint8_t* __restrict__ bimg,
                                                         const float* __restrict__ bias,
                                                         const float* __restrict__ head, float* __restrict__ y,
-                                                        float* __restrict__ logit) {
+                                                        float* __restrict__ logit, const PackJob pack,
+                                                        int do_pack) {
   using C = FwdCfg<CI, CO>;
   static_assert(!kHead || CO == 32, "head after the 32-channel layer");
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -179,7 +244,12 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
     mbar_init(&bar, 1);
     fence_barrier_init();
   }
-  copy16(B, bimg, C::BIMG);   // B[ky]: row n = kx * NB + o, K = c (pack_b_fwd)
+  if (do_pack) {   // layer 0: its own B from the weights, and a slice of the other images
+    for (int i = tid; i < 3 * C::N * C::KP; i += kThreads) pack_b_fwd<CI, CO>(B, pack.w0, i);
+    pack_slice(pack, blockIdx.x, gridDim.x);
+  } else {
+    copy16(B, bimg, C::BIMG);   // B[ky]: row n = kx * NB + o, K = c (pack_b_fwd)
+  }
   if (tid < CO) sbias[tid] = bias[tid];
   if (kHead) {
     if (tid < 32) sw3[tid] = head[tid];
@@ -275,23 +345,6 @@ __global__ void __launch_bounds__(kThreads) tc_conv_fwd(const float* __restrict_
 }
 
 // -------------------------------------------------------------------- dgrad --
-template <int CI, int CO>
-struct DgCfg {
-  static constexpr int KP = CO;                  // K: output channels (16 or 32)
-  static_assert(CO % 8 == 0, "K steps of 8");
-  static constexpr int NB = up16(CI);
-  static constexpr int N = 3 * NB;
-  static constexpr int SBO = KP / 4 * 128;
-  static constexpr int A_BYTES = kT * KP * 4;
-  static constexpr int B_BYTES = N * KP * 4;
-  static constexpr int XB = 2 * CI * kXb * 4;
-  static constexpr int NACC = KP / 8 < 2 ? KP / 8 : 2;   // K steps alternate between two accumulators
-  static constexpr int COLS = tmem_cols(NACC * N);
-  // ky rows of dy that exist for some output row: min(3, ho) A slots
-  static constexpr int BIMG = 3 * kP * B_BYTES;  // the packed B operands (tc_pack_weights)
-  static int a_region(int ho) { return cmax((ho < 3 ? ho : 3) * kP * A_BYTES, XB); }
-  static int smem(int ho) { return a_region(ho) + 3 * kP * B_BYTES; }
-};
 
 // dx: [m][CI][hi][wi] = (sum_{o,ky,kx} dy[o][y-ky][x-kx] w[o][c][ky][kx]) * (xin > 0);
 // dy: [m][CO][hi-2][wi-2]; persistent CTAs loop over tiles (b, y, 126 columns)
@@ -397,48 +450,6 @@ __global__ void __launch_bounds__(kThreads) tc_conv_dgrad(const float* __restric
   }
   tmem_release(tmem, C::COLS);
 }
-
-// ------------------------------------------------------- packed B operands --
-// The conv kernels' B operands (weights as K-major TF32 pieces) are built once
-// per forward by tc_pack_weights into the workspace, in their shared-memory
-// layout, and copied by every CTA (instead of each CTA rebuilding them).
-// forward: B[ky][piece] row n = kx * NB + o, K = c; dgrad: row n = kx * NB + c, K = o.
-template <int CI, int CO>
-ECA_DEV void pack_b_fwd(uint8_t* dst, const float* __restrict__ wk, int i) {
-  using C = FwdCfg<CI, CO>;
-  if (i >= 3 * C::N * C::KP) return;
-  const int c = i % C::KP, n = (i / C::KP) % C::N, ky = i / (C::KP * C::N);
-  const int kx = n / C::NB, o = n % C::NB;
-  const float v = (o < CO && c < CI) ? wk[((o * CI + c) * 3 + ky) * 3 + kx] : 0.f;
-  st_pieces1(dst + ky * kP * C::B_BYTES, C::B_BYTES, kmaj_off(n, c, C::SBO), v);
-}
-template <int CI, int CO>
-ECA_DEV void pack_b_dgrad(uint8_t* dst, const float* __restrict__ wk, int i) {
-  using C = DgCfg<CI, CO>;
-  if (i >= 3 * C::N * C::KP) return;
-  const int o = i % C::KP, n = (i / C::KP) % C::N, ky = i / (C::KP * C::N);
-  const int kx = n / C::NB, c = n % C::NB;
-  const float v = c < CI ? wk[((o * CI + c) * 3 + ky) * 3 + kx] : 0.f;
-  st_pieces1(dst + ky * kP * C::B_BYTES, C::B_BYTES, kmaj_off(n, o, C::SBO), v);
-}
-struct PackJob {
-  const float *w0, *w1, *w2;   // OIHW kernels of the three 3x3 layers
-  uint8_t *f0, *f1, *f2, *d2, *d1;
-};
-constexpr int kPackThreads = 256;
-// blockIdx.y: forward 0, 1, 2, dgrad 2, 1; one element per thread
-__global__ void __launch_bounds__(kPackThreads) tc_pack_weights(const __grid_constant__ PackJob J) {
-  const int i = blockIdx.x * kPackThreads + threadIdx.x;
-  switch (blockIdx.y) {
-    case 0: pack_b_fwd<5, 8>(J.f0, J.w0, i); break;
-    case 1: pack_b_fwd<8, 16>(J.f1, J.w1, i); break;
-    case 2: pack_b_fwd<16, 32>(J.f2, J.w2, i); break;
-    case 3: pack_b_dgrad<16, 32>(J.d2, J.w2, i); break;
-    default: pack_b_dgrad<8, 16>(J.d1, J.w1, i); break;
-  }
-}
-constexpr int kPackMax = cmax(cmax(3 * FwdCfg<16, 32>::N * FwdCfg<16, 32>::KP, 3 * DgCfg<16, 32>::N * 32),
-                              3 * FwdCfg<5, 8>::N * FwdCfg<5, 8>::KP);
 
 // -------------------------------------------------------------------- wgrad --
 template <int CI, int CO, int KS>
@@ -632,10 +643,38 @@ struct WgLayer {
 };
 struct WgReduceJob {
   WgLayer l[4];
+  // blockIdx.y == 4: the mean loss from the loss kernel's block partials, as
+  // loss_final does (same order), and the non-finite flag
+  const double* lpart;
+  int nlblk;
+  int64_t n;
+  double* out_loss;
+  int32_t* flag;
 };
 constexpr int kRedG = 32;
 __global__ void __launch_bounds__(32 * kRedG) tc_wgrad_reduce(const __grid_constant__ WgReduceJob J) {
   __shared__ float red[kRedG][32];
+  if (blockIdx.y == 4) {   // the loss (one block; loss_final's 256-thread order)
+    if (blockIdx.x != 0) return;
+    __shared__ double lred[256];
+    const int t = threadIdx.y * 32 + threadIdx.x;
+    if (t < 256) {
+      double v = 0.0;
+      for (int i = t; i < J.nlblk; i += 256) v += J.lpart[i];
+      lred[t] = v;
+    }
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+      if (t < o) lred[t] += lred[t + o];
+      __syncthreads();
+    }
+    if (t == 0) {
+      const double loss = lred[0] / double(J.n);
+      *J.out_loss = loss;
+      if (!isfinite(loss) && J.flag) *J.flag = 1;
+    }
+    return;
+  }
   const WgLayer& L = J.l[blockIdx.y];
   const int n = L.R * L.CO, i = blockIdx.x * 32 + threadIdx.x, g0 = threadIdx.y;
   if (blockIdx.x * 32 >= n) return;
