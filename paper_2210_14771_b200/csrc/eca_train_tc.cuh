@@ -26,9 +26,10 @@
 // accumulation truncates at every MMA, relative to the running sum, so long
 // chains in one TMEM accumulator lose bits (measured: 8e-7 relative logit
 // error with one accumulator per output, tools/train_err.py); every kernel
-// therefore keeps chains short -- an accumulator per ky (forward), per K step
-// (dgrad), per K step of each 32-position unit (wgrad) -- and sums those in
-// FP32 registers with round-to-nearest.  The reference's sgemm also
+// therefore keeps chains short -- an accumulator per ky (forward, N = 96) or
+// per ky pair (N = 48), two alternating over the K steps (dgrad), one per K
+// step of each 32-position unit (wgrad) -- and sums those in FP32 registers
+// with round-to-nearest.  The reference's sgemm also
 // reassociates, so results agree to FP32 rounding level, not bitwise
 // (tolerances in tests/test_gpu_train.py).
 #pragma once
@@ -46,7 +47,10 @@ constexpr int kWgK = 32;         // positions per weight-gradient unit
 constexpr int kWgCtas = 1024;    // most weight-gradient CTAs (partials) per layer
 
 // FP32 operands as kP TF32 pieces (v = p0 + p1 (+ p2), each the TF32 rounding
-// of the remainder) and the products of the pieces summed up to order kP - 1
+// of the remainder) and the products of the pieces summed up to order kP - 1.
+// (ECA_TC_PIECES=3 / ECA_TC_LOLO=1: experiment builds; measured no more
+// accurate than the default -- the accumulation, not the split, sets the
+// error; K7.)
 #ifndef ECA_TC_PIECES
 #define ECA_TC_PIECES 2
 #endif
@@ -54,7 +58,6 @@ constexpr int kWgCtas = 1024;    // most weight-gradient CTAs (partials) per lay
 #define ECA_TC_LOLO 0
 #endif
 constexpr int kP = ECA_TC_PIECES;
-constexpr int kTerms = kP == 3 ? 6 : (ECA_TC_LOLO ? 4 : 3);
 static_assert(kP == 2 || kP == 3, "2 or 3 pieces");
 
 ECA_DEV void st_pieces(uint8_t* base, int pstride, int off, float4 v) {
@@ -95,7 +98,7 @@ ECA_DEV void mma_terms(uint32_t tmem, uint32_t a, int astride, int sboa, uint32_
 constexpr int up8(int c) { return (c + 7) / 8 * 8; }
 constexpr int up16(int c) { return (c + 15) / 16 * 16; }
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
-#ifndef ECA_TMEM_ALL
+#ifndef ECA_TMEM_ALL   // diagnostics: every kernel takes all 512 columns (one CTA per SM's TMEM)
 #define ECA_TMEM_ALL 0
 #endif
 constexpr int tmem_cols(int n) {
