@@ -44,8 +44,19 @@ constexpr int kSlots = 8;
 #define ECA_STATIC_ROUNDS 1
 #endif
 constexpr int kStaticRounds = ECA_STATIC_ROUNDS;   // items per warp assigned before tickets
-constexpr int kRefineMin = 8;    // step C: refine lane-chunk bounds above this many
-constexpr float kEarlyD = 0.1f;   // D_up(carry) level that triggers the early LB (gray ~37)
+// Scheduling knobs (the results do not depend on them: they decide when the
+// exact bound tests run, not what they conclude); r02 sweep, tools/time_pipe.py
+// + tools/prof_zc.py: early LB at D_up 0.05 / 0.1 / 0.2 / 0.35 / 0.6 / 1.01 ->
+// 28.1 / 27.6 / 27.3 / 27.3 / 27.3 / 42.3 us per step; refine above 4 / 8 / 16
+// -> 27.8 / 27.6 / 27.5; 0.35 + 16: 27.2 us and 3 % fewer zero-copy bytes.
+#ifndef ECA_REFINE_MIN
+#define ECA_REFINE_MIN 16
+#endif
+#ifndef ECA_EARLY_D
+#define ECA_EARLY_D 0.35f
+#endif
+constexpr int kRefineMin = ECA_REFINE_MIN;   // step C: refine lane-chunk bounds above this many
+constexpr float kEarlyD = ECA_EARLY_D;       // D_up(carry) level that triggers the early LB (gray ~28)
 
 // one survivor: column, preceding sum and the 9 neighbourhood sums (rows h-1..h+1)
 struct SurvSlot {
