@@ -37,7 +37,10 @@ namespace eca {
 
 constexpr int kPx = 8;        // pixels per thread
 constexpr int kTBins = 800;   // tanh-term bins: float(|3g|^2) exponent (25) x 5 mantissa bits
-constexpr int kABins = 128;   // angle-term bins over pseudo-angle [0, 2]
+#ifndef ECA_ABINS
+#define ECA_ABINS 128
+#endif
+constexpr int kABins = ECA_ABINS;   // angle-term bins over pseudo-angle [0, 2]
 constexpr int kDBins = 768;   // darkness-term table over preceding sums 0..765
 // Relative outward pad of every FP32 bound: not a constant but the modelled
 // error bound of the config (StripJob::pad = eca_prefilter_bound, >= 4x the
