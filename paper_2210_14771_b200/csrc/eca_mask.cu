@@ -8,6 +8,8 @@
 //
 // Crop: crop_augment's rectangle (dataset.py:151-187) evaluated in FP64 on the
 // device, then a coalesced row copy into a packed HWC buffer.
+#include <cstdlib>
+
 #include "eca_common.cuh"
 
 using namespace eca;
@@ -114,6 +116,43 @@ __global__ void __launch_bounds__(256) mask_kernel(const EcaFitRecord* fits, int
   }
 }
 
+// Packed masks (frame stride H*W, W % 16 == 0, 16-byte aligned): the rows of
+// the batch are one contiguous byte array.  A CTA takes kFlatRows rows at a
+// time: one warp finds their intervals (FP64, as mask_kernel) into shared
+// memory, then all its threads stream the rows' bytes as one span of 16-byte
+// chunks (row of chunk c = c / (W / 16) by a multiply-high with the host's
+// magic), so every warp writes long runs and no per-row loop or shuffle remains.
+constexpr int kFlatRows = 32;
+__global__ void __launch_bounds__(256) mask_kernel_flat(const EcaFitRecord* fits, int batch, int H, int W,
+                                                        uint8_t* out, uint32_t cpr_magic) {
+  __shared__ int2 ivl[kFlatRows];
+  const int cpr = W >> 4;   // 16-byte chunks per row
+  const int64_t n_rows = int64_t(batch) * H;
+  for (int64_t r0 = int64_t(blockIdx.x) * kFlatRows; r0 < n_rows; r0 += int64_t(gridDim.x) * kFlatRows) {
+    const int nr = int(n_rows - r0 < kFlatRows ? n_rows - r0 : kFlatRows);
+    if (threadIdx.x < nr) {
+      const int64_t my = r0 + threadIdx.x;
+      const int b = int(my / H), y = int(my - int64_t(b) * H);
+      int lo = 0, hi = W - 1;
+      const EcaFitRecord f = fits[b];
+      if (f.status == ECA_ACCEPTED) {
+        const double dy = sub_rn(double(y), f.cy);
+        row_interval(f.cx, mul_rn(dy, dy), mul_rn(f.r, f.r), W, lo, hi);
+      }
+      ivl[threadIdx.x] = make_int2(lo, hi);
+    }
+    __syncthreads();
+    uint4* base = reinterpret_cast<uint4*>(out + r0 * W);
+    const int n16 = nr * cpr;
+    for (int c = threadIdx.x; c < n16; c += blockDim.x) {
+      const int row = int(__umulhi(uint32_t(c), cpr_magic));   // c / cpr (c < 2^16 here)
+      const int2 iv = ivl[row];
+      base[c] = mask16((c - row * cpr) << 4, iv.x, iv.y);
+    }
+    __syncthreads();
+  }
+}
+
 ECA_DEV bool contains_pt(double x, double y, double cx, double cy, double r) {
   const double dx = sub_rn(x, cx), dy = sub_rn(y, cy);
   return add_rn(mul_rn(dx, dx), mul_rn(dy, dy)) <= mul_rn(r, r);
@@ -194,6 +233,15 @@ __global__ void __launch_bounds__(256) crop_copy_kernel(const uint8_t* frames, i
   }
 }
 
+// ECA_MASK_ROWS=1: always the per-row kernel (comparison runs)
+bool getenv_mask_rows() {
+  static const bool v = [] {
+    const char* e = std::getenv("ECA_MASK_ROWS");
+    return e && *e == '1';
+  }();
+  return v;
+}
+
 }  // namespace
 
 extern "C" int eca_draw_mask(const EcaFitRecord* fits, int batch, int height, int width,
@@ -204,11 +252,21 @@ extern "C" int eca_draw_mask(const EcaFitRecord* fits, int batch, int height, in
   if (batch == 0) return ECA_OK;
   if (!fits || !out) return ECA_ERR_ARG;
   const int64_t rows = int64_t(batch) * height;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool flat = !getenv_mask_rows() && width % 16 == 0 && out_frame_stride == int64_t(height) * width &&
+                    (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (flat) {   // one contiguous span of rows
+    const uint32_t cpr = uint32_t(width >> 4);
+    const uint32_t magic = uint32_t((0xFFFFFFFFull + cpr) / cpr);   // ceil(2^32 / cpr): exact for c < 2^16
+    const int64_t blocks64 = (rows + kFlatRows - 1) / kFlatRows;
+    const int cap = 148 * ECA_MASK_BPS * 2;
+    mask_kernel_flat<<<int(blocks64 < cap ? blocks64 : cap), 256, 0, st>>>(fits, batch, height, width, out,
+                                                                           magic);
+    return cudaGetLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
+  }
   const int64_t blocks64 = (rows + 255) / 256;   // 8 warps x 32 rows per CTA pass
   const int blocks = int(blocks64 < 148 * ECA_MASK_BPS ? blocks64 : 148 * ECA_MASK_BPS);
-  mask_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(fits, batch, height,
-                                                                          width, out,
-                                                                          out_frame_stride);
+  mask_kernel<<<blocks, 256, 0, st>>>(fits, batch, height, width, out, out_frame_stride);
   return cudaGetLastError() == cudaSuccess ? ECA_OK : ECA_ERR_CUDA;
 }
 

@@ -515,6 +515,19 @@ def test_mask_bit_exact_vs_oracle():
     assert np.array_equal(odd, orc.disk_mask(50.3, 20.7, 17.0, 41, 101))
 
 
+def test_mask_1080p_flat_path_bit_exact():
+    """Packed 1080p masks take the span writer (W % 16 == 0): a batch of 9
+    frames (rows of consecutive frames share a CTA's span), against the oracle."""
+    circles = [eb.Circle(958.88, 545.03, 759.54), eb.Circle(959.5, 539.5, 1200.0),
+               eb.Circle(0.5, 0.5, 300.25), eb.Circle(1919.0, 1079.0, 77.7), eb.Circle(960.0, -500.0, 600.0),
+               eb.Circle(-10.0, 540.0, 9.0), eb.Circle(960.0, 540.0, 0.75), eb.Circle(300.1, 900.9, 410.4)]
+    areas = [eb.CircularArea(c, 1.0) for c in circles] + [eb.FULL_FRAME]
+    masks = eb.draw_mask(areas, 1080, 1920).cpu().numpy()
+    for m, c in zip(masks, circles):
+        assert np.array_equal(m, orc.disk_mask(c.cx, c.cy, c.r, 1080, 1920)), c
+    assert masks[-1].all()
+
+
 def test_crop_bounds_match_reference():
     fails = []
     for c in load_json("crops.json"):
