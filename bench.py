@@ -823,7 +823,7 @@ def label_leg(eb, dev, base) -> dict:
                       "1080p; decode-bound)",
             "value": round(len(anns) / dt, 1), "unit": "frames/s", "frames": len(anns),
             "circles": int(sum(a.area is not None for a in anns)),
-            "workers": max(1, min(32, (os.cpu_count() or 2) - 1)),
+            "workers": max(1, min(32, os.cpu_count() or 1)),
             "note": "PNG decode bound (PIL, ~45 ms per 1080p frame per core): the GPU estimate is <1 % of "
                     "the wall clock; the CPU port decodes on every core and estimates inline", "_dir": d}
 
